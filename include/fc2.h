@@ -1,0 +1,132 @@
+/*
+ * fc2.h -- C ABI of the B200-native FlashCommunication-V2 hot path.
+ *
+ * Plain C: pointers, sizes and int status codes; no torch / C++ types.  All
+ * compute entry points are asynchronous on the caller's CUDA stream (passed
+ * as `void* stream`, a cudaStream_t), never allocate, never synchronize, and
+ * report data-dependent errors through a caller-owned device int32 word
+ * (`dev_err`, bit mask FC2_ERR_*) that the host checks when it wants to.
+ *
+ * Each entry point names the reference interface it replaces (paths relative
+ * to /root/reference/pkg/src/qcomm).  The reference is a pure Python+numpy
+ * package with no FFI; the binding a maintainer would add is the ctypes stub
+ * in INTEGRATION.md, which is exactly what paper_2508_03760_b200/_lib.py does.
+ */
+#ifndef FC2_H
+#define FC2_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (map onto errors.py:4-21) ---------------------------- */
+#define FC2_OK              0
+#define FC2_ECONFIG        -1  /* ConfigError      */
+#define FC2_EDATA          -2  /* DataError        */
+#define FC2_EFORMAT        -3  /* DecodeFormatError */
+#define FC2_ENOTAPPLICABLE -4  /* NotApplicableError */
+#define FC2_ECUDA          -5  /* CUDA runtime failure (fc2_last_error has text) */
+
+/* ---- device error word bits (dev_err) ---------------------------------- */
+#define FC2_ERR_NONFINITE   1  /* encode saw NaN/inf    -> DataError (codec.py:482-483) */
+#define FC2_ERR_SPIKE_INDEX 2  /* decode spike index out of range -> DecodeFormatError (codec.py:555-558) */
+#define FC2_ERR_LOG2_TIE    4  /* INT_LOG: log2(scale)*theta within 1e-9 of a .5 tie (parity warning) */
+#define FC2_ERR_TIMEOUT     8  /* cross-rank flag wait timed out */
+#define FC2_ERR_CODE_RANGE 16  /* pack: code outside [0, 2^bits) -> CodeRangeError (codec.py:216-217) */
+
+/* ---- element types ----------------------------------------------------- */
+#define FC2_BF16 0
+#define FC2_F32  1
+#define FC2_F64  2
+
+/* QuantConfig (codec.py:55-90).  scheme: 0 RTN, 1 SPIKE_RESERVING.
+ * scale_encoding: 0 BF16, 1 INT_LOG.  chunk_size is a host-side notion: every
+ * call below passes the chunk length `n` explicitly. */
+typedef struct fc2_config {
+    int32_t bitwidth;
+    int32_t group_size;
+    int32_t scheme;
+    int32_t scale_encoding;
+    int32_t theta;
+} fc2_config;
+
+/* Validate a config (codec.py:71-86).  Returns FC2_OK or FC2_ECONFIG. */
+int fc2_check_config(const fc2_config* cfg);
+
+/* Payload bytes for n elements: planes + metadata (codec.py:428-432). */
+int fc2_footprint(const fc2_config* cfg, int64_t n, int64_t* nbytes);
+
+/* Byte offset of bit-split plane u / of the metadata section inside one
+ * chunk payload of n elements (R9-R11; codec.py:129,518). */
+int64_t fc2_plane_offset(const fc2_config* cfg, int64_t n, int32_t unit);
+int64_t fc2_meta_offset(const fc2_config* cfg, int64_t n);
+
+/* Must be called once per process before INT_LOG work: the 256-entry table
+ * exp2(si/theta), si = -128..127, computed on the host by numpy so the
+ * device scale values are bit-identical to codec.py:468,542. */
+int fc2_set_intlog_table(int32_t theta, const double* table256);
+
+/* encode_chunk (codec.py:477-519) on device memory.
+ * x: n_valid elements of x_dtype; elements [n_valid, n) are encoded as +0.0
+ * (the zero padding of collectives.py:167-172).  n % group_size == 0.
+ * payload: fc2_footprint(n) bytes, 4-byte aligned (16 for full speed). */
+int fc2_encode(const fc2_config* cfg, const void* x, int32_t x_dtype, int64_t n_valid,
+               int64_t n, void* payload, int32_t* dev_err, void* stream);
+
+/* Batched encode: njobs independent chunks in one launch (the per-(src,shard)
+ * loop of collectives.py:280-290 and the per-block loop of :462-480).
+ * Host arrays of length njobs; njobs <= FC2_MAX_JOBS. */
+#define FC2_MAX_JOBS 256
+int fc2_encode_batch(const fc2_config* cfg, int32_t x_dtype, int32_t njobs,
+                     const void* const* xs, const int64_t* n_valid, const int64_t* n,
+                     void* const* payloads, int32_t* dev_err, void* stream);
+
+/* decode_chunk (codec.py:522-563): payload of n elements -> y (y_dtype).
+ * Only the first n_out <= n values are written (padding strip,
+ * collectives.py:185-186, :480).  FC2_F64 output is bit-identical to the
+ * reference's float64 result; FC2_F32 to its .astype(float32)
+ * (collectives.py:182); FC2_BF16 to bf16_round of that (:185-186). */
+int fc2_decode(const fc2_config* cfg, const void* payload, int64_t n, void* y,
+               int32_t y_dtype, int64_t n_out, int32_t* dev_err, void* stream);
+
+int fc2_decode_batch(const fc2_config* cfg, int32_t y_dtype, int32_t njobs,
+                     const void* const* payloads, const int64_t* n, void* const* ys,
+                     const int64_t* n_out, int32_t* dev_err, void* stream);
+
+/* Two-step AllReduce middle stage (collectives.py:291-311): decode nsrc
+ * payloads of the same shard (n elements each), accumulate in fp32 in source
+ * order from +0.0, re-encode the sum, and store the packed result to every
+ * one of ndst destinations (local buffer and/or peer pointers). */
+int fc2_reduce_requant(const fc2_config* cfg, int32_t nsrc, const void* const* src_payloads,
+                       int64_t n, int32_t ndst, void* const* dst_payloads, int32_t* dev_err,
+                       void* stream);
+
+/* Decode the N gathered shard payloads of a two-step AllReduce straight into
+ * the bf16/f32 output, stripping padding (collectives.py:313-314). */
+int fc2_gather_decode(const fc2_config* cfg, int32_t nshards, const void* const* shard_payloads,
+                      int64_t shard_len, void* y, int32_t y_dtype, int64_t n_out,
+                      int32_t* dev_err, void* stream);
+
+/* pack_codes / unpack_codes (codec.py:204-238): codes are int64 (range
+ * checked on device, FC2_ERR_CODE_RANGE), n % 8 == 0; planes is one
+ * contiguous buffer (plane 0, plane 1, ...). */
+int fc2_pack_codes(const int64_t* codes, int64_t n, int32_t bitwidth, uint8_t* planes,
+                   int32_t* dev_err, void* stream);
+int fc2_unpack_codes(const uint8_t* planes, int64_t n, int32_t bitwidth, uint8_t* codes,
+                     void* stream);
+
+/* bfloat16.py:16-36 on device arrays. */
+int fc2_f32_to_bf16_bits(const float* x, int64_t n, uint16_t* out, void* stream);
+int fc2_bf16_bits_to_f32(const uint16_t* x, int64_t n, float* out, void* stream);
+
+/* Diagnostics. */
+const char* fc2_last_error(void);
+int64_t fc2_launch_count(void);   /* kernels launched by this library so far */
+int fc2_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FC2_H */

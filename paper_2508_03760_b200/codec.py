@@ -1,0 +1,338 @@
+"""Drop-in codec API (reference: codec.py) on the B200 CUDA library.
+
+``encode_chunk`` / ``decode_chunk`` / ``pack_codes`` / ``unpack_codes`` keep
+the reference names, argument meaning and exceptions.  All arithmetic runs in
+libfc2.so on the GPU; host code only validates shapes and moves bytes.
+
+Two residencies:
+* host in, host out (the reference contract): numpy/list input, the returned
+  :class:`QuantizedChunk` holds ``bytes``; ``decode_chunk`` returns float64
+  numpy bit-identical to the reference.
+* device resident: a CUDA tensor input keeps the payload on the GPU
+  (``chunk.payload``); ``decode_chunk`` then returns a CUDA tensor
+  (float32 unless ``out_dtype`` says otherwise).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import struct
+
+import numpy as np
+import torch
+
+from . import _device, _lib
+from .config import (
+    GroupMeta,
+    QuantConfig,
+    ScaleEncoding,
+    Scheme,
+    bit_split,
+    default_group_size,
+    footprint_breakdown,
+    footprint_bytes,
+    meta_record_nbytes,
+    plane_sizes,
+)
+from .errors import ConfigError, DataError, DecodeFormatError
+
+CHUNK_MAGIC = b"FCV2"
+CHUNK_VERSION = 2
+_HEADER = struct.Struct("<4sBBHBBBI")  # codec.py:33-35
+HEADER_BYTES = _HEADER.size
+
+__all__ = [
+    "QuantConfig", "Scheme", "ScaleEncoding", "GroupMeta", "QuantizedChunk",
+    "bit_split", "default_group_size", "footprint_bytes", "footprint_breakdown",
+    "meta_record_nbytes", "encode_chunk", "decode_chunk", "pack_codes", "unpack_codes",
+    "parse_chunk", "encode_payload", "decode_payload",
+]
+
+
+class QuantizedChunk:
+    """Packed code planes + per-group metadata (codec.py:105-136).
+
+    Host chunks hold ``bytes``; device chunks hold one contiguous uint8 CUDA
+    tensor ``payload`` (planes in split order, then metadata) and materialize
+    ``planes``/``meta`` bytes lazily.
+    """
+
+    def __init__(self, config: QuantConfig, planes=None, meta=None, element_count: int = 0,
+                 *, payload: torch.Tensor | None = None):
+        self.config = config
+        self.element_count = int(element_count)
+        self._payload = payload
+        self._planes = None if planes is None else [bytes(p) for p in planes]
+        self._meta = None if meta is None else bytes(meta)
+        if payload is None and (self._planes is None or self._meta is None):
+            raise DataError("QuantizedChunk needs planes and meta, or a device payload")
+
+    # -- residency ---------------------------------------------------------
+    @property
+    def on_device(self) -> bool:
+        return self._payload is not None
+
+    @property
+    def payload(self) -> torch.Tensor:
+        """The payload as one uint8 CUDA tensor (uploads host bytes once)."""
+        if self._payload is None:
+            dev = _device.require_cuda()
+            buf = np.frombuffer(b"".join(self._planes) + self._meta, dtype=np.uint8)
+            self._payload = torch.from_numpy(buf.copy()).to(dev)
+        return self._payload
+
+    def _materialize(self):
+        raw = self._payload.cpu().numpy().tobytes()
+        sizes = plane_sizes(self.config, self.element_count)
+        planes, pos = [], 0
+        for s in sizes:
+            planes.append(raw[pos:pos + s])
+            pos += s
+        self._planes, self._meta = planes, raw[pos:]
+
+    @property
+    def planes(self) -> list[bytes]:
+        if self._planes is None:
+            self._materialize()
+        return self._planes
+
+    @property
+    def meta(self) -> bytes:
+        if self._meta is None:
+            self._materialize()
+        return self._meta
+
+    @property
+    def payload_nbytes(self) -> int:
+        if self._payload is not None:
+            return int(self._payload.numel())
+        return sum(len(p) for p in self._planes) + len(self._meta)
+
+    # -- wire format (host framing, codec.py:118-136) ------------------------
+    def to_bytes(self) -> bytes:
+        c = self.config
+        header = _HEADER.pack(CHUNK_MAGIC, CHUNK_VERSION, c.bitwidth, c.group_size,
+                              0 if c.scheme is Scheme.RTN else 1,
+                              0 if c.scale_encoding is ScaleEncoding.BF16 else 1,
+                              c.theta, self.element_count)
+        return header + b"".join(self.planes) + self.meta
+
+    @classmethod
+    def from_bytes(cls, buf: bytes) -> "QuantizedChunk":
+        chunk, consumed = parse_chunk(buf, 0)
+        if consumed != len(buf):
+            raise DecodeFormatError(f"{len(buf) - consumed} trailing bytes after chunk")
+        return chunk
+
+    def __eq__(self, other):
+        if not isinstance(other, QuantizedChunk):
+            return NotImplemented
+        return (self.config == other.config and self.element_count == other.element_count
+                and self.planes == other.planes and self.meta == other.meta)
+
+    def __repr__(self):
+        where = "device" if self.on_device else "host"
+        return (f"QuantizedChunk(bits={self.config.bitwidth}, g={self.config.group_size}, "
+                f"scheme={self.config.scheme.value}, n={self.element_count}, "
+                f"bytes={self.payload_nbytes}, {where})")
+
+
+def parse_chunk(buf: bytes, offset: int = 0) -> tuple[QuantizedChunk, int]:
+    """Parse one serialized chunk at ``offset``; returns (chunk, end) (codec.py:566-606)."""
+    if len(buf) - offset < HEADER_BYTES:
+        raise DecodeFormatError("buffer too short for chunk header")
+    magic, version, bits, gs, sch, enc, theta, count = _HEADER.unpack_from(buf, offset)
+    if magic != CHUNK_MAGIC:
+        raise DecodeFormatError(f"bad magic {magic!r}")
+    if version != CHUNK_VERSION:
+        raise DecodeFormatError(f"unsupported version {version}")
+    if sch not in (0, 1) or enc not in (0, 1):
+        raise DecodeFormatError("unknown scheme or scale-encoding byte")
+    try:
+        config = QuantConfig(bits, group_size=gs,
+                             scheme=Scheme.RTN if sch == 0 else Scheme.SPIKE_RESERVING,
+                             scale_encoding=ScaleEncoding.BF16 if enc == 0 else ScaleEncoding.INT_LOG,
+                             theta=theta, chunk_size=count if count > 0 else gs)
+    except ConfigError as exc:
+        raise DecodeFormatError(f"inconsistent chunk header: {exc}") from exc
+    if count % gs:
+        raise DecodeFormatError(f"element count {count} not a multiple of group size {gs}")
+    pos = offset + HEADER_BYTES
+    planes = []
+    for w in bit_split(bits):
+        size = count * w // 8
+        if len(buf) - pos < size:
+            raise DecodeFormatError("buffer truncated inside code planes")
+        planes.append(bytes(buf[pos:pos + size]))
+        pos += size
+    msize = (count // gs) * meta_record_nbytes(config)
+    if len(buf) - pos < msize:
+        raise DecodeFormatError("buffer truncated inside metadata")
+    meta = bytes(buf[pos:pos + msize])
+    return QuantizedChunk(config, planes, meta, count), pos + msize
+
+
+# ---------------------------------------------------------------------------
+# device-level entry points (tensors in, tensors out; no host sync unless checked)
+# ---------------------------------------------------------------------------
+
+
+def encode_payload(x: torch.Tensor, config: QuantConfig, n: int | None = None,
+                   out: torch.Tensor | None = None, err: torch.Tensor | None = None,
+                   check: bool = True) -> torch.Tensor:
+    """Encode a 1-D CUDA tensor (bf16/f32/f64) as one chunk of ``n`` elements
+    (``n >= x.numel()``, zero-padded) into a uint8 CUDA payload."""
+    dev = _device.require_cuda()
+    if config.int_log:
+        _device.ensure_intlog(config.theta, dev)
+    x = x.reshape(-1)
+    nv = x.numel()
+    n = nv if n is None else int(n)
+    nbytes = footprint_bytes(config, n)
+    if out is None:
+        out = torch.empty(nbytes, dtype=torch.uint8, device=x.device)
+    own_err = err is None
+    if own_err:
+        err = _device.new_err(x.device)
+    cfg = config.c_struct()
+    _lib.check(_lib.lib().fc2_encode(ctypes.byref(cfg), x.data_ptr(), _device.dtype_code(x), nv, n,
+                                     out.data_ptr(), err.data_ptr(), _device.stream_handle()))
+    if check and own_err:
+        _device.check_err(err)
+    return out
+
+
+def decode_payload(payload: torch.Tensor, config: QuantConfig, n: int,
+                   out_dtype: torch.dtype = torch.float32, n_out: int | None = None,
+                   out: torch.Tensor | None = None, err: torch.Tensor | None = None,
+                   check: bool = True) -> torch.Tensor:
+    """Decode a uint8 CUDA payload of ``n`` elements into ``out_dtype``
+    (bf16 / float32 / float64), keeping the first ``n_out`` values."""
+    dev = _device.require_cuda()
+    if config.int_log:
+        _device.ensure_intlog(config.theta, dev)
+    n_out = n if n_out is None else int(n_out)
+    if out is None:
+        out = torch.empty(n_out, dtype=out_dtype, device=payload.device)
+    own_err = err is None
+    if own_err:
+        err = _device.new_err(payload.device)
+    cfg = config.c_struct()
+    _lib.check(_lib.lib().fc2_decode(ctypes.byref(cfg), payload.data_ptr(), n, out.data_ptr(),
+                                     _device.dtype_code(out), n_out, err.data_ptr(),
+                                     _device.stream_handle()))
+    if check and own_err:
+        _device.check_err(err)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# reference-named API
+# ---------------------------------------------------------------------------
+
+
+def encode_chunk(values, config: QuantConfig) -> QuantizedChunk:
+    """Encode ``config.chunk_size`` values into a chunk (codec.py:477-519)."""
+    dev = _device.require_cuda()
+    device_in = _device.is_cuda_tensor(values)
+    if device_in:
+        x = values.detach()
+        if x.dtype not in (torch.bfloat16, torch.float32, torch.float64):
+            x = x.to(torch.float64)
+        if x.dim() != 1 or x.numel() != config.chunk_size:
+            raise DataError(f"expected {config.chunk_size} values, got shape {tuple(x.shape)}")
+        x = x.contiguous()
+    else:
+        arr = np.asarray(values) if not isinstance(values, torch.Tensor) else values.numpy()
+        if arr.ndim != 1 or arr.size != config.chunk_size:
+            raise DataError(f"expected {config.chunk_size} values, got shape {arr.shape}")
+        x = _device.to_device_values(arr, dev)
+    payload = encode_payload(x, config, config.chunk_size)
+    if device_in:
+        return QuantizedChunk(config, element_count=config.chunk_size, payload=payload)
+    chunk = QuantizedChunk(config, element_count=config.chunk_size, payload=payload)
+    chunk._materialize()
+    chunk._payload = None  # host residency: bytes only, like the reference
+    return chunk
+
+
+def decode_chunk(chunk: QuantizedChunk, out_dtype=None):
+    """Invert :func:`encode_chunk` (codec.py:522-563).
+
+    Host chunks decode to float64 numpy (bit-identical to the reference);
+    device chunks decode to a CUDA tensor (float32 unless ``out_dtype``)."""
+    config = chunk.config
+    n = chunk.element_count
+    if not chunk.on_device:
+        units = bit_split(config.bitwidth)
+        if len(chunk.planes) != len(units):
+            raise DecodeFormatError(f"expected {len(units)} planes, got {len(chunk.planes)}")
+        for p, w in zip(chunk.planes, units):
+            if len(p) != n * w // 8:
+                raise DecodeFormatError(f"plane of width {w} has {len(p)} bytes, expected {n * w // 8}")
+        if n % config.group_size:
+            raise DecodeFormatError("element count not a multiple of group size")
+        expected = (n // config.group_size) * meta_record_nbytes(config)
+        if len(chunk.meta) != expected:
+            raise DecodeFormatError(f"metadata has {len(chunk.meta)} bytes, expected {expected}")
+    dt = out_dtype or (torch.float32 if chunk.on_device else torch.float64)
+    y = decode_payload(chunk.payload, config, n, out_dtype=dt)
+    if chunk.on_device:
+        return y
+    chunk._payload = None
+    return y.cpu().numpy()
+
+
+def pack_codes(codes, bitwidth: int) -> list[bytes]:
+    """Pack integer codes into one byte plane per bit-split unit (codec.py:204-225)."""
+    from .errors import CodeRangeError
+
+    units = bit_split(bitwidth)
+    arr = np.asarray(codes)
+    if arr.ndim != 1:
+        raise DataError("codes must be one-dimensional")
+    if arr.size % 8 != 0:
+        raise DataError(f"code count {arr.size} must be a multiple of 8")
+    if arr.size == 0:
+        return [b"" for _ in units]
+    if arr.dtype.kind not in "iub":
+        arr = arr.astype(np.int64)
+    big = arr.astype(np.int64)
+    dev = _device.require_cuda()
+    if np.any(big != arr):
+        raise CodeRangeError(f"codes out of range for {bitwidth}-bit encoding")
+    d_codes = torch.from_numpy(np.ascontiguousarray(big)).to(dev)
+    n = arr.size
+    out = torch.empty(n * bitwidth // 8, dtype=torch.uint8, device=dev)
+    err = _device.new_err(dev)
+    _lib.check(_lib.lib().fc2_pack_codes(d_codes.data_ptr(), n, bitwidth, out.data_ptr(),
+                                         err.data_ptr(), _device.stream_handle()))
+    _device.check_err(err)
+    raw = out.cpu().numpy().tobytes()
+    planes, pos = [], 0
+    for w in units:
+        planes.append(raw[pos:pos + n * w // 8])
+        pos += n * w // 8
+    return planes
+
+
+def unpack_codes(planes, bitwidth: int, count: int) -> np.ndarray:
+    """Exact inverse of :func:`pack_codes` (codec.py:228-238)."""
+    units = bit_split(bitwidth)
+    if len(planes) != len(units):
+        raise DecodeFormatError(f"expected {len(units)} planes, got {len(planes)}")
+    for p, w in zip(planes, units):
+        if len(p) != count * w // 8:
+            raise DecodeFormatError(
+                f"plane of width {w} has {len(p)} bytes, expected {count * w // 8}")
+    if count == 0:
+        return np.zeros(0, dtype=np.uint8)
+    if count % 8:
+        raise DecodeFormatError("count must be a multiple of 8")
+    dev = _device.require_cuda()
+    buf = np.frombuffer(b"".join(bytes(p) for p in planes), dtype=np.uint8)
+    d_in = torch.from_numpy(buf.copy()).to(dev)
+    d_out = torch.empty(count, dtype=torch.uint8, device=dev)
+    _lib.check(_lib.lib().fc2_unpack_codes(d_in.data_ptr(), count, bitwidth, d_out.data_ptr(),
+                                           _device.stream_handle()))
+    return d_out.cpu().numpy()

@@ -1,0 +1,430 @@
+// fc2_codec.cu -- sm_100a kernels and the C ABI for the codec hot path.
+//
+//   k_encode_fast   encode_chunk (codec.py:477-519) for bf16/f32 input and
+//                   G in {32,64,128,256}: cp.async-staged, warp-tile = 1024
+//                   elements, lane = 32 consecutive elements.
+//   k_encode_gen    the same contract for any G (multiple of 8) and f64 input,
+//                   warp-per-group, exact float64.
+//   k_decode_fast   decode_chunk (codec.py:522-563), G % 32 == 0.
+//   k_decode_gen    elementwise decode for any G.
+//   k_reduce_fast   two-step middle stage (collectives.py:291-311): decode N
+//                   sources, fp32 rank-order accumulate, re-encode, push to N
+//                   destinations.
+//   k_reduce_gen    the same for any G.
+//   k_pack / k_unpack / bf16 casts: codec.py:204-238, bfloat16.py:16-36.
+#include <cstdarg>
+#include <cstdio>
+#include <utility>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "fc2_kernels.cuh"
+
+namespace fc2 {
+
+// ---------------------------------------------------------------------------
+// library state
+// ---------------------------------------------------------------------------
+
+thread_local std::string g_err;
+static int64_t g_launches = 0;
+static std::mutex g_mu;
+static double* g_lut = nullptr;          // 255 thetas x 256 entries
+static bool g_lut_ok[256] = {false};
+static int g_lut_dev = -1;
+
+int set_err(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_check(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_err(FC2_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  __atomic_add_fetch(&g_launches, 1, __ATOMIC_RELAXED);
+  return FC2_OK;
+}
+
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+
+#define FC2_BSWITCH(EXPR)                                                   \
+  switch (B) {                                                              \
+    case 2: return EXPR(2); case 3: return EXPR(3); case 4: return EXPR(4);  \
+    case 5: return EXPR(5); case 6: return EXPR(6); case 7: return EXPR(7);  \
+    case 8: return EXPR(8);                                                 \
+  }                                                                         \
+  return set_err(FC2_ECONFIG, "bad bitwidth %d", B);
+
+struct SumLoader {
+  const ReduceArgs* a;
+  DecCtx c;
+  __device__ double operator()(int64_t i) const {
+    float s = 0.0f;
+    for (int k = 0; k < a->nsrc; ++k) s = __fadd_rn(s, decode_elem32(a->src[k], i, c));
+    return (double)s;
+  }
+};
+
+__global__ void __launch_bounds__(256) k_reduce_gen(const __grid_constant__ ReduceArgs a) {
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  SumLoader ld;
+  ld.a = &a;
+  ld.c.n = a.n; ld.c.meta_off = a.n * a.B / 8; ld.c.B = a.B; ld.c.G = a.G; ld.c.sr = a.sr;
+  ld.c.intlog = a.intlog; ld.c.theta = a.theta; ld.c.lut = a.lut; ld.c.err = a.err;
+  EncCtx cx;
+  cx.n = a.n; cx.meta_off = a.n * a.B / 8; cx.intlog = a.intlog; cx.theta = a.theta; cx.lut = a.lut;
+  cx.err = a.err;
+  OutList o;
+  o.nd = a.ndst < 8 ? a.ndst : 8;
+  for (int d = 0; d < o.nd; ++d) o.p[d] = a.dst[d];
+  for (int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < a.total; g += nw)
+    generic_encode_group(ld, o, a.n, g, a.B, a.G, a.sr != 0, cx);
+}
+
+// ---------------------------------------------------------------------------
+// pack / unpack (codec.py:204-238) and bf16 casts (bfloat16.py:16-31)
+// ---------------------------------------------------------------------------
+
+__global__ void k_pack(const int64_t* codes, int64_t n, int B, uint8_t* planes, int32_t* err) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // run of 8 codes
+  if (r * 8 >= n) return;
+  uint32_t c[8];
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    int64_t v = codes[r * 8 + j];
+    if (v < 0 || v >= (1ll << B)) bad = true;
+    c[j] = (uint32_t)v;
+  }
+  if (bad) atomicOr(err, FC2_ERR_CODE_RANGE);
+  for (int u = 0; u < n_units(B); ++u) {
+    const int W = unit_w(B, u), O = unit_off(B, u);
+    uint64_t bits = 0;
+    for (int j = 0; j < 8; ++j) bits |= (uint64_t)((c[j] >> O) & ((1u << W) - 1u)) << (j * W);
+    uint8_t* p = planes + (n * O) / 8 + r * W;
+    for (int i = 0; i < W; ++i) p[i] = (uint8_t)(bits >> (8 * i));
+  }
+}
+
+__global__ void k_unpack(const uint8_t* planes, int64_t n, int B, uint8_t* codes) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r * 8 >= n) return;
+  uint32_t c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int u = 0; u < n_units(B); ++u) {
+    const int W = unit_w(B, u), O = unit_off(B, u);
+    const uint8_t* p = planes + (n * O) / 8 + r * W;
+    uint64_t bits = 0;
+    for (int i = 0; i < W; ++i) bits |= (uint64_t)p[i] << (8 * i);
+    for (int j = 0; j < 8; ++j) c[j] |= (uint32_t)((bits >> (j * W)) & ((1u << W) - 1u)) << O;
+  }
+  for (int j = 0; j < 8; ++j) codes[r * 8 + j] = (uint8_t)c[j];
+}
+
+__global__ void k_f32_to_bf16(const float* x, int64_t n, uint16_t* y) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = (uint16_t)bf16_bits(x[i]);
+}
+__global__ void k_bf16_to_f32(const uint16_t* x, int64_t n, float* y) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = bf16_val(x[i]);
+}
+
+static int enc_fast(int B, int dtype, bool sr, int G, const EncBatch& b, cudaStream_t st) {
+#define E(BB) launch_enc_fast<BB>(dtype, sr, G, b, st)
+  FC2_BSWITCH(E)
+#undef E
+}
+static int red_fast(int B, bool sr, int G, const ReduceArgs& a, cudaStream_t st) {
+#define E(BB) launch_red_fast<BB>(sr, G, a, st)
+  FC2_BSWITCH(E)
+#undef E
+}
+static int dec_fast(int B, int dtype, int64_t blocks, const DecBatch& b, cudaStream_t st) {
+#define E(BB) launch_dec_fast<BB>(dtype, blocks, b, st)
+  FC2_BSWITCH(E)
+#undef E
+}
+
+static bool fast_group(int G) { return G == 32 || G == 64 || G == 128 || G == 256; }
+
+// ---------------------------------------------------------------------------
+// host helpers
+// ---------------------------------------------------------------------------
+
+static int check_cfg(const fc2_config* c) {
+  if (!c) return set_err(FC2_ECONFIG, "null config");
+  if (c->bitwidth < 2 || c->bitwidth > 8) return set_err(FC2_ECONFIG, "bitwidth must be in [2, 8], got %d", c->bitwidth);
+  if (c->group_size <= 0 || c->group_size % 8) return set_err(FC2_ECONFIG, "group_size must be a positive multiple of 8, got %d", c->group_size);
+  if (c->scheme == 1 && (c->group_size < 4 || c->group_size > 256))
+    return set_err(FC2_ECONFIG, "spike reserving needs 4 <= group_size <= 256, got %d", c->group_size);
+  if (c->scheme != 0 && c->scheme != 1) return set_err(FC2_ECONFIG, "bad scheme %d", c->scheme);
+  if (c->scale_encoding != 0 && c->scale_encoding != 1) return set_err(FC2_ECONFIG, "bad scale encoding %d", c->scale_encoding);
+  if (c->theta < 1 || c->theta > 255) return set_err(FC2_ECONFIG, "theta must be in [1, 255], got %d", c->theta);
+  return FC2_OK;
+}
+
+static const double* lut_for(const fc2_config* c, int* rc) {
+  *rc = FC2_OK;
+  if (c->scale_encoding != 1) return nullptr;
+  std::lock_guard<std::mutex> lk(g_mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!g_lut || g_lut_dev != dev || !g_lut_ok[c->theta]) {
+    *rc = set_err(FC2_ECONFIG, "INT_LOG table for theta=%d not loaded (call fc2_set_intlog_table)", c->theta);
+    return nullptr;
+  }
+  return g_lut + (size_t)(c->theta - 1) * 256;
+}
+
+static int64_t rec_nb(const fc2_config* c) { return rec_bytes(c->scheme == 1, c->scale_encoding == 1); }
+
+}  // namespace fc2
+
+using namespace fc2;
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+
+extern "C" {
+
+int fc2_version(void) { return 1; }
+const char* fc2_last_error(void) { return g_err.c_str(); }
+int64_t fc2_launch_count(void) { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
+
+int fc2_check_config(const fc2_config* cfg) { return check_cfg(cfg); }
+
+int fc2_footprint(const fc2_config* cfg, int64_t n, int64_t* nbytes) {
+  int rc = check_cfg(cfg);
+  if (rc) return rc;
+  if (n < 0 || n % cfg->group_size) return set_err(FC2_ECONFIG, "element count %lld not a multiple of group_size %d", (long long)n, cfg->group_size);
+  *nbytes = n * cfg->bitwidth / 8 + (n / cfg->group_size) * rec_nb(cfg);
+  return FC2_OK;
+}
+
+int64_t fc2_plane_offset(const fc2_config* cfg, int64_t n, int32_t unit) {
+  if (check_cfg(cfg) || unit < 0 || unit >= n_units(cfg->bitwidth)) return -1;
+  return n * unit_off(cfg->bitwidth, unit) / 8;
+}
+int64_t fc2_meta_offset(const fc2_config* cfg, int64_t n) {
+  if (check_cfg(cfg)) return -1;
+  return n * cfg->bitwidth / 8;
+}
+
+int fc2_set_intlog_table(int32_t theta, const double* table256) {
+  if (theta < 1 || theta > 255 || !table256) return set_err(FC2_ECONFIG, "bad theta/table");
+  std::lock_guard<std::mutex> lk(g_mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!g_lut || g_lut_dev != dev) {
+    if (cudaMalloc(&g_lut, sizeof(double) * 255 * 256) != cudaSuccess)
+      return set_err(FC2_ECUDA, "cudaMalloc lut failed");
+    g_lut_dev = dev;
+    for (int i = 0; i < 256; ++i) g_lut_ok[i] = false;
+  }
+  if (cudaMemcpy(g_lut + (size_t)(theta - 1) * 256, table256, 256 * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
+    return set_err(FC2_ECUDA, "lut upload failed");
+  g_lut_ok[theta] = true;
+  return FC2_OK;
+}
+
+int fc2_encode_batch(const fc2_config* cfg, int32_t x_dtype, int32_t njobs, const void* const* xs,
+                     const int64_t* n_valid, const int64_t* n, void* const* payloads, int32_t* dev_err,
+                     void* stream) {
+  int rc = check_cfg(cfg);
+  if (rc) return rc;
+  if (njobs < 0 || njobs > FC2_MAX_JOBS) return set_err(FC2_ECONFIG, "njobs %d out of range", njobs);
+  if (x_dtype < 0 || x_dtype > 2) return set_err(FC2_ECONFIG, "bad dtype %d", x_dtype);
+  const double* lut = lut_for(cfg, &rc);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int B = cfg->bitwidth, G = cfg->group_size;
+  const bool sr = cfg->scheme == 1;
+  const int esz = x_dtype == FC2_BF16 ? 2 : (x_dtype == FC2_F32 ? 4 : 8);
+  EncBatch fast, gen;
+  for (EncBatch* b : {&fast, &gen}) {
+    b->nj = 0; b->B = B; b->G = G; b->sr = sr; b->intlog = cfg->scale_encoding; b->theta = cfg->theta;
+    b->total = 0; b->lut = lut; b->err = dev_err;
+  }
+  for (int i = 0; i < njobs; ++i) {
+    if (n[i] < 0 || n[i] % G) return set_err(FC2_ECONFIG, "chunk %lld not a multiple of group_size %d", (long long)n[i], G);
+    if (n_valid[i] < 0 || n_valid[i] > n[i]) return set_err(FC2_EDATA, "n_valid %lld outside [0, %lld]", (long long)n_valid[i], (long long)n[i]);
+    if (n[i] == 0) continue;
+    if (reinterpret_cast<uintptr_t>(payloads[i]) & 3u) return set_err(FC2_ECONFIG, "payload must be 4-byte aligned");
+    const bool aligned = (reinterpret_cast<uintptr_t>(xs[i]) & 15u) == 0 || n_valid[i] == 0;
+    const bool use_fast = fast_group(G) && x_dtype != FC2_F64 && aligned;
+    EncBatch* b = use_fast ? &fast : &gen;
+    EncJob& j = b->j[b->nj++];
+    j.x = xs[i] ? xs[i] : payloads[i];
+    j.out = (uint8_t*)payloads[i];
+    j.n_valid = n_valid[i];
+    j.n = n[i];
+    j.t0 = b->total;
+    b->total += use_fast ? (n[i] + 1023) / 1024 : n[i] / G;
+    (void)esz;
+  }
+  if (fast.nj) {
+    rc = enc_fast(B, x_dtype, sr, G, fast, st);
+    if (rc) return rc;
+  }
+  if (gen.nj) {
+    int64_t blocks = (gen.total + 7) / 8;
+    int64_t cap = (int64_t)num_sms() * 8;
+    if (blocks > cap) blocks = cap;
+    if (x_dtype == FC2_BF16) k_encode_gen<__nv_bfloat16><<<(unsigned)blocks, 256, 0, st>>>(gen);
+    else if (x_dtype == FC2_F32) k_encode_gen<float><<<(unsigned)blocks, 256, 0, st>>>(gen);
+    else k_encode_gen<double><<<(unsigned)blocks, 256, 0, st>>>(gen);
+    rc = cuda_check("k_encode_gen");
+    if (rc) return rc;
+  }
+  return FC2_OK;
+}
+
+int fc2_encode(const fc2_config* cfg, const void* x, int32_t x_dtype, int64_t n_valid, int64_t n, void* payload,
+               int32_t* dev_err, void* stream) {
+  return fc2_encode_batch(cfg, x_dtype, 1, &x, &n_valid, &n, &payload, dev_err, stream);
+}
+
+int fc2_decode_batch(const fc2_config* cfg, int32_t y_dtype, int32_t njobs, const void* const* payloads,
+                     const int64_t* n, void* const* ys, const int64_t* n_out, int32_t* dev_err, void* stream) {
+  int rc = check_cfg(cfg);
+  if (rc) return rc;
+  if (njobs < 0 || njobs > FC2_MAX_JOBS) return set_err(FC2_ECONFIG, "njobs %d out of range", njobs);
+  if (y_dtype < 0 || y_dtype > 2) return set_err(FC2_ECONFIG, "bad dtype %d", y_dtype);
+  const double* lut = lut_for(cfg, &rc);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int B = cfg->bitwidth, G = cfg->group_size;
+  const bool fastG = G % 32 == 0 && y_dtype != FC2_F64;
+  DecBatch b;
+  b.nj = 0; b.B = B; b.G = G; b.sr = cfg->scheme == 1; b.intlog = cfg->scale_encoding; b.theta = cfg->theta;
+  b.total = 0; b.lut = lut; b.err = dev_err;
+  for (int i = 0; i < njobs; ++i) {
+    if (n[i] < 0 || n[i] % G) return set_err(FC2_ECONFIG, "chunk %lld not a multiple of group_size %d", (long long)n[i], G);
+    if (n_out[i] < 0 || n_out[i] > n[i]) return set_err(FC2_ECONFIG, "n_out out of range");
+    if (n[i] == 0 || n_out[i] == 0) continue;
+    DecJob& j = b.j[b.nj++];
+    j.pay = (const uint8_t*)payloads[i];
+    j.y = ys[i];
+    j.n = n[i];
+    j.n_out = n_out[i];
+    j.t0 = b.total;
+    b.total += fastG ? (n[i] + 1023) / 1024 : n_out[i];
+  }
+  if (!b.nj) return FC2_OK;
+  if (fastG) {
+    int64_t blocks = (b.total + 7) / 8;
+    int64_t cap = (int64_t)num_sms() * 8;
+    if (blocks > cap) blocks = cap;
+return dec_fast(B, y_dtype, blocks, b, st);
+  }
+  int64_t blocks = (b.total + 255) / 256;
+  int64_t cap = (int64_t)num_sms() * 16;
+  if (blocks > cap) blocks = cap;
+  if (y_dtype == FC2_BF16) k_decode_gen<__nv_bfloat16><<<(unsigned)blocks, 256, 0, st>>>(b);
+  else if (y_dtype == FC2_F32) k_decode_gen<float><<<(unsigned)blocks, 256, 0, st>>>(b);
+  else k_decode_gen<double><<<(unsigned)blocks, 256, 0, st>>>(b);
+  return cuda_check("k_decode_gen");
+}
+
+int fc2_decode(const fc2_config* cfg, const void* payload, int64_t n, void* y, int32_t y_dtype, int64_t n_out,
+               int32_t* dev_err, void* stream) {
+  return fc2_decode_batch(cfg, y_dtype, 1, &payload, &n, &y, &n_out, dev_err, stream);
+}
+
+int fc2_gather_decode(const fc2_config* cfg, int32_t nshards, const void* const* shard_payloads, int64_t shard_len,
+                      void* y, int32_t y_dtype, int64_t n_out, int32_t* dev_err, void* stream) {
+  if (nshards < 0 || nshards > FC2_MAX_JOBS) return set_err(FC2_ECONFIG, "nshards out of range");
+  const int esz = y_dtype == FC2_BF16 ? 2 : (y_dtype == FC2_F32 ? 4 : 8);
+  int64_t ns[FC2_MAX_JOBS], no[FC2_MAX_JOBS];
+  void* ys[FC2_MAX_JOBS];
+  for (int i = 0; i < nshards; ++i) {
+    ns[i] = shard_len;
+    int64_t rem = n_out - (int64_t)i * shard_len;
+    no[i] = rem < 0 ? 0 : (rem > shard_len ? shard_len : rem);
+    ys[i] = (uint8_t*)y + (size_t)i * shard_len * esz;
+  }
+  return fc2_decode_batch(cfg, y_dtype, nshards, shard_payloads, ns, ys, no, dev_err, stream);
+}
+
+int fc2_reduce_requant(const fc2_config* cfg, int32_t nsrc, const void* const* src_payloads, int64_t n, int32_t ndst,
+                       void* const* dst_payloads, int32_t* dev_err, void* stream) {
+  int rc = check_cfg(cfg);
+  if (rc) return rc;
+  if (nsrc < 1 || nsrc > FC2_MAX_PEERS || ndst < 1 || ndst > FC2_MAX_PEERS)
+    return set_err(FC2_ECONFIG, "nsrc/ndst out of range");
+  if (n < 0 || n % cfg->group_size) return set_err(FC2_ECONFIG, "shard not a multiple of group_size");
+  if (n == 0) return FC2_OK;
+  const double* lut = lut_for(cfg, &rc);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  ReduceArgs a;
+  a.nsrc = nsrc; a.ndst = ndst; a.B = cfg->bitwidth; a.G = cfg->group_size; a.sr = cfg->scheme == 1;
+  a.intlog = cfg->scale_encoding; a.theta = cfg->theta; a.n = n; a.lut = lut; a.err = dev_err;
+  for (int i = 0; i < nsrc; ++i) a.src[i] = (const uint8_t*)src_payloads[i];
+  for (int i = 0; i < ndst; ++i) a.dst[i] = (uint8_t*)dst_payloads[i];
+  if (fast_group(a.G)) {
+    a.total = (n + 1023) / 1024;
+    return red_fast(a.B, a.sr != 0, a.G, a, st);
+  }
+  if (ndst > 8) return set_err(FC2_ECONFIG, "generic reduce supports <= 8 destinations");
+  a.total = n / a.G;
+  int64_t blocks = (a.total + 7) / 8;
+  int64_t cap = (int64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  k_reduce_gen<<<(unsigned)blocks, 256, 0, st>>>(a);
+  return cuda_check("k_reduce_gen");
+}
+
+int fc2_pack_codes(const int64_t* codes, int64_t n, int32_t bitwidth, uint8_t* planes, int32_t* dev_err,
+                   void* stream) {
+  if (bitwidth < 2 || bitwidth > 8) return set_err(FC2_ECONFIG, "bitwidth must be in [2, 8], got %d", bitwidth);
+  if (n < 0 || n % 8) return set_err(FC2_EDATA, "code count %lld must be a multiple of 8", (long long)n);
+  if (n == 0) return FC2_OK;
+  int64_t runs = n / 8;
+  k_pack<<<(unsigned)((runs + 255) / 256), 256, 0, (cudaStream_t)stream>>>(codes, n, bitwidth, planes, dev_err);
+  return cuda_check("k_pack");
+}
+
+int fc2_unpack_codes(const uint8_t* planes, int64_t n, int32_t bitwidth, uint8_t* codes, void* stream) {
+  if (bitwidth < 2 || bitwidth > 8) return set_err(FC2_ECONFIG, "bitwidth must be in [2, 8], got %d", bitwidth);
+  if (n < 0 || n % 8) return set_err(FC2_EDATA, "code count must be a multiple of 8");
+  if (n == 0) return FC2_OK;
+  int64_t runs = n / 8;
+  k_unpack<<<(unsigned)((runs + 255) / 256), 256, 0, (cudaStream_t)stream>>>(planes, n, bitwidth, codes);
+  return cuda_check("k_unpack");
+}
+
+int fc2_f32_to_bf16_bits(const float* x, int64_t n, uint16_t* out, void* stream) {
+  if (n <= 0) return FC2_OK;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
+  k_f32_to_bf16<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(x, n, out);
+  return cuda_check("k_f32_to_bf16");
+}
+
+int fc2_bf16_bits_to_f32(const uint16_t* x, int64_t n, float* out, void* stream) {
+  if (n <= 0) return FC2_OK;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
+  k_bf16_to_f32<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(x, n, out);
+  return cuda_check("k_bf16_to_f32");
+}
+
+}  // extern "C"

@@ -1,0 +1,212 @@
+// fc2_common.cuh -- device helpers shared by the FlashCommunication-V2 kernels.
+//
+// Arithmetic contract: SURVEY.md section 8.0 (R1-R15), which restates
+// /root/reference/pkg/src/qcomm/codec.py and bfloat16.py.  Every helper
+// here cites the reference line it must reproduce bit-for-bit.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "../../include/fc2.h"
+
+namespace fc2 {
+
+// ---------------------------------------------------------------------------
+// bit-split units, low bits first (codec.py:143-151, 154-162)
+// ---------------------------------------------------------------------------
+
+__host__ __device__ constexpr int n_units(int b) {
+  return b == 2 ? 1 : b == 3 ? 2 : b == 4 ? 1 : b == 5 ? 2 : b == 6 ? 2 : b == 7 ? 3 : 1;
+}
+__host__ __device__ constexpr int unit_w(int b, int u) {
+  // 2:(2) 3:(2,1) 4:(4) 5:(4,1) 6:(4,2) 7:(4,2,1) 8:(8)
+  return b == 2 ? (u == 0 ? 2 : 0)
+       : b == 3 ? (u == 0 ? 2 : u == 1 ? 1 : 0)
+       : b == 4 ? (u == 0 ? 4 : 0)
+       : b == 5 ? (u == 0 ? 4 : u == 1 ? 1 : 0)
+       : b == 6 ? (u == 0 ? 4 : u == 1 ? 2 : 0)
+       : b == 7 ? (u == 0 ? 4 : u == 1 ? 2 : u == 2 ? 1 : 0)
+       : (u == 0 ? 8 : 0);
+}
+// bit offset of unit u inside a code == cumulative width of earlier units
+__host__ __device__ constexpr int unit_off(int b, int u) {
+  return u == 0 ? 0 : unit_off(b, u - 1) + unit_w(b, u - 1);
+}
+
+// metadata record bytes (codec.py:400-425)
+__host__ __device__ constexpr int rec_bytes(bool sr, bool intlog) {
+  return intlog ? (sr ? 8 : 2) : (sr ? 12 : 4);
+}
+
+// ---------------------------------------------------------------------------
+// bfloat16 (bfloat16.py:16-31)
+// ---------------------------------------------------------------------------
+
+// float32 -> bf16 bits, RNE via the 0x7FFF bias (bfloat16.py:16-25).  Inputs
+// on this path are finite or +-inf; inf maps to 0x7F80 exactly like numpy.
+__device__ __forceinline__ uint32_t bf16_bits(float f) {
+  uint32_t u = __float_as_uint(f);
+  if (f != f) return 0x7FC0u;
+  return (u + 0x7FFFu + ((u >> 16) & 1u)) >> 16;
+}
+__device__ __forceinline__ float bf16_val(uint32_t bits) {
+  return __uint_as_float(bits << 16);
+}
+
+// NaN-propagating min/max (a NaN anywhere poisons the group statistics, which
+// is how the encoder detects non-finite input, codec.py:482-483).
+__device__ __forceinline__ float fmin_nan(float a, float b) {
+  float r;
+  asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// exact per-element code (codec.py:246-256, R8), float64, no contraction
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ int exact_code(double v, double off, double div, int L) {
+  if (!(div > 0.0)) return 0;                       // np.where(scale > 0, q, 0)
+  double q = __ddiv_rn(__dsub_rn(v, off), div);      // (rows - offset) / safe
+  if (!(q > 0.0)) return 0;                          // copysign(...) <= 0 -> clip 0
+  double r = floor(__dadd_rn(q, 0.5));               // floor(|q| + 0.5)
+  return r >= (double)L ? L : (int)r;                // clip(., 0, L)
+}
+
+// round half away from zero (codec.py:246-248)
+__device__ __forceinline__ double rha(double x) {
+  double r = floor(__dadd_rn(fabs(x), 0.5));
+  return copysign(r, x);
+}
+
+// ---------------------------------------------------------------------------
+// per-group parameters (codec.py:454-474, 512; R6, R7, R13)
+// ---------------------------------------------------------------------------
+
+struct GroupParams {
+  double off;        // code offset: zero (BF16) or -z*s_eff (INT_LOG)
+  double div;        // code divisor: scale (BF16) or s_eff (INT_LOG); 0 => codes 0
+  float off32;       // fast-path float copies
+  float inv32;
+  bool exact;        // range too small/large for the fp32 estimate: exact f64 for all
+  uint32_t sz;       // BF16: scale_bits | zero_bits << 16 ; INT_LOG: (u8)si | (u8)zi << 8
+};
+
+__device__ __forceinline__ GroupParams group_params(double zero, double vmax, int L, bool intlog,
+                                                    int theta, const double* __restrict__ lut,
+                                                    int32_t* err) {
+  GroupParams p;
+  double scale = __ddiv_rn(__dsub_rn(vmax, zero), (double)L);  // codec.py:512
+  if (!intlog) {
+    p.off = zero;
+    p.div = scale;
+    p.sz = bf16_bits(__double2float_rn(scale)) | (bf16_bits(__double2float_rn(zero)) << 16);
+  } else {
+    int si = -128;
+    if (scale > 0.0) {
+      double t = __dmul_rn(log2(scale), (double)theta);
+      double ft = fabs(t) - floor(fabs(t));
+      if (fabs(ft - 0.5) < 1e-9 && err) atomicOr(err, FC2_ERR_LOG2_TIE);
+      double r = rha(t);
+      r = r < -128.0 ? -128.0 : (r > 127.0 ? 127.0 : r);
+      si = (int)r;
+    }
+    double s_eff = si == -128 ? 0.0 : lut[si + 128];               // codec.py:468
+    int zi = 0;
+    if (s_eff > 0.0) {
+      double r = rha(__ddiv_rn(-zero, s_eff));                      // codec.py:471
+      r = r < -128.0 ? -128.0 : (r > 127.0 ? 127.0 : r);
+      zi = (int)r;
+    }
+    p.off = __dmul_rn(-(double)zi, s_eff);                          // codec.py:473
+    p.div = s_eff;
+    p.sz = (uint32_t)(uint8_t)(int8_t)si | ((uint32_t)(uint8_t)(int8_t)zi << 8);
+  }
+  if (p.div > 0.0) {
+    p.exact = !(p.div >= 1e-32 && p.div <= 1e28);
+    p.off32 = __double2float_rn(p.off);
+    p.inv32 = __frcp_rn(__double2float_rn(p.div));
+    if (p.exact) { p.off32 = 0.f; p.inv32 = 0.f; }
+  } else {
+    p.exact = false;
+    p.off32 = 0.f;
+    p.inv32 = 0.f;
+  }
+  return p;
+}
+
+// ---------------------------------------------------------------------------
+// fp32 code estimate with a 10-bit fixed-point fraction:
+// y = fma(v - off, inv, 0.5 + 2^-9) + 1.5*2^13 puts floor(q + 0.5 + 2^-9) in
+// bits [10, 18) and the fraction in bits [0, 10).  Whenever bits [2,10) are
+// all zero the element is within 2^-9 of a rounding tie and is recomputed
+// exactly in float64 (the estimate error is < 1e-4, so every other element is
+// provably identical to the reference's float64 result).
+// ---------------------------------------------------------------------------
+
+constexpr float kFixC = 0.5f + 1.0f / 512.0f;
+constexpr float kFixMagic = 12288.0f;  // 1.5 * 2^13: ulp 2^-10 over [8192, 16384)
+
+__device__ __forceinline__ uint32_t fix_est(float v, float off32, float inv32) {
+  float d = __fsub_rn(v, off32);
+  float f = __fmaf_rn(d, inv32, kFixC);
+  return __float_as_uint(__fadd_rn(f, kFixMagic));
+}
+__device__ __forceinline__ uint32_t fix_est_clamped(float v, float off32, float inv32, float Lh) {
+  float d = __fsub_rn(v, off32);
+  float f = __fmaf_rn(d, inv32, kFixC);
+  f = fminf(fmaxf(f, kFixC), Lh);  // INT_LOG codes may legitimately clip at both ends
+  return __float_as_uint(__fadd_rn(f, kFixMagic));
+}
+__device__ __forceinline__ bool fix_is_tie(uint32_t X) { return (X & 0x3FCu) == 0u; }
+
+// ---------------------------------------------------------------------------
+// misc
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+
+// store nbytes (<= 12) from words[]; widest stores the alignment allows
+__device__ __forceinline__ void store_record(uint8_t* p, const uint32_t* w, int nbytes) {
+  uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  if ((a & 3u) == 0 && (nbytes & 3) == 0) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      if (i < nbytes / 4) reinterpret_cast<uint32_t*>(p)[i] = w[i];
+  } else if ((a & 1u) == 0 && (nbytes & 1) == 0) {
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+      if (i < nbytes / 2) reinterpret_cast<uint16_t*>(p)[i] = (uint16_t)(w[i >> 1] >> ((i & 1) * 16));
+  } else {
+#pragma unroll
+    for (int i = 0; i < 12; ++i)
+      if (i < nbytes) p[i] = (uint8_t)(w[i >> 2] >> ((i & 3) * 8));
+  }
+}
+
+__device__ __forceinline__ void load_record(const uint8_t* p, uint32_t* w, int nbytes) {
+  uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  w[0] = w[1] = w[2] = 0;
+  if ((a & 3u) == 0 && (nbytes & 3) == 0) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      if (i < nbytes / 4) w[i] = reinterpret_cast<const uint32_t*>(p)[i];
+  } else if ((a & 1u) == 0 && (nbytes & 1) == 0) {
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+      if (i < nbytes / 2) w[i >> 1] |= (uint32_t)reinterpret_cast<const uint16_t*>(p)[i] << ((i & 1) * 16);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 12; ++i)
+      if (i < nbytes) w[i >> 2] |= (uint32_t)p[i] << ((i & 3) * 8);
+  }
+}
+
+}  // namespace fc2

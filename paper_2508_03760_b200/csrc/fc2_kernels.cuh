@@ -1,0 +1,506 @@
+// fc2_kernels.cuh -- kernel templates + per-bitwidth launchers (instantiated in
+// fc2_inst_b<B>.cu so the 8 bitwidths compile in parallel).
+#pragma once
+#include <cstdarg>
+#include <cstdio>
+#include <utility>
+
+#include "fc2_decode.cuh"
+#include "fc2_encode.cuh"
+
+namespace fc2 {
+
+// library state lives in fc2_codec.cu
+int set_err(int code, const char* fmt, ...);
+int cuda_check(const char* what);
+int num_sms();
+
+// ---------------------------------------------------------------------------
+// job tables (passed by value as __grid_constant__ kernel parameters)
+// ---------------------------------------------------------------------------
+
+struct EncJob {
+  const void* x;
+  uint8_t* out;
+  int64_t n_valid, n, t0;  // t0: first global tile (fast) / group (generic)
+};
+struct EncBatch {
+  int nj, B, G, sr, intlog, theta;
+  int64_t total;
+  const double* lut;
+  int32_t* err;
+  EncJob j[FC2_MAX_JOBS];
+};
+
+struct DecJob {
+  const uint8_t* pay;
+  void* y;
+  int64_t n, n_out, t0;
+};
+struct DecBatch {
+  int nj, B, G, sr, intlog, theta;
+  int64_t total;
+  const double* lut;
+  int32_t* err;
+  DecJob j[FC2_MAX_JOBS];
+};
+
+#define FC2_MAX_PEERS 16
+struct ReduceArgs {
+  int nsrc, ndst, B, G, sr, intlog, theta;
+  int64_t n, total;
+  const double* lut;
+  int32_t* err;
+  const uint8_t* src[FC2_MAX_PEERS];
+  uint8_t* dst[FC2_MAX_PEERS];
+};
+
+template <class Batch>
+__device__ __forceinline__ int find_job(const Batch& b, int64_t t) {
+  int lo = 0, hi = b.nj - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (b.j[mid].t0 <= t) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// ---------------------------------------------------------------------------
+// fast encoder
+// ---------------------------------------------------------------------------
+
+constexpr int kEncWarps = 4;   // warps per CTA
+constexpr int kStages = 3;     // cp.async pipeline depth per warp
+
+template <typename T>
+struct Stage {
+  static constexpr int EPC = 16 / sizeof(T);   // elements per 16-byte chunk
+  static constexpr int CPL = 32 / EPC;         // chunks per lane (32 elements)
+  static constexpr int CHUNKS = 32 * CPL;      // chunks per warp tile
+  static constexpr int BYTES = CHUNKS * 16;    // bytes per warp tile stage
+  // XOR swizzle: conflict-free for both the coalesced fill (chunk c = l + 32j)
+  // and the per-lane read-back (chunks CPL*l .. CPL*l + CPL - 1)
+  __device__ static __forceinline__ int pos(int c) { return swz<CPL>(c); }
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <typename T>
+__device__ __forceinline__ void issue_tile(const EncBatch& b, int64_t t, uint8_t* stage) {
+  using S = Stage<T>;
+  const int ji = find_job(b, t);
+  const EncJob& jb = b.j[ji];
+  const int64_t e_base = (t - jb.t0) * 1024;
+  const int lane = (int)lane_id();
+  const T* x = reinterpret_cast<const T*>(jb.x);
+#pragma unroll
+  for (int j = 0; j < S::CPL; ++j) {
+    const int c = lane + 32 * j;
+    const int64_t e = e_base + (int64_t)c * S::EPC;
+    int64_t valid = jb.n_valid - e;
+    valid = valid < 0 ? 0 : (valid > S::EPC ? S::EPC : valid);
+    const void* src = valid > 0 ? (const void*)(x + e) : (const void*)x;
+    cp_async16(stage + S::pos(c) * 16, src, (int)(valid * sizeof(T)));
+  }
+}
+
+template <typename T, int B, bool SR, int G>
+__global__ void __launch_bounds__(kEncWarps * 32) k_encode_fast(const __grid_constant__ EncBatch b) {
+  using S = Stage<T>;
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int warp = (int)(threadIdx.x >> 5), lane = (int)lane_id();
+  uint8_t* my = smem + warp * kStages * S::BYTES;
+  const int64_t nw = (int64_t)gridDim.x * kEncWarps;
+  int64_t t = (int64_t)blockIdx.x * kEncWarps + warp;
+
+  // prologue: put kStages-1 tiles in flight
+#pragma unroll
+  for (int s = 0; s < kStages - 1; ++s) {
+    const int64_t tt = t + s * nw;
+    if (tt < b.total) issue_tile<T>(b, tt, my + s * S::BYTES);
+    cp_async_commit();
+  }
+  int stage = 0;
+  for (; t < b.total; t += nw) {
+    {  // refill the slot consumed in the previous iteration
+      const int64_t tt = t + (kStages - 1) * nw;
+      const int s = (stage + kStages - 1) % kStages;
+      if (tt < b.total) issue_tile<T>(b, tt, my + s * S::BYTES);
+      cp_async_commit();
+    }
+    cp_async_wait<kStages - 1>();
+    __syncwarp();
+    const uint8_t* st = my + stage * S::BYTES;
+
+    const int ji = find_job(b, t);
+    const EncJob& jb = b.j[ji];
+    const int64_t e0 = (t - jb.t0) * 1024 + lane * 32;
+    const bool active = e0 < jb.n;
+    EncCtx cx;
+    cx.n = jb.n;
+    cx.meta_off = jb.n * B / 8;
+    cx.intlog = b.intlog;
+    cx.theta = b.theta;
+    cx.lut = b.lut;
+    cx.err = b.err;
+    uint8_t* out = jb.out;
+    auto store = [&](const uint32_t* w, int64_t e0_, bool meta, int64_t moff, const uint32_t* rec, int rb) {
+#pragma unroll
+      for (int u = 0; u < n_units(B); ++u) {
+        const int W = unit_w(B, u), O = unit_off(B, u);
+        uint8_t* p = out + (cx.n * O) / 8 + (e0_ * W) / 8;
+        if (W == 1) store_words<1>(p, w + LaneWords<B>::base(u));
+        else if (W == 2) store_words<2>(p, w + LaneWords<B>::base(u));
+        else if (W == 4) store_words<4>(p, w + LaneWords<B>::base(u));
+        else store_words<8>(p, w + LaneWords<B>::base(u));
+      }
+      if (meta) store_record(out + cx.meta_off + moff, rec, rb);
+    };
+    if constexpr (sizeof(T) == 2) {
+      Bf16Vals v;
+      v.st = st;
+#pragma unroll
+      for (int j = 0; j < S::CPL; ++j) {
+        uint4 q = *reinterpret_cast<const uint4*>(st + S::pos(S::CPL * lane + j) * 16);
+        v.w[4 * j] = q.x; v.w[4 * j + 1] = q.y; v.w[4 * j + 2] = q.z; v.w[4 * j + 3] = q.w;
+      }
+      __syncwarp();
+      encode_lane<B, SR, G>(v, active, e0, cx, store);
+    } else {
+      F32Vals v;
+      v.st = st;
+      v.spill = nullptr;
+#pragma unroll
+      for (int j = 0; j < S::CPL; ++j) {
+        float4 q = *reinterpret_cast<const float4*>(st + S::pos(S::CPL * lane + j) * 16);
+        v.f[4 * j] = q.x; v.f[4 * j + 1] = q.y; v.f[4 * j + 2] = q.z; v.f[4 * j + 3] = q.w;
+      }
+      __syncwarp();
+      encode_lane<B, SR, G>(v, active, e0, cx, store);
+    }
+    __syncwarp();  // every lane is done with this slot before it is refilled
+    stage = (stage + 1) % kStages;
+  }
+  cp_async_wait<0>();
+}
+
+// ---------------------------------------------------------------------------
+// generic encoder: warp per group, exact float64
+// ---------------------------------------------------------------------------
+
+template <typename T>
+struct PlainLoader {
+  const T* x;
+  int64_t nv;
+  __device__ double operator()(int64_t i) const { return load_elem<T>(x, i, nv); }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_encode_gen(const __grid_constant__ EncBatch b) {
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < b.total; g += nw) {
+    const int ji = find_job(b, g);
+    const EncJob& jb = b.j[ji];
+    EncCtx cx;
+    cx.n = jb.n;
+    cx.meta_off = jb.n * b.B / 8;
+    cx.intlog = b.intlog;
+    cx.theta = b.theta;
+    cx.lut = b.lut;
+    cx.err = b.err;
+    OutList o;
+    o.p[0] = jb.out;
+    o.nd = 1;
+    PlainLoader<T> ld{reinterpret_cast<const T*>(jb.x), jb.n_valid};
+    generic_encode_group(ld, o, jb.n, g - jb.t0, b.B, b.G, b.sr != 0, cx);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// decoders
+// ---------------------------------------------------------------------------
+
+template <typename OT>
+__device__ __forceinline__ OT cvt_out(float v);
+template <>
+__device__ __forceinline__ float cvt_out<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 cvt_out<__nv_bfloat16>(float v) {
+  return __ushort_as_bfloat16((unsigned short)bf16_bits(v));  // bfloat16.py:16-25
+}
+
+template <typename OT>
+__device__ __forceinline__ void store_run(OT* y, int64_t e0, int64_t n_out, const float* v) {
+  // 32 values at y[e0..]; vectorized when the whole run is in bounds and aligned
+  constexpr int VE = 16 / sizeof(OT);
+  OT* p = y + e0;
+  if (e0 + 32 <= n_out && (reinterpret_cast<uintptr_t>(p) & 15u) == 0) {
+#pragma unroll
+    for (int i = 0; i < 32; i += VE) {
+      uint4 q;
+      if constexpr (sizeof(OT) == 2) {
+        q.x = bf16_bits(v[i]) | (bf16_bits(v[i + 1]) << 16);
+        q.y = bf16_bits(v[i + 2]) | (bf16_bits(v[i + 3]) << 16);
+        q.z = bf16_bits(v[i + 4]) | (bf16_bits(v[i + 5]) << 16);
+        q.w = bf16_bits(v[i + 6]) | (bf16_bits(v[i + 7]) << 16);
+      } else {
+        q.x = __float_as_uint(v[i]); q.y = __float_as_uint(v[i + 1]);
+        q.z = __float_as_uint(v[i + 2]); q.w = __float_as_uint(v[i + 3]);
+      }
+      *reinterpret_cast<uint4*>(p + i) = q;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (e0 + i < n_out) p[i] = cvt_out<OT>(v[i]);
+  }
+}
+
+// fast decode, 32 elements per lane, G % 32 == 0.  OT: bf16/f32 (f64 -> generic)
+template <typename OT, int B>
+__global__ void __launch_bounds__(256) k_decode_fast(const __grid_constant__ DecBatch b) {
+  const int lane = (int)lane_id();
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < b.total; t += nw) {
+    const int ji = find_job(b, t);
+    const DecJob& jb = b.j[ji];
+    const int64_t e0 = (t - jb.t0) * 1024 + lane * 32;
+    if (e0 >= jb.n || e0 >= jb.n_out) continue;
+    DecCtx c;
+    c.n = jb.n; c.meta_off = jb.n * B / 8; c.B = B; c.G = b.G; c.sr = b.sr; c.intlog = b.intlog;
+    c.theta = b.theta; c.lut = b.lut; c.err = b.err;
+    const int64_t grp = e0 / b.G;
+    GroupMeta m = read_meta(jb.pay, grp, c);
+    uint32_t code[32];
+    load_codes32<B>(jb.pay, jb.n, e0, code);
+    float v[32];
+    if (!b.intlog) {
+#pragma unroll
+      for (int k = 0; k < 32; ++k) v[k] = __fmaf_rn(code_f32(code[k]), m.s32, m.z32);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 32; ++k) v[k] = dq32(code[k], m, true);
+    }
+    OT* y = reinterpret_cast<OT*>(jb.y);
+    store_run<OT>(y, e0, jb.n_out, v);
+    if (b.sr) {  // reserved values: imin then imax (same thread -> program order)
+      const int64_t g0 = grp * b.G;
+      const int64_t a = g0 + m.imin, z = g0 + m.imax;
+      if (m.imin >= 0 && a >= e0 && a < e0 + 32 && a < jb.n_out) y[a] = cvt_out<OT>(m.smin);
+      if (m.imax >= 0 && z >= e0 && z < e0 + 32 && z < jb.n_out) y[z] = cvt_out<OT>(m.smax);
+    }
+  }
+}
+
+// generic decode: thread per element (any G, any output type)
+template <typename OT>
+__global__ void __launch_bounds__(256) k_decode_gen(const __grid_constant__ DecBatch b) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < b.total; t += stride) {
+    const int ji = find_job(b, t);
+    const DecJob& jb = b.j[ji];
+    const int64_t e = t - jb.t0;
+    if (e >= jb.n_out) continue;
+    DecCtx c;
+    c.n = jb.n; c.meta_off = jb.n * b.B / 8; c.B = b.B; c.G = b.G; c.sr = b.sr; c.intlog = b.intlog;
+    c.theta = b.theta; c.lut = b.lut; c.err = b.err;
+    OT* y = reinterpret_cast<OT*>(jb.y);
+    if constexpr (sizeof(OT) == 8) {
+      y[e] = decode_elem64(jb.pay, e, c);
+    } else {
+      y[e] = cvt_out<OT>(decode_elem32(jb.pay, e, c));
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// reduce + requantize (two-step middle stage)
+// ---------------------------------------------------------------------------
+
+constexpr int kRedWarps = 4;
+
+template <int B, bool SR, int G>
+__global__ void __launch_bounds__(kRedWarps * 32) k_reduce_fast(const __grid_constant__ ReduceArgs a) {
+  // per-lane spill region for the spike patch: 36 floats (padded, conflict-free)
+  __shared__ __align__(16) float sp[kRedWarps * 32 * 36];
+  const int warp = (int)(threadIdx.x >> 5), lane = (int)lane_id();
+  float* mine = sp + (warp * 32 + lane) * 36;
+  const int64_t nw = (int64_t)gridDim.x * kRedWarps;
+  DecCtx dc;
+  dc.n = a.n; dc.meta_off = a.n * B / 8; dc.B = B; dc.G = G; dc.sr = SR; dc.intlog = a.intlog;
+  dc.theta = a.theta; dc.lut = a.lut; dc.err = a.err;
+  EncCtx cx;
+  cx.n = a.n; cx.meta_off = a.n * B / 8; cx.intlog = a.intlog; cx.theta = a.theta; cx.lut = a.lut;
+  cx.err = a.err;
+  for (int64_t t = (int64_t)blockIdx.x * kRedWarps + warp; t < a.total; t += nw) {
+    const int64_t e0 = t * 1024 + lane * 32;
+    const bool active = e0 < a.n;
+    const int64_t ec = active ? e0 : 0;
+    F32Vals acc;
+    acc.st = nullptr;
+    acc.spill = mine;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) acc.f[k] = 0.0f;  // acc = zeros(float32) (collectives.py:293)
+    const int64_t grp = ec / G;
+    const int il = (int)(ec - grp * G);  // element offset of this lane inside its group
+    for (int s = 0; s < a.nsrc; ++s) {
+      GroupMeta m = read_meta(a.src[s], grp, dc);
+      uint32_t code[32];
+      load_codes32<B>(a.src[s], a.n, ec, code);
+      float d[32];
+      if (!a.intlog) {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) d[k] = __fmaf_rn(code_f32(code[k]), m.s32, m.z32);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) d[k] = dq32(code[k], m, true);
+      }
+      if constexpr (SR) {
+        const bool hit_a = m.imin >= il && m.imin < il + 32;
+        const bool hit_z = m.imax >= il && m.imax < il + 32;
+        if (__any_sync(0xffffffffu, hit_a || hit_z)) {
+#pragma unroll
+          for (int k = 0; k < 32; k += 4) *reinterpret_cast<float4*>(mine + k) = make_float4(d[k], d[k + 1], d[k + 2], d[k + 3]);
+          if (hit_a) mine[m.imin - il] = m.smin;
+          if (hit_z) mine[m.imax - il] = m.smax;
+#pragma unroll
+          for (int k = 0; k < 32; k += 4) {
+            float4 q = *reinterpret_cast<const float4*>(mine + k);
+            d[k] = q.x; d[k + 1] = q.y; d[k + 2] = q.z; d[k + 3] = q.w;
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 32; ++k) acc.f[k] = __fadd_rn(acc.f[k], d[k]);  // acc += dq (rank order)
+    }
+    auto store = [&](const uint32_t* w, int64_t e0_, bool meta, int64_t moff, const uint32_t* rec, int rb) {
+      for (int dd = 0; dd < a.ndst; ++dd) {
+        uint8_t* out = a.dst[dd];
+#pragma unroll
+        for (int u = 0; u < n_units(B); ++u) {
+          const int W = unit_w(B, u), O = unit_off(B, u);
+          uint8_t* p = out + (a.n * O) / 8 + (e0_ * W) / 8;
+          if (W == 1) store_words<1>(p, w + LaneWords<B>::base(u));
+          else if (W == 2) store_words<2>(p, w + LaneWords<B>::base(u));
+          else if (W == 4) store_words<4>(p, w + LaneWords<B>::base(u));
+          else store_words<8>(p, w + LaneWords<B>::base(u));
+        }
+        if (meta) store_record(out + cx.meta_off + moff, rec, rb);
+      }
+    };
+#pragma unroll
+    for (int k = 0; k < 32; k += 4)  // spill the sums for the rare exact path
+      *reinterpret_cast<float4*>(mine + k) = make_float4(acc.f[k], acc.f[k + 1], acc.f[k + 2], acc.f[k + 3]);
+    encode_lane<B, SR, G>(acc, active, e0, cx, store);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// template dispatch
+// ---------------------------------------------------------------------------
+
+template <int B, bool SR, int G>
+struct EncFast {
+  template <typename T>
+  static int launch(const EncBatch& b, cudaStream_t st) {
+    auto kern = k_encode_fast<T, B, SR, G>;
+    const int smem = kEncWarps * kStages * Stage<T>::BYTES;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      attr = true;
+    }
+    int64_t blocks = (b.total + kEncWarps - 1) / kEncWarps;
+    int64_t cap = (int64_t)num_sms() * 4;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    kern<<<(unsigned)blocks, kEncWarps * 32, smem, st>>>(b);
+    return cuda_check("k_encode_fast");
+  }
+};
+
+#define FC2_G_CASES(BB, SS)                                              \
+  switch (G) {                                                           \
+    case 32: return F<BB, SS, 32>::go(std::forward<Args>(args)...);      \
+    case 64: return F<BB, SS, 64>::go(std::forward<Args>(args)...);      \
+    case 128: return F<BB, SS, 128>::go(std::forward<Args>(args)...);    \
+    case 256: return F<BB, SS, 256>::go(std::forward<Args>(args)...);    \
+  }                                                                      \
+  break;
+#define FC2_B_CASE(BB)                        \
+  case BB:                                    \
+    if (sr) { FC2_G_CASES(BB, true) }         \
+    else { FC2_G_CASES(BB, false) }           \
+    break;
+
+template <int B, bool SR, int G>
+struct EncFastBf16 {
+  static int go(const EncBatch& b, cudaStream_t st) { return EncFast<B, SR, G>::template launch<__nv_bfloat16>(b, st); }
+};
+template <int B, bool SR, int G>
+struct EncFastF32 {
+  static int go(const EncBatch& b, cudaStream_t st) { return EncFast<B, SR, G>::template launch<float>(b, st); }
+};
+
+template <int B, bool SR, int G>
+struct RedFast {
+  static int go(const ReduceArgs& a, cudaStream_t st) {
+    int64_t blocks = (a.total + kRedWarps - 1) / kRedWarps;
+    int64_t cap = (int64_t)num_sms() * 4;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    k_reduce_fast<B, SR, G><<<(unsigned)blocks, kRedWarps * 32, 0, st>>>(a);
+    return cuda_check("k_reduce_fast");
+  }
+};
+
+
+// per-bitwidth launchers (defined in fc2_inst_b<B>.cu)
+template <int B> int launch_enc_fast(int dtype, bool sr, int G, const EncBatch& b, cudaStream_t st);
+template <int B> int launch_red_fast(bool sr, int G, const ReduceArgs& a, cudaStream_t st);
+template <int B> int launch_dec_fast(int dtype, int64_t blocks, const DecBatch& b, cudaStream_t st);
+
+template <int B>
+struct Launchers {
+  template <bool SR>
+  static int enc(int dtype, int G, const EncBatch& b, cudaStream_t st) {
+    switch (G) {
+      case 32: return dtype == FC2_BF16 ? EncFastBf16<B, SR, 32>::go(b, st) : EncFastF32<B, SR, 32>::go(b, st);
+      case 64: return dtype == FC2_BF16 ? EncFastBf16<B, SR, 64>::go(b, st) : EncFastF32<B, SR, 64>::go(b, st);
+      case 128: return dtype == FC2_BF16 ? EncFastBf16<B, SR, 128>::go(b, st) : EncFastF32<B, SR, 128>::go(b, st);
+      case 256: return dtype == FC2_BF16 ? EncFastBf16<B, SR, 256>::go(b, st) : EncFastF32<B, SR, 256>::go(b, st);
+    }
+    return set_err(FC2_ECONFIG, "no fast encoder for G=%d", G);
+  }
+  template <bool SR>
+  static int red(int G, const ReduceArgs& a, cudaStream_t st) {
+    switch (G) {
+      case 32: return RedFast<B, SR, 32>::go(a, st);
+      case 64: return RedFast<B, SR, 64>::go(a, st);
+      case 128: return RedFast<B, SR, 128>::go(a, st);
+      case 256: return RedFast<B, SR, 256>::go(a, st);
+    }
+    return set_err(FC2_ECONFIG, "no fast reducer for G=%d", G);
+  }
+};
+
+#define FC2_INSTANTIATE_B(BB)                                                                  \
+  template <> int launch_enc_fast<BB>(int dtype, bool sr, int G, const EncBatch& b, cudaStream_t st) { \
+    return sr ? Launchers<BB>::enc<true>(dtype, G, b, st) : Launchers<BB>::enc<false>(dtype, G, b, st); \
+  }                                                                                            \
+  template <> int launch_red_fast<BB>(bool sr, int G, const ReduceArgs& a, cudaStream_t st) {  \
+    return sr ? Launchers<BB>::red<true>(G, a, st) : Launchers<BB>::red<false>(G, a, st);     \
+  }                                                                                            \
+  template <> int launch_dec_fast<BB>(int dtype, int64_t blocks, const DecBatch& b, cudaStream_t st) { \
+    if (dtype == FC2_BF16) k_decode_fast<__nv_bfloat16, BB><<<(unsigned)blocks, 256, 0, st>>>(b); \
+    else k_decode_fast<float, BB><<<(unsigned)blocks, 256, 0, st>>>(b);                        \
+    return cuda_check("k_decode_fast");                                                        \
+  }
+
+}  // namespace fc2
