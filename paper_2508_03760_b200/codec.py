@@ -263,7 +263,8 @@ def decode_chunk(chunk: QuantizedChunk, out_dtype=None):
     device chunks decode to a CUDA tensor (float32 unless ``out_dtype``)."""
     config = chunk.config
     n = chunk.element_count
-    if not chunk.on_device:
+    host = not chunk.on_device
+    if host:
         units = bit_split(config.bitwidth)
         if len(chunk.planes) != len(units):
             raise DecodeFormatError(f"expected {len(units)} planes, got {len(chunk.planes)}")
@@ -275,11 +276,11 @@ def decode_chunk(chunk: QuantizedChunk, out_dtype=None):
         expected = (n // config.group_size) * meta_record_nbytes(config)
         if len(chunk.meta) != expected:
             raise DecodeFormatError(f"metadata has {len(chunk.meta)} bytes, expected {expected}")
-    dt = out_dtype or (torch.float32 if chunk.on_device else torch.float64)
+    dt = out_dtype or (torch.float64 if host else torch.float32)
     y = decode_payload(chunk.payload, config, n, out_dtype=dt)
-    if chunk.on_device:
+    if not host:
         return y
-    chunk._payload = None
+    chunk._payload = None  # keep host residency
     return y.cpu().numpy()
 
 

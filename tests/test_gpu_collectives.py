@@ -16,7 +16,8 @@ A2A, A2A_IDX = load("a2a_golden.npz")
 
 
 def cfg(bits, g, sr):
-    return fc.QuantConfig(bits, group_size=g, scheme=fc.Scheme.SPIKE_RESERVING if sr else fc.Scheme.RTN)
+    return fc.QuantConfig(bits, group_size=g, scheme=fc.Scheme.SPIKE_RESERVING if sr else fc.Scheme.RTN,
+                          chunk_size=g)
 
 
 @pytest.mark.parametrize("case", [c for c in TS_IDX if c["key"] != "ts_identical"], ids=lambda c: c["key"])
