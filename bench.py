@@ -1,0 +1,495 @@
+"""Benchmark contract for the FlashCommunication-V2 hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N == 1 (default): BASELINE configs[1] -- codec round trip (encode -> packed
+payload -> decode) of a 64 MiB bf16 tensor (33,554,432 elements), 4-bit,
+group 128, spike reserving; the full bit-width sweep rides along in "sweep".
+value = algbw = tensor bytes / round-trip latency (GB/s, nccl-tests style).
+
+N > 1 (torchrun, one rank per GPU): BASELINE configs[2] -- two-step quantized
+AllReduce of 8192 x 4096 bf16 per rank (4-bit SR g128) over CUDA-IPC peer
+memory, with the bf16 NCCL AllReduce timed on the same box; value = aggregate
+algbw over all ranks, latency = max over ranks.
+
+--impl reference: the reference's CPU algorithm (oracle/ numpy port; the
+reference is pure Python+numpy) on the same workload, bounded
+sample per step, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "quantized AllReduce/All2All algbw GB/s & latency at 2/4/8 B200 vs bf16 NCCL"
+N_ELEMS = 8192 * 4096  # 64 MiB of bf16
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _ncu_traffic(kernel_key: str):
+    """DRAM bytes per launch from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(kernel_key)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5.0:  # first sample before timing starts
+                time.sleep(0.02)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# our arm, N == 1: codec round trip
+# ---------------------------------------------------------------------------
+
+
+def spiky_bf16(n, seed, device):
+    import torch
+
+    g = torch.Generator(device=device).manual_seed(seed)
+    x = torch.randn(n, device=device, generator=g)
+    spike = torch.rand(n, device=device, generator=g) < 1 / 64
+    return torch.where(spike, torch.sign(x) * 50, x).to(torch.bfloat16)
+
+
+def time_roundtrip(fc, x, cfg, steps, warmup, flush):
+    """Per-step CUDA-event time of encode + decode (and each kernel alone)."""
+    import torch
+
+    n = x.numel()
+    F = fc.footprint_bytes(cfg, n)
+    pay = torch.empty(F, dtype=torch.uint8, device=x.device)
+    y = torch.empty(n, dtype=torch.bfloat16, device=x.device)
+    err = torch.zeros(1, dtype=torch.int32, device=x.device)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+    for _ in range(warmup):
+        flush.zero_()
+        fc.encode_payload(x, cfg, n, out=pay, err=err, check=False)
+        fc.decode_payload(pay, cfg, n, out=y, err=err, check=False)
+    torch.cuda.synchronize()
+    lib = fc._lib.lib()
+    l0 = lib.fc2_launch_count()
+    for i in range(steps):
+        flush.zero_()  # evict L2 between steps (outside the timed region)
+        ev[i][0].record()
+        fc.encode_payload(x, cfg, n, out=pay, err=err, check=False)
+        ev[i][1].record()
+        fc.decode_payload(pay, cfg, n, out=y, err=err, check=False)
+        ev[i][2].record()
+    torch.cuda.synchronize()
+    launches = lib.fc2_launch_count() - l0
+    enc = [ev[i][0].elapsed_time(ev[i][1]) for i in range(steps)]
+    dec = [ev[i][1].elapsed_time(ev[i][2]) for i in range(steps)]
+    if int(err.item()):
+        raise RuntimeError(f"device error word {int(err.item())} during bench")
+    return enc, dec, F, launches, (pay, y)
+
+
+def time_e2e(fc, x_host, cfg, steps, warmup):
+    """Host-buffer round trip through the public API: pinned bf16 in -> H2D ->
+    encode -> payload D2H (the wire bytes) -> decode -> bf16 D2H."""
+    import torch
+
+    n = x_host.numel()
+    F = fc.footprint_bytes(cfg, n)
+    dev = torch.device("cuda")
+    xd = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    pay = torch.empty(F, dtype=torch.uint8, device=dev)
+    yd = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    pay_h = torch.empty(F, dtype=torch.uint8).pin_memory()
+    y_h = torch.empty(n, dtype=torch.bfloat16).pin_memory()
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def step():
+        xd.copy_(x_host, non_blocking=True)
+        fc.encode_payload(xd, cfg, n, out=pay, err=err, check=False)
+        pay_h.copy_(pay, non_blocking=True)
+        fc.decode_payload(pay, cfg, n, out=yd, err=err, check=False)
+        y_h.copy_(yd, non_blocking=True)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(steps):
+        step()
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / steps
+    return ms, 2 * n, F + 2 * n
+
+
+def cpu_baseline_codec(n_sample, reps, bits, g, sr):
+    """The oracle (numpy port of the reference algorithm) timed on host cores."""
+    import numpy as np
+
+    from oracle import fc2_oracle as O
+
+    if reps <= 0:
+        return None, None
+    x = O.bf16_snap(O.spiky(n_sample, 0)).astype(np.float32)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        planes, meta = O.encode(x, bits, g, sr)
+        O.decode(planes, meta, n_sample, bits, g, sr)
+    dt = (time.perf_counter() - t0) / reps
+    return 2 * n_sample / dt / 1e9, dt
+
+
+def run_codec(args):
+    import torch
+
+    import paper_2508_03760_b200 as fc
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    n = args.n
+    sr = args.scheme == "sr"
+    cfg = fc.QuantConfig(args.bits, group_size=args.group,
+                         scheme=fc.Scheme.SPIKE_RESERVING if sr else fc.Scheme.RTN, chunk_size=args.group)
+    x = spiky_bf16(n, 0, dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    with ClockSampler(dev.index) as clk:
+        enc, dec, F, launches, _ = time_roundtrip(fc, x, cfg, args.steps, args.warmup, flush)
+        # keep the timed loop running long enough for the sampler to see it
+        t_end = time.time() + 1.0
+        while time.time() < t_end:
+            time_roundtrip(fc, x, cfg, args.steps, 0, flush)
+    t_enc, t_dec = statistics.mean(enc), statistics.mean(dec)
+    ms = t_enc + t_dec
+    value = 2 * n / (ms * 1e-3) / 1e9
+    peak, peak_kind = _peaks()
+    enc_bytes, dec_bytes = 2 * n + F, F + 2 * n
+    kernels = {
+        "encode": {"ms": t_enc, "bytes": enc_bytes, "GBps": enc_bytes / (t_enc * 1e-3) / 1e9},
+        "decode": {"ms": t_dec, "bytes": dec_bytes, "GBps": dec_bytes / (t_dec * 1e-3) / 1e9},
+    }
+    dom = "encode" if t_enc >= t_dec else "decode"
+    roof = {
+        "kernel": "k_encode_fast" if dom == "encode" else "k_decode_fast",
+        "bound": "hbm",
+        "achieved": kernels[dom]["GBps"],
+        "peak": peak,
+        "peak_kind": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json, burst copy)",
+        "unit": "GB/s",
+        "frac": kernels[dom]["GBps"] / peak,
+        "traffic": _ncu_traffic(f"{dom}_b{args.bits}_{args.scheme}_g{args.group}"),
+        "algorithmic_bytes_per_launch": kernels[dom]["bytes"],
+    }
+    # bit-width sweep (configs[1]): RTN and SR for 2/3/4/5/6/8 bits
+    sweep = {}
+    if not args.no_sweep:
+        for b in (2, 3, 4, 5, 6, 8):
+            for sch in ("rtn", "sr"):
+                c = fc.QuantConfig(b, group_size=args.group, chunk_size=args.group,
+                                   scheme=fc.Scheme.SPIKE_RESERVING if sch == "sr" else fc.Scheme.RTN)
+                e, d, Fb, _, _ = time_roundtrip(fc, x, c, max(3, args.steps // 2), 2, flush)
+                te, td = statistics.mean(e), statistics.mean(d)
+                sweep[f"b{b}_{sch}"] = {"roundtrip_GBps": round(2 * n / ((te + td) * 1e-3) / 1e9, 1),
+                                        "encode_GBps": round((2 * n + Fb) / (te * 1e-3) / 1e9, 1),
+                                        "decode_GBps": round((Fb + 2 * n) / (td * 1e-3) / 1e9, 1),
+                                        "payload_bytes": Fb}
+    # end to end through host buffers
+    x_host = x.cpu().pin_memory()
+    e2e_ms, h2d, d2h = time_e2e(fc, x_host, cfg, max(3, args.steps), 2)
+    cpu_val, cpu_dt = cpu_baseline_codec(n, args.cpu_reps, args.bits, args.group, sr)
+    line = {
+        "metric": METRIC,
+        "value": round(value, 2),
+        "unit": "GB/s",
+        "n_gpus": 1,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms, 5),
+        "latency_us": round(ms * 1e3, 2),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16 in/out, fp32 math (f64 on near-ties), packed u8 planes",
+        "data": "synthetic: N(0,1) with 1/64 of entries at +-50 (reference default_spiky_spec), bf16",
+        "config": {"workload": "codec round trip, 64 MiB bf16 tensor (BASELINE configs[1])",
+                   "n": n, "bits": args.bits, "group": args.group, "scheme": args.scheme,
+                   "payload_bytes": F, "l2": "flushed (256 MiB write) before every step"},
+        "kernels": kernels,
+        "roofline": roof,
+        "e2e": {"value": round(2 * n / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+                "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "path": "encode_payload/decode_payload (C ABI) with pinned host buffers"},
+        "cpu_baseline": None if cpu_val is None else {
+            "value": round(cpu_val, 4), "unit": "GB/s", "cores": 1, "kind": "port",
+            "sample": f"full workload ({n} elements) x {args.cpu_reps}, oracle/fc2_oracle.py "
+                      f"(numpy restatement of codec.py), {cpu_dt:.2f} s per round trip"},
+        "sweep": sweep,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm, N > 1: SPMD two-step AllReduce over NVLink
+# ---------------------------------------------------------------------------
+
+
+def run_allreduce(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2508_03760_b200 as fc
+    from paper_2508_03760_b200 import dist as fcd
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist.init_process_group("nccl", device_id=dev)
+    sr = args.scheme == "sr"
+    cfg = fc.QuantConfig(args.bits, group_size=args.group, chunk_size=args.group,
+                         scheme=fc.Scheme.SPIKE_RESERVING if sr else fc.Scheme.RTN)
+    n = args.n
+    x = spiky_bf16(n, 1000 + rank, dev)
+    comm = fcd.QComm(dist.group.WORLD, max_elems=n, config=cfg)
+    y = torch.empty_like(x)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def timed(fn, steps, warmup):
+        for _ in range(warmup):
+            flush.zero_()
+            fn()
+        torch.cuda.synchronize()
+        tot = 0.0
+        for _ in range(steps):
+            flush.zero_()
+            dist.barrier()
+            torch.cuda.synchronize()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            fn()
+            e.record()
+            torch.cuda.synchronize()
+            tot += s.elapsed_time(e)
+        t = torch.tensor([tot / steps], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    lib = fc._lib.lib()
+    l0 = lib.fc2_launch_count()
+    with ClockSampler(local_rank) as clk:
+        ms = timed(lambda: comm.all_reduce(x, out=y), args.steps, args.warmup)
+    launches = lib.fc2_launch_count() - l0
+    xb = x.clone()
+    ms_nccl = timed(lambda: dist.all_reduce(xb), args.steps, args.warmup)
+    # e2e: pinned host in -> allreduce -> host out
+    xh = x.cpu().pin_memory()
+    yh = torch.empty_like(xh).pin_memory()
+    xd = torch.empty_like(x)
+
+    def e2e():
+        xd.copy_(xh, non_blocking=True)
+        comm.all_reduce(xd, out=y)
+        yh.copy_(y, non_blocking=True)
+
+    ms_e2e = timed(e2e, max(3, args.steps), 2)
+    if rank == 0:
+        algbw = 2 * n / (ms * 1e-3) / 1e9
+        F = fc.footprint_bytes(cfg, comm.shard_len)
+        line = {
+            "metric": METRIC,
+            "value": round(algbw * world, 2),
+            "unit": "GB/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms, 5),
+            "latency_us": round(ms * 1e3, 2),
+            "per_rank_algbw_GBps": round(algbw, 2),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "bf16 in/out, fp32 reduce, packed u8 planes",
+            "data": "synthetic spiky bf16 per rank",
+            "config": {"workload": "two-step quantized AllReduce, 8192x4096 bf16 per rank (BASELINE configs[2])",
+                       "n": n, "bits": args.bits, "group": args.group, "scheme": args.scheme,
+                       "l2": "flushed before every step", "parallelism": f"tp{world}"},
+            "nccl_bf16": {"ms": round(ms_nccl, 5), "algbw_GBps": round(2 * n / (ms_nccl * 1e-3) / 1e9, 2),
+                          "speedup": round(ms_nccl / ms, 3),
+                          "nvls_env": os.environ.get("NCCL_NVLS_ENABLE", "default")},
+            "roofline": {"bound": "nvlink", "unit": "GB/s",
+                         "achieved": round(2 * (world - 1) / world * F * world / (ms * 1e-3) / 1e9 / world, 2),
+                         "peak": 770.0, "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
+                         "frac": round(2 * (world - 1) / world * F * world / (ms * 1e-3) / 1e9 / world / 770.0, 4),
+                         "traffic": None},
+            "e2e": {"value": round(2 * n * world / (ms_e2e * 1e-3) / 1e9, 2), "unit": "GB/s",
+                    "ms_per_step": round(ms_e2e, 4), "h2d_bytes_per_step": 2 * n, "d2h_bytes_per_step": 2 * n},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    comm.close()
+    dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    sr = args.scheme == "sr"
+    n_sample = args.ref_sample
+    times = []
+    from oracle import fc2_oracle as O
+    import numpy as np
+
+    if world > 1:
+        # two-step AllReduce of the oracle on a bounded per-rank sample
+        payloads = [O.bf16_snap(O.spiky(n_sample, s)).astype(np.float32) for s in O.child_seeds(0, world)]
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            O.two_step(payloads, args.bits, args.group, sr)
+            if i >= args.warmup:
+                times.append(time.perf_counter() - t0)
+        dt = statistics.mean(times)
+        value = 2 * n_sample * world / dt / 1e9
+        what = f"oracle two_step over {world} simulated ranks x {n_sample} elements"
+    else:
+        x = O.bf16_snap(O.spiky(n_sample, 0)).astype(np.float32)
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            planes, meta = O.encode(x, args.bits, args.group, sr)
+            O.decode(planes, meta, n_sample, args.bits, args.group, sr)
+            if i >= args.warmup:
+                times.append(time.perf_counter() - t0)
+        dt = statistics.mean(times)
+        value = 2 * n_sample / dt / 1e9
+        what = f"oracle encode+decode of {n_sample} bf16 elements"
+    cb = {"value": round(value, 5), "unit": "GB/s", "cores": 1, "kind": "port",
+          "sample": what + " (numpy restatement of the pure-Python reference; numpy elementwise is single-threaded)"}
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": cb["value"],
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(dt * 1e3, 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64 codec math (numpy), fp32 reduce",
+        "data": "synthetic spiky bf16",
+        "config": {"workload": ("two-step quantized AllReduce" if world > 1 else "codec round trip"),
+                   "n": n_sample, "bits": args.bits, "group": args.group, "scheme": args.scheme},
+        "cpu_baseline": cb,
+        "e2e": {"value": cb["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--bits", type=int, default=4)
+    ap.add_argument("--group", type=int, default=128)
+    ap.add_argument("--scheme", choices=["sr", "rtn"], default="sr")
+    ap.add_argument("--n", type=int, default=N_ELEMS)
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--cpu-reps", type=int, default=2)
+    ap.add_argument("--ref-sample", type=int, default=1 << 22)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        run_allreduce(args, rank, world, local_rank)
+    else:
+        run_codec(args)
+
+
+if __name__ == "__main__":
+    main()

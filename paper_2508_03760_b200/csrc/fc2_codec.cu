@@ -276,7 +276,9 @@ int fc2_encode_batch(const fc2_config* cfg, int32_t x_dtype, int32_t njobs, cons
     j.n_valid = n_valid[i];
     j.n = n[i];
     j.t0 = b->total;
-    b->total += use_fast ? (n[i] + 1023) / 1024 : n[i] / G;
+    // fast tiles: bf16 -> 32 groups per warp tile (lane per group); f32 -> 1024 elements
+    const int64_t tile = x_dtype == FC2_BF16 ? 32 * (int64_t)G : 1024;
+    b->total += use_fast ? (n[i] + tile - 1) / tile : n[i] / G;
     (void)esz;
   }
   if (fast.nj) {
@@ -311,7 +313,10 @@ int fc2_decode_batch(const fc2_config* cfg, int32_t y_dtype, int32_t njobs, cons
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   const int B = cfg->bitwidth, G = cfg->group_size;
-  const bool fastG = G % 32 == 0 && y_dtype != FC2_F64;
+  // fast decode: G % 32 == 0, bf16/f32 output, payloads 16-byte aligned
+  bool fastG = y_dtype != FC2_F64 && G % 32 == 0;
+  for (int i = 0; i < njobs; ++i)
+    if (reinterpret_cast<uintptr_t>(payloads[i]) & 15u) fastG = false;
   DecBatch b;
   b.nj = 0; b.B = B; b.G = G; b.sr = cfg->scheme == 1; b.intlog = cfg->scale_encoding; b.theta = cfg->theta;
   b.total = 0; b.lut = lut; b.err = dev_err;

@@ -7,6 +7,7 @@
 
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <stdint.h>
 
 #include "../../include/fc2.h"
@@ -87,6 +88,100 @@ __device__ __forceinline__ double rha(double x) {
 }
 
 // ---------------------------------------------------------------------------
+// fp32 code estimate with a 14-bit fixed-point fraction:
+//   y = (v - off) * inv + (0.5 + 8*2^-14) + 512
+// lands in [512, 1024) where the float32 ulp is 2^-14, so bits(y) holds
+// floor(q + 0.5 + 8u) in bits [14, 22) and the fraction in bits [0, 14).
+// When bits [4, 14) are all zero the element is within 8u of a rounding tie
+// and is recomputed exactly in float64; the estimate error is < 2.2e-4 < 7.5u,
+// so every other element provably gets the reference's float64 code.
+// ---------------------------------------------------------------------------
+
+constexpr int kFixBits = 14;
+constexpr float kFixC = 0.5f + 8.0f / 16384.0f;
+constexpr float kFixMagic = 512.0f;
+constexpr float kFixCM = 512.5f + 8.0f / 16384.0f;  // exactly representable
+constexpr uint32_t kTieMask = 0x3FF0u;
+constexpr float kFoldLimit = 1024.0f;               // |off * inv| bound for the folded form
+
+__device__ __forceinline__ uint32_t fix_est(float v, float off32, float inv32) {
+  float d = __fsub_rn(v, off32);
+  float f = __fmaf_rn(d, inv32, kFixC);
+  return __float_as_uint(__fadd_rn(f, kFixMagic));
+}
+__device__ __forceinline__ uint32_t fix_est_clamped(float v, float off32, float inv32, float Lh) {
+  float d = __fsub_rn(v, off32);
+  float f = __fmaf_rn(d, inv32, kFixC);
+  f = fminf(fmaxf(f, kFixC), Lh);  // codes may legitimately clip at both ends
+  return __float_as_uint(__fadd_rn(f, kFixMagic));
+}
+__device__ __forceinline__ bool fix_is_tie(uint32_t X) { return (X & kTieMask) == 0u; }
+
+// Fixed-point parameters by fraction width: 16 bits when codes fit 7 bits
+// (y in [128, 256), code = byte 2 of bits(y)), 14 bits for 8-bit codes.
+template <int FB>
+struct Fix;
+template <>
+struct Fix<14> {
+  static constexpr int kBits = 14;
+  static constexpr float kC = 0.5f + 8.0f / 16384.0f;
+  static constexpr float kM = 512.0f;
+  static constexpr float kCM = 512.5f + 8.0f / 16384.0f;
+  static constexpr uint32_t kTie = 0x3FF0u;
+  static constexpr float kFold = 1024.0f;
+};
+// 15-bit fraction: y in [256, 512), code in bits [15, 23), fraction bits
+// [0, 15); the tie test (bits [4, 15) zero) never touches bit 15, so packed
+// f16 zero tests on fraction pairs are exact.
+template <>
+struct Fix<15> {
+  static constexpr int kBits = 15;
+  static constexpr float kC = 0.5f + 8.0f / 32768.0f;
+  static constexpr float kM = 256.0f;
+  static constexpr float kCM = 256.5f + 8.0f / 32768.0f;
+  static constexpr uint32_t kTie = 0x7FF0u;
+  static constexpr float kFold = 512.0f;
+};
+template <int B>
+struct FixFor {
+  static constexpr int FB = 15;
+};
+
+template <int FB>
+__device__ __forceinline__ uint32_t fixq_clamped(float v, float off32, float inv32, float Lh) {
+  float d = __fsub_rn(v, off32);
+  float f = __fmaf_rn(d, inv32, Fix<FB>::kC);
+  f = fminf(fmaxf(f, Fix<FB>::kC), Lh);
+  return __float_as_uint(__fadd_rn(f, Fix<FB>::kM));
+}
+
+// tie mask bits for a pair of fixed-point words: bit `pp` for X0 and bit
+// `16 + pp` for X1 when the fraction is within 8 ulps of a rounding tie
+template <int FB>
+__device__ __forceinline__ uint32_t pair_tie_bits(uint32_t X0, uint32_t X1, int pp) {
+  uint32_t fr = __byte_perm(X0, X1, 0x5410) & (Fix<FB>::kTie | (Fix<FB>::kTie << 16));
+  __half2 h = *reinterpret_cast<const __half2*>(&fr);
+  return __heq2_mask(h, __float2half2_rn(0.0f)) & (0x00010001u << pp);
+}
+
+// packed float32x2 arithmetic (sm_100: FFMA2 / FADD2)
+__device__ __forceinline__ void fma2(float& r0, float& r1, float a0, float a1, float b0, float b1, float c0,
+                                     float c1) {
+  asm("{\n\t.reg .b64 a, b, c, d;\n\t"
+      "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\tmov.b64 c, {%6, %7};\n\t"
+      "fma.rn.f32x2 d, a, b, c;\n\tmov.b64 {%0, %1}, d;\n\t}"
+      : "=f"(r0), "=f"(r1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
+}
+__device__ __forceinline__ void add2(float& r0, float& r1, float a0, float a1, float b0, float b1) {
+  asm("{\n\t.reg .b64 a, b, d;\n\t"
+      "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "add.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
+      : "=f"(r0), "=f"(r1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+
+// ---------------------------------------------------------------------------
 // per-group parameters (codec.py:454-474, 512; R6, R7, R13)
 // ---------------------------------------------------------------------------
 
@@ -95,6 +190,8 @@ struct GroupParams {
   double div;        // code divisor: scale (BF16) or s_eff (INT_LOG); 0 => codes 0
   float off32;       // fast-path float copies
   float inv32;
+  float nz;          // -off32 * inv32 (folded form: q ~ fma(v, inv32, nz))
+  bool fold;         // |nz| small enough for the folded form
   bool exact;        // range too small/large for the fp32 estimate: exact f64 for all
   uint32_t sz;       // BF16: scale_bits | zero_bits << 16 ; INT_LOG: (u8)si | (u8)zi << 8
 };
@@ -139,33 +236,10 @@ __device__ __forceinline__ GroupParams group_params(double zero, double vmax, in
     p.off32 = 0.f;
     p.inv32 = 0.f;
   }
+  p.nz = -__fmul_rn(p.off32, p.inv32);
+  p.fold = !p.exact && fabsf(p.nz) <= kFoldLimit;
   return p;
 }
-
-// ---------------------------------------------------------------------------
-// fp32 code estimate with a 10-bit fixed-point fraction:
-// y = fma(v - off, inv, 0.5 + 2^-9) + 1.5*2^13 puts floor(q + 0.5 + 2^-9) in
-// bits [10, 18) and the fraction in bits [0, 10).  Whenever bits [2,10) are
-// all zero the element is within 2^-9 of a rounding tie and is recomputed
-// exactly in float64 (the estimate error is < 1e-4, so every other element is
-// provably identical to the reference's float64 result).
-// ---------------------------------------------------------------------------
-
-constexpr float kFixC = 0.5f + 1.0f / 512.0f;
-constexpr float kFixMagic = 12288.0f;  // 1.5 * 2^13: ulp 2^-10 over [8192, 16384)
-
-__device__ __forceinline__ uint32_t fix_est(float v, float off32, float inv32) {
-  float d = __fsub_rn(v, off32);
-  float f = __fmaf_rn(d, inv32, kFixC);
-  return __float_as_uint(__fadd_rn(f, kFixMagic));
-}
-__device__ __forceinline__ uint32_t fix_est_clamped(float v, float off32, float inv32, float Lh) {
-  float d = __fsub_rn(v, off32);
-  float f = __fmaf_rn(d, inv32, kFixC);
-  f = fminf(fmaxf(f, kFixC), Lh);  // INT_LOG codes may legitimately clip at both ends
-  return __float_as_uint(__fadd_rn(f, kFixMagic));
-}
-__device__ __forceinline__ bool fix_is_tie(uint32_t X) { return (X & 0x3FCu) == 0u; }
 
 // ---------------------------------------------------------------------------
 // misc

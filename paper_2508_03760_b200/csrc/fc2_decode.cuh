@@ -114,6 +114,27 @@ __device__ __forceinline__ void load_codes32(const uint8_t* payload, int64_t n, 
   }
 }
 
+// 32 decoded float32 values of one run (BF16 metadata: code*s + z as one
+// FMA; codes become floats exactly via the 2^23 magic), packed f32x2 math.
+template <int B>
+__device__ __forceinline__ void dq_run32(const uint8_t* payload, int64_t n, int64_t e0, const GroupMeta& m,
+                                         bool intlog, float* v) {
+  uint32_t c[32];
+  load_codes32<B>(payload, n, e0, c);
+  if (!intlog) {
+#pragma unroll
+    for (int k = 0; k < 32; k += 2) {
+      float a, b;
+      add2(a, b, __uint_as_float(0x4B000000u | c[k]), __uint_as_float(0x4B000000u | c[k + 1]), -8388608.0f,
+           -8388608.0f);
+      fma2(v[k], v[k + 1], a, b, m.s32, m.s32, m.z32, m.z32);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 32; ++k) v[k] = __double2float_rn(__dadd_rn(__dmul_rn((double)c[k], m.s64), m.o64));
+  }
+}
+
 // Code of one element (generic path, any alignment).
 __device__ __forceinline__ uint32_t load_code1(const uint8_t* payload, int64_t n, int64_t e, int B) {
   uint32_t c = 0;

@@ -69,21 +69,21 @@ struct Bf16Vals {  // w[k] = elements (2k, 2k+1) as packed bf16x2
     mx1 = fmax_nan(l1, h1);
     mx2 = fmax_nan(fmin_nan(l1, h1), fmax_nan(l2, h2));
   }
-  // bit k set <=> element k == m (float equality: -0 == +0, codec.py:261-262)
-  __device__ __forceinline__ uint32_t eq_mask(float m) const {
+  // first k with element k == m (float equality: -0 == +0, codec.py:261-262), 64 if none
+  __device__ __forceinline__ int first_eq(float m) const {
     __nv_bfloat162 mm = __float2bfloat162_rn(m);  // m is a bf16 value: exact
-    uint32_t lo = 0, hi = 0;
+    uint32_t msk = 0;  // bit k: element 2k matches; bit 16+k: element 2k+1 matches
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      uint32_t e = __heq2_mask(*reinterpret_cast<const __nv_bfloat162*>(&w[k]), mm);
-      lo |= (e & 1u) << k;
-      hi |= ((e >> 16) & 1u) << k;
-    }
-    // interleave: element 2k <- lo bit k, element 2k+1 <- hi bit k
-    uint32_t r = 0;
-#pragma unroll
-    for (int k = 0; k < 16; ++k) r |= (((lo >> k) & 1u) << (2 * k)) | (((hi >> k) & 1u) << (2 * k + 1));
-    return r;
+    for (int k = 0; k < 16; ++k)
+      msk |= __heq2_mask(*reinterpret_cast<const __nv_bfloat162*>(&w[k]), mm) & (0x00010001u << k);
+    const uint32_t lo = msk & 0xFFFFu, hi = msk >> 16;
+    const int fl = lo ? 2 * (__ffs(lo) - 1) : 64;
+    const int fh = hi ? 2 * (__ffs(hi) - 1) + 1 : 64;
+    return min(fl, fh);
+  }
+  __device__ __forceinline__ void pair(int k, float& a, float& b) const {
+    a = __uint_as_float(w[k] << 16);
+    b = __uint_as_float(w[k] & 0xFFFF0000u);
   }
 };
 
@@ -116,11 +116,15 @@ struct F32Vals {
       mx1 = fmax_nan(mx1, x);
     }
   }
-  __device__ __forceinline__ uint32_t eq_mask(float m) const {
+  __device__ __forceinline__ int first_eq(float m) const {
     uint32_t r = 0;
 #pragma unroll
     for (int k = 0; k < 32; ++k) r |= (f[k] == m ? 1u : 0u) << k;
-    return r;
+    return r ? __ffs(r) - 1 : 64;
+  }
+  __device__ __forceinline__ void pair(int k, float& a, float& b) const {
+    a = f[2 * k];
+    b = f[2 * k + 1];
   }
 };
 
@@ -137,14 +141,28 @@ struct LaneWords {
 #pragma unroll
     for (int i = 0; i < B; ++i) w[i] = 0;
   }
-  // insert code bits from the fixed-point word X (code in bits [10,18))
+  // insert code bits from the fixed-point word X (code in bits [kFixBits, kFixBits+8))
   __device__ __forceinline__ void put_fix(int k, uint32_t X) {
 #pragma unroll
     for (int u = 0; u < NU; ++u) {
       const int W = unit_w(B, u), O = unit_off(B, u);
       const int wi = (k * W) >> 5, pos = (k * W) & 31;
       const uint32_t m = (1u << W) - 1u;
-      const int sh = pos - (10 + O);
+      const int sh = pos - (kFixBits + O);
+      uint32_t t = sh >= 0 ? (X << sh) : (X >> (-sh));
+      w[base(u) + wi] |= t & (m << pos);
+    }
+  }
+  // same with an explicit fraction width FB (code in bits [FB, FB+8))
+  template <int FB>
+  __device__ __forceinline__ void put_fixb(int k, uint32_t X, int u0 = 0) {
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+      if (u < u0) continue;
+      const int W = unit_w(B, u), O = unit_off(B, u);
+      const int wi = (k * W) >> 5, pos = (k * W) & 31;
+      const uint32_t m = (1u << W) - 1u;
+      const int sh = pos - (FB + O);
       uint32_t t = sh >= 0 ? (X << sh) : (X >> (-sh));
       w[base(u) + wi] |= t & (m << pos);
     }
@@ -234,9 +252,9 @@ __device__ __forceinline__ void encode_lane(const V& v, bool active, int64_t e0,
   int imin = 0, imax = 1;
   uint32_t smin_bits = 0, smax_bits = 0;
   if constexpr (SR) {
-    uint32_t em = v.eq_mask(mn1), eM = v.eq_mask(mx1);
-    int fi = em ? lig * 32 + __ffs(em) - 1 : 1 << 20;
-    int fa = eM ? lig * 32 + __ffs(eM) - 1 : 1 << 20;
+    const int li = v.first_eq(mn1), la = v.first_eq(mx1);
+    int fi = li < 32 ? lig * 32 + li : 1 << 20;
+    int fa = la < 32 ? lig * 32 + la : 1 << 20;
 #pragma unroll
     for (int o = 1; o < TPG; o <<= 1) {
       fi = min(fi, __shfl_xor_sync(0xffffffffu, fi, o));
@@ -272,11 +290,35 @@ __device__ __forceinline__ void encode_lane(const V& v, bool active, int64_t e0,
   lw.clear();
   uint32_t tie = 0;
   if (!cx.intlog) {
+    // warp-uniform choice between the folded form q ~ fma(v, inv, -off*inv)
+    // (2 packed ops per pair) and the explicit v - off form (3 packed ops)
+    if (__all_sync(0xffffffffu, p.fold || p.exact || !active)) {
 #pragma unroll
-    for (int k = 0; k < 32; ++k) {
-      uint32_t X = fix_est(v.get(k), p.off32, p.inv32);
-      tie |= (fix_is_tie(X) ? 1u : 0u) << k;
-      lw.put_fix(k, X);
+      for (int k = 0; k < 16; ++k) {
+        float a, b, t0, t1, y0, y1;
+        v.pair(k, a, b);
+        fma2(t0, t1, a, b, p.inv32, p.inv32, p.nz, p.nz);
+        add2(y0, y1, t0, t1, kFixCM, kFixCM);
+        const uint32_t X0 = __float_as_uint(y0), X1 = __float_as_uint(y1);
+        tie |= (fix_is_tie(X0) ? 1u : 0u) << (2 * k);
+        tie |= (fix_is_tie(X1) ? 1u : 0u) << (2 * k + 1);
+        lw.put_fix(2 * k, X0);
+        lw.put_fix(2 * k + 1, X1);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        float a, b, d0, d1, t0, t1, y0, y1;
+        v.pair(k, a, b);
+        add2(d0, d1, a, b, -p.off32, -p.off32);
+        fma2(t0, t1, d0, d1, p.inv32, p.inv32, kFixC, kFixC);
+        add2(y0, y1, t0, t1, kFixMagic, kFixMagic);
+        const uint32_t X0 = __float_as_uint(y0), X1 = __float_as_uint(y1);
+        tie |= (fix_is_tie(X0) ? 1u : 0u) << (2 * k);
+        tie |= (fix_is_tie(X1) ? 1u : 0u) << (2 * k + 1);
+        lw.put_fix(2 * k, X0);
+        lw.put_fix(2 * k + 1, X1);
+      }
     }
   } else {
     const float Lh = (float)L + 0.5f;
@@ -295,7 +337,10 @@ __device__ __forceinline__ void encode_lane(const V& v, bool active, int64_t e0,
     lw.patch(k, exact_code((double)v.get_dyn(k), p.off, p.div, L));
   }
   if constexpr (SR) {  // reserved slots are quantized as 0.0 (codec.py:494-496)
-    const int sc = exact_code(0.0, p.off, p.div, L);
+    int sc;
+    const uint32_t Xs = fix_est_clamped(0.0f, p.off32, p.inv32, (float)L + 0.5f);
+    if (p.exact || fix_is_tie(Xs)) sc = exact_code(0.0, p.off, p.div, L);
+    else sc = (int)((Xs >> kFixBits) & (uint32_t)L);
     if (lig == (imin >> 5)) lw.patch(imin & 31, sc);
     if (lig == (imax >> 5)) lw.patch(imax & 31, sc);
   }

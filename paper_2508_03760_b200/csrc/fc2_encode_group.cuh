@@ -1,0 +1,390 @@
+// fc2_encode_group.cuh -- lane-per-group encoder (the production fast path).
+//
+// A warp tile is 32 consecutive groups; lane l owns group l of the tile
+// entirely, so every per-group step (statistics, spike search, scale/zero,
+// metadata, tie resolution) runs once per G elements with no shuffles.
+//
+//   global --cp.async--> input stage (swizzled 16-byte chunks, 2 stages)
+//   pass 1  stats       packed bf16x2 min/max (top-2 for spike reserving)
+//   pass 2  spikes      first argmin / argmax via packed equality masks
+//   pass 3  codes       fp32x2 fixed-point estimate -> packed plane words ->
+//                       output stage (smem); near-tie elements recomputed in
+//                       float64 and patched in smem; spike slots patched
+//   copy-out            coalesced 16-byte stores of each plane segment,
+//                       metadata records straight from the owning lane
+//
+// Contract: SURVEY 8.0 R1-R11/R13 (codec.py:477-519), same as encode_lane.
+#pragma once
+
+#include "fc2_encode.cuh"
+
+namespace fc2 {
+
+template <typename T, int G>
+struct GTile {
+  static constexpr int CPG = G * (int)sizeof(T) / 16;   // input chunks per group
+  static constexpr int IN_BYTES = 32 * G * (int)sizeof(T);
+  // input swizzle: chunk c of group g -> slot g*CPG + (c ^ (g & m)), m < 8
+  static constexpr int IM = CPG >= 8 ? 7 : CPG - 1;
+  __device__ static __forceinline__ int in_pos(int g, int c) {
+    return g * CPG + (c ^ (CPG >= 8 ? (g & 7) : ((g >> (CPG == 4 ? 1 : (CPG == 2 ? 2 : 3))) & IM)));
+  }
+};
+
+// output staging for one unit of width W: the tile's plane segment
+// (32 * G * W / 8 bytes) in 16-byte chunks, swizzled when a group owns >= 1 chunk
+template <int G, int W>
+struct OTile {
+  static constexpr int GB = G * W / 8;                 // bytes per group
+  static constexpr int CPG = GB >= 16 ? GB / 16 : 0;   // chunks per group (0: linear)
+  static constexpr int BYTES = 32 * GB;
+  __device__ static __forceinline__ int chunk_pos(int g, int c) {
+    if constexpr (CPG == 0) {
+      return 0;
+    } else if constexpr (CPG >= 8) {
+      return g * CPG + (c ^ (g & 7));
+    } else {
+      constexpr int sh = CPG == 4 ? 1 : (CPG == 2 ? 2 : 3);
+      return g * CPG + (c ^ ((g >> sh) & (CPG - 1)));
+    }
+  }
+  // byte address of byte `b` of group g's segment
+  __device__ static __forceinline__ int byte_pos(int g, int b) {
+    if constexpr (CPG == 0) return g * GB + b;
+    else return chunk_pos(g, b >> 4) * 16 + (b & 15);
+  }
+  // linear chunk t of the tile segment -> its slot
+  __device__ static __forceinline__ int lin_pos(int t) {
+    if constexpr (CPG == 0) return t * 16;
+    else return chunk_pos(t / CPG, t % CPG) * 16;
+  }
+};
+
+template <int B, int G>
+struct OutStage {
+  static constexpr int NU = n_units(B);
+  __host__ __device__ static constexpr int off(int u) {
+    return u == 0 ? 0 : off(u - 1) + 32 * G * unit_w(B, u - 1) / 8;
+  }
+  static constexpr int BYTES = 32 * G * B / 8;
+};
+
+// patch element e (group-relative) of lane g with code c in the output stage
+template <int B, int G>
+__device__ __forceinline__ void stage_patch(uint8_t* ost, int g, int e, int c) {
+#pragma unroll
+  for (int u = 0; u < n_units(B); ++u) {
+    const int W = unit_w(B, u), O = unit_off(B, u);
+    const int bit = e * W;
+    uint8_t* p;
+    if (W == 1) p = ost + OutStage<B, G>::off(u) + OTile<G, 1>::byte_pos(g, bit >> 3);
+    else if (W == 2) p = ost + OutStage<B, G>::off(u) + OTile<G, 2>::byte_pos(g, bit >> 3);
+    else if (W == 4) p = ost + OutStage<B, G>::off(u) + OTile<G, 4>::byte_pos(g, bit >> 3);
+    else p = ost + OutStage<B, G>::off(u) + OTile<G, 8>::byte_pos(g, bit >> 3);
+    const uint32_t m = ((1u << W) - 1u) << (bit & 7);
+    const uint32_t v = (((uint32_t)c >> O) << (bit & 7)) & m;
+    *p = (uint8_t)((*p & ~m) | v);
+  }
+}
+
+// write one 32-element run's words (unit u) of group g into the output stage
+template <int G, int W>
+__device__ __forceinline__ void stage_words(uint8_t* base, int g, int run, const uint32_t* w) {
+  // run r covers bytes [r*4W, r*4W + 4W) of the group segment
+  const int b0 = run * 4 * W;
+  if constexpr (OTile<G, W>::CPG == 0 || W < 4) {
+#pragma unroll
+    for (int i = 0; i < W; ++i)
+      *reinterpret_cast<uint32_t*>(base + OTile<G, W>::byte_pos(g, b0 + 4 * i)) = w[i];
+  } else {
+#pragma unroll
+    for (int i = 0; i < W; i += 4)
+      *reinterpret_cast<uint4*>(base + OTile<G, W>::byte_pos(g, b0 + 4 * i)) =
+          make_uint4(w[i], w[i + 1], w[i + 2], w[i + 3]);
+  }
+}
+
+// copy the tile's unit segment (ng groups) from the stage to global, coalesced
+template <int G, int W>
+__device__ __forceinline__ void copy_out(const uint8_t* base, uint8_t* dst, int ng) {
+  const int lane = (int)lane_id();
+  const int bytes = ng * OTile<G, W>::GB;
+  if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0 && (bytes & 15) == 0) {
+    for (int t = lane; t < bytes / 16; t += 32)
+      *reinterpret_cast<uint4*>(dst + 16 * t) = *reinterpret_cast<const uint4*>(base + OTile<G, W>::lin_pos(t));
+  } else {
+    for (int t = lane; t < bytes / 4; t += 32) {
+      const int lp = OTile<G, W>::lin_pos(t >> 2) + 4 * (t & 3);
+      *reinterpret_cast<uint32_t*>(dst + 4 * t) = *reinterpret_cast<const uint32_t*>(base + lp);
+    }
+  }
+}
+
+// ---- per-chunk helpers on 16-byte chunks -----------------------------------
+
+struct TopState {  // packed bf16x2 running statistics (two independent streams)
+  __nv_bfloat162 a1, a2, b1, b2;
+};
+
+__device__ __forceinline__ void top_init(TopState& s, uint32_t w0) {
+  s.a1 = *reinterpret_cast<const __nv_bfloat162*>(&w0);
+  s.b1 = s.a1;
+  const uint32_t pinf = 0x7F807F80u, ninf = 0xFF80FF80u;
+  s.a2 = *reinterpret_cast<const __nv_bfloat162*>(&pinf);
+  s.b2 = *reinterpret_cast<const __nv_bfloat162*>(&ninf);
+}
+
+template <bool SR>
+__device__ __forceinline__ void top_add(TopState& s, uint32_t w) {
+  const __nv_bfloat162 x = *reinterpret_cast<const __nv_bfloat162*>(&w);
+  if constexpr (SR) {
+    s.a2 = __hmin2_nan(s.a2, __hmax2_nan(s.a1, x));
+    s.b2 = __hmax2_nan(s.b2, __hmin2_nan(s.b1, x));
+  }
+  s.a1 = __hmin2_nan(s.a1, x);
+  s.b1 = __hmax2_nan(s.b1, x);
+}
+
+template <bool SR>
+__device__ __forceinline__ void top_final(const TopState& s, float& mn1, float& mn2, float& mx1, float& mx2) {
+  float l1 = __low2float(s.a1), h1 = __high2float(s.a1);
+  mn1 = fmin_nan(l1, h1);
+  float L1 = __low2float(s.b1), H1 = __high2float(s.b1);
+  mx1 = fmax_nan(L1, H1);
+  if constexpr (SR) {
+    mn2 = fmin_nan(fmax_nan(l1, h1), fmin_nan(__low2float(s.a2), __high2float(s.a2)));
+    mx2 = fmax_nan(fmin_nan(L1, H1), fmax_nan(__low2float(s.b2), __high2float(s.b2)));
+  } else {
+    mn2 = mn1;
+    mx2 = mx1;
+  }
+}
+
+// pass 3 for all runs of the lane's group with the code form fixed at compile
+// time (MODE 0: folded fma, 1: explicit v - off, 2: INT_LOG clamped).
+// Writes packed words into the output stage, returns per-run tie masks in
+// split layout (bit i < 16: element 2i; bit 16 + i: element 2i + 1).
+template <int B, int G, int MODE>
+__device__ __forceinline__ void quant_runs(const uint8_t* ist, uint8_t* ost, const GroupParams& p, float Lh,
+                                           bool active) {
+  using IT = GTile<__nv_bfloat16, G>;
+  constexpr int RUNS = G / 32;
+  constexpr int FB = FixFor<B>::FB;
+  using FX = Fix<FB>;
+  const int lane = (int)lane_id();
+  constexpr int L = (1 << B) - 1;
+#pragma unroll 1
+  for (int r = 0; r < RUNS; ++r) {
+    LaneWords<B> lw;
+    lw.clear();
+    uint32_t tm = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint4 q = *reinterpret_cast<const uint4*>(ist + IT::in_pos(lane, 4 * r + j) * 16);
+      const uint32_t ww[4] = {q.x, q.y, q.z, q.w};
+      uint32_t X[8];
+#pragma unroll
+      for (int pp = 0; pp < 4; ++pp) {
+        const float a = __uint_as_float(ww[pp] << 16), b = __uint_as_float(ww[pp] & 0xFFFF0000u);
+        float y0, y1;
+        if constexpr (MODE == 0) {
+          float t0, t1;
+          fma2(t0, t1, a, b, p.inv32, p.inv32, p.nz, p.nz);
+          add2(y0, y1, t0, t1, FX::kCM, FX::kCM);
+        } else if constexpr (MODE == 1) {
+          float d0, d1, t0, t1;
+          add2(d0, d1, a, b, -p.off32, -p.off32);
+          fma2(t0, t1, d0, d1, p.inv32, p.inv32, FX::kC, FX::kC);
+          add2(y0, y1, t0, t1, FX::kM, FX::kM);
+        } else {
+          y0 = __uint_as_float(fixq_clamped<FB>(a, p.off32, p.inv32, Lh));
+          y1 = __uint_as_float(fixq_clamped<FB>(b, p.off32, p.inv32, Lh));
+        }
+        X[2 * pp] = __float_as_uint(y0);
+        X[2 * pp + 1] = __float_as_uint(y1);
+        tm |= pair_tie_bits<FB>(X[2 * pp], X[2 * pp + 1], 4 * j + pp);
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) lw.template put_fixb<FB>(8 * j + e, X[e], 0);
+    }
+#pragma unroll
+    for (int u = 0; u < n_units(B); ++u) {
+      const int W = unit_w(B, u);
+      uint8_t* base = ost + OutStage<B, G>::off(u);
+      const uint32_t* w = lw.w + LaneWords<B>::base(u);
+      if (W == 1) stage_words<G, 1>(base, lane, r, w);
+      else if (W == 2) stage_words<G, 2>(base, lane, r, w);
+      else if (W == 4) stage_words<G, 4>(base, lane, r, w);
+      else stage_words<G, 8>(base, lane, r, w);
+    }
+    // exact float64 recompute of near-tie elements (rare), patched in smem;
+    // split layout: bit i < 16 -> element 2i, bit 16 + i -> element 2i + 1
+    tm = (p.exact ? 0xffffffffu : tm) & (active ? 0xffffffffu : 0u);
+    while (tm) {
+      const int k = __ffs(tm) - 1;
+      tm &= tm - 1;
+      const int e = 32 * r + (k < 16 ? 2 * k : 2 * (k - 16) + 1);
+      const float v = __uint_as_float(
+          (uint32_t)*reinterpret_cast<const uint16_t*>(ist + IT::in_pos(lane, e >> 3) * 16 + (e & 7) * 2) << 16);
+      stage_patch<B, G>(ost, lane, e, exact_code((double)v, p.off, p.div, L));
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// the kernel body for one warp tile (bf16 input)
+// ---------------------------------------------------------------------------
+
+template <int B, bool SR, int G>
+__device__ __forceinline__ void encode_tile_bf16(const uint8_t* ist, uint8_t* ost, bool active, int64_t g_abs,
+                                                 const EncCtx& cx, uint8_t* out, int64_t tile_g0, int ng) {
+  using IT = GTile<__nv_bfloat16, G>;
+  constexpr int CPG = IT::CPG;  // 8 bf16 per chunk
+  constexpr int L = (1 << B) - 1;
+  const int lane = (int)lane_id();
+  auto chunk = [&](int c) -> uint4 { return *reinterpret_cast<const uint4*>(ist + IT::in_pos(lane, c) * 16); };
+
+  constexpr int RUNS = G / 32;
+  constexpr int FB = FixFor<B>::FB;
+  using FX = Fix<FB>;
+
+  // ---- pass 1: statistics; ra / rz = run where the running min / max last
+  // strictly improved == run holding the first occurrence of the extreme ----
+  TopState ts;
+  int ra = 0, rz = 0;
+  {
+    uint4 q = chunk(0);
+    top_init(ts, q.x);
+    top_add<SR>(ts, q.y); top_add<SR>(ts, q.z); top_add<SR>(ts, q.w);
+#pragma unroll
+    for (int j = 1; j < 4; ++j) {
+      q = chunk(j);
+      top_add<SR>(ts, q.x); top_add<SR>(ts, q.y); top_add<SR>(ts, q.z); top_add<SR>(ts, q.w);
+    }
+  }
+  float rmin = 0.f, rmax = 0.f;
+  if constexpr (SR) {
+    rmin = fmin_nan(__low2float(ts.a1), __high2float(ts.a1));
+    rmax = fmax_nan(__low2float(ts.b1), __high2float(ts.b1));
+  }
+#pragma unroll 1
+  for (int r = 1; r < RUNS; ++r) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint4 q = chunk(4 * r + j);
+      top_add<SR>(ts, q.x); top_add<SR>(ts, q.y); top_add<SR>(ts, q.z); top_add<SR>(ts, q.w);
+    }
+    if constexpr (SR) {
+      const float nmin = fmin_nan(__low2float(ts.a1), __high2float(ts.a1));
+      const float nmax = fmax_nan(__low2float(ts.b1), __high2float(ts.b1));
+      if (nmin < rmin) ra = r;
+      if (nmax > rmax) rz = r;
+      rmin = nmin;
+      rmax = nmax;
+    }
+  }
+  float mn1, mn2, mx1, mx2;
+  top_final<SR>(ts, mn1, mn2, mx1, mx2);
+  const bool finite = isfinite(mn1) && isfinite(mx1);
+  if (active && !finite) atomicOr(cx.err, FC2_ERR_NONFINITE);
+
+  // ---- spikes: first argmin / argmax (codec.py:259-266) ---------------------
+  // The running minimum first equals the group minimum in the run holding its
+  // first occurrence; only that run is searched.
+  int imin = 0, imax = 1;
+  uint32_t smin_bits = 0, smax_bits = 0;
+  if constexpr (SR) {
+    auto first_in_run = [&](int r, float m) -> int {
+      const __nv_bfloat162 mm = __float2bfloat162_rn(m);
+      uint32_t em = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint4 q = chunk(4 * r + j);
+        const uint32_t ww[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int pp = 0; pp < 4; ++pp)
+          em |= __heq2_mask(*reinterpret_cast<const __nv_bfloat162*>(&ww[pp]), mm) & (0x00010001u << (4 * j + pp));
+      }
+      const uint32_t lo = em & 0xFFFFu, hi = em >> 16;
+      const int f = min(lo ? 2 * (__ffs(lo) - 1) : 64, hi ? 2 * (__ffs(hi) - 1) + 1 : 64);
+      return f < 32 ? 32 * r + f : 1 << 20;
+    };
+    int fi = first_in_run(ra, mn1), fa = first_in_run(rz, mx1);
+    if (fi >= G) fi = 0;  // only with NaN input (already flagged)
+    if (fa >= G) fa = 1;
+    if (fi == fa) { fi = 0; fa = 1; }
+    imin = fi; imax = fa;
+    // reserved values are the elements themselves (codec.py:492-493)
+    auto elem = [&](int e) -> uint32_t {
+      return *reinterpret_cast<const uint16_t*>(ist + IT::in_pos(lane, e >> 3) * 16 + (e & 7) * 2);
+    };
+    smin_bits = elem(imin);
+    smax_bits = elem(imax);
+  }
+  const float zf = SR ? mn2 : mn1, vf = SR ? mx2 : mx1;
+  GroupParams p = group_params((double)zf, (double)vf, L, cx.intlog != 0, cx.theta, cx.lut,
+                               active ? cx.err : nullptr);
+
+  // ---- pass 3: codes -> output stage (+ exact recompute of near ties) --------
+  // 0: folded fma form, 1: explicit (v - off) form, 2: INT_LOG (clamped)
+  const bool fold_ok = !p.exact && fabsf(p.nz) <= FX::kFold;
+  const float Lh = (float)L + 0.5f;
+  if (cx.intlog) {
+    quant_runs<B, G, 2>(ist, ost, p, Lh, active);
+  } else if (__all_sync(0xffffffffu, fold_ok || p.exact || !active)) {
+    quant_runs<B, G, 0>(ist, ost, p, Lh, active);
+  } else {
+    quant_runs<B, G, 1>(ist, ost, p, Lh, active);
+  }
+  if constexpr (SR) {  // reserved slots are quantized as 0.0 (codec.py:494-496)
+    int sc;
+    const uint32_t Xs = fixq_clamped<FB>(0.0f, p.off32, p.inv32, (float)L + 0.5f);
+    if (p.exact || (Xs & FX::kTie) == 0u) sc = exact_code(0.0, p.off, p.div, L);
+    else sc = (int)((Xs >> FB) & (uint32_t)L);
+    if (active) {
+      stage_patch<B, G>(ost, lane, imin, sc);
+      stage_patch<B, G>(ost, lane, imax, sc);
+    }
+  }
+
+  // ---- metadata record (R10), straight from the owning lane ---------------
+  if (active) {
+    uint32_t rec[3];
+    int rb;
+    if (!cx.intlog) {
+      rec[0] = p.sz;
+      if constexpr (SR) {
+        rec[1] = smin_bits | (smax_bits << 16);
+        rec[2] = (__float_as_uint((float)imin) >> 16) | (__float_as_uint((float)imax) & 0xFFFF0000u);
+        rb = 12;
+      } else {
+        rb = 4;
+      }
+    } else {
+      if constexpr (SR) {
+        rec[0] = (p.sz & 0xFFFFu) | (smin_bits << 16);
+        rec[1] = smax_bits | ((uint32_t)imin << 16) | ((uint32_t)imax << 24);
+        rb = 8;
+      } else {
+        rec[0] = p.sz & 0xFFFFu;
+        rb = 2;
+      }
+    }
+    store_record(out + cx.meta_off + g_abs * rb, rec, rb);
+  }
+  __syncwarp();
+  // ---- coalesced copy-out of the plane segments ---------------------------
+#pragma unroll
+  for (int u = 0; u < n_units(B); ++u) {
+    const int W = unit_w(B, u), O = unit_off(B, u);
+    const uint8_t* base = ost + OutStage<B, G>::off(u);
+    uint8_t* dst = out + (cx.n * O) / 8 + tile_g0 * (G * W / 8);
+    if (W == 1) copy_out<G, 1>(base, dst, ng);
+    else if (W == 2) copy_out<G, 2>(base, dst, ng);
+    else if (W == 4) copy_out<G, 4>(base, dst, ng);
+    else copy_out<G, 8>(base, dst, ng);
+  }
+  __syncwarp();
+}
+
+}  // namespace fc2

@@ -7,6 +7,7 @@
 
 #include "fc2_decode.cuh"
 #include "fc2_encode.cuh"
+#include "fc2_encode_group.cuh"
 
 namespace fc2 {
 
@@ -191,6 +192,96 @@ __global__ void __launch_bounds__(kEncWarps * 32) k_encode_fast(const __grid_con
 }
 
 // ---------------------------------------------------------------------------
+// lane-per-group encoder (bf16 input, G in {32,64,128,256})
+// ---------------------------------------------------------------------------
+
+template <int G>
+__device__ __forceinline__ void issue_grp_tile(const EncBatch& b, int64_t t, uint8_t* stage) {
+  using IT = GTile<__nv_bfloat16, G>;
+  const int ji = find_job(b, t);
+  const EncJob& jb = b.j[ji];
+  const int64_t e0 = (t - jb.t0) * 32 * G;
+  const int lane = (int)lane_id();
+  const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(jb.x);
+  if (e0 + 32 * G <= jb.n_valid) {  // whole tile present: plain 16-byte copies
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(x + e0);
+#pragma unroll
+    for (int j = 0; j < IT::CPG; ++j) {
+      const int tc = lane + 32 * j;
+      cp_async16(stage + IT::in_pos(tc / IT::CPG, tc % IT::CPG) * 16, src + 16 * tc, 16);
+    }
+  } else {  // tail tile: zero-fill past n_valid (the padding of collectives.py:167-172)
+    const int64_t rem = jb.n_valid - e0;  // may be <= 0
+#pragma unroll 4
+    for (int j = 0; j < IT::CPG; ++j) {
+      const int tc = lane + 32 * j;
+      const int64_t v = rem - (int64_t)tc * 8;
+      const int valid = v <= 0 ? 0 : (v >= 8 ? 8 : (int)v);
+      const void* src = valid > 0 ? (const void*)(x + e0 + (int64_t)tc * 8) : (const void*)x;
+      cp_async16(stage + IT::in_pos(tc / IT::CPG, tc % IT::CPG) * 16, src, valid * 2);
+    }
+  }
+}
+
+template <int B, bool SR, int G, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_encode_grp(const __grid_constant__ EncBatch b) {
+  using IT = GTile<__nv_bfloat16, G>;
+  constexpr int PER_WARP = 2 * IT::IN_BYTES + OutStage<B, G>::BYTES;
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int warp = (int)(threadIdx.x >> 5), lane = (int)lane_id();
+  uint8_t* in0 = smem + warp * PER_WARP;
+  uint8_t* ost = in0 + 2 * IT::IN_BYTES;
+  const int64_t nw = (int64_t)gridDim.x * WARPS;
+  int64_t t = (int64_t)blockIdx.x * WARPS + warp;
+  if (t < b.total) issue_grp_tile<G>(b, t, in0);
+  cp_async_commit();
+  int stage = 0;
+  for (; t < b.total; t += nw) {
+    const int64_t tn = t + nw;
+    if (tn < b.total) issue_grp_tile<G>(b, tn, in0 + (stage ^ 1) * IT::IN_BYTES);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncwarp();
+    const int ji = find_job(b, t);
+    const EncJob& jb = b.j[ji];
+    const int64_t ngroups = jb.n / G;
+    const int64_t tg0 = (t - jb.t0) * 32;
+    const int64_t gabs = tg0 + lane;
+    const int ng = (int)min((int64_t)32, ngroups - tg0);
+    EncCtx cx;
+    cx.n = jb.n;
+    cx.meta_off = jb.n * B / 8;
+    cx.intlog = b.intlog;
+    cx.theta = b.theta;
+    cx.lut = b.lut;
+    cx.err = b.err;
+    encode_tile_bf16<B, SR, G>(in0 + stage * IT::IN_BYTES, ost, gabs < ngroups, gabs, cx, jb.out, tg0, ng);
+    stage ^= 1;
+  }
+  cp_async_wait<0>();
+}
+
+template <int B, bool SR, int G>
+struct EncGrp {
+  static constexpr int WARPS = G <= 128 ? 4 : 2;
+  static constexpr int SMEM = WARPS * (2 * GTile<__nv_bfloat16, G>::IN_BYTES + OutStage<B, G>::BYTES);
+  static int go(const EncBatch& b, cudaStream_t st) {
+    auto kern = k_encode_grp<B, SR, G, WARPS>;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+      attr = true;
+    }
+    int64_t blocks = (b.total + WARPS - 1) / WARPS;
+    int64_t cap = (int64_t)num_sms() * (G <= 128 ? 3 : 3);
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    kern<<<(unsigned)blocks, WARPS * 32, SMEM, st>>>(b);
+    return cuda_check("k_encode_grp");
+  }
+};
+
+// ---------------------------------------------------------------------------
 // generic encoder: warp per group, exact float64
 // ---------------------------------------------------------------------------
 
@@ -244,11 +335,11 @@ __device__ __forceinline__ void store_run(OT* y, int64_t e0, int64_t n_out, cons
 #pragma unroll
     for (int i = 0; i < 32; i += VE) {
       uint4 q;
-      if constexpr (sizeof(OT) == 2) {
-        q.x = bf16_bits(v[i]) | (bf16_bits(v[i + 1]) << 16);
-        q.y = bf16_bits(v[i + 2]) | (bf16_bits(v[i + 3]) << 16);
-        q.z = bf16_bits(v[i + 4]) | (bf16_bits(v[i + 5]) << 16);
-        q.w = bf16_bits(v[i + 6]) | (bf16_bits(v[i + 7]) << 16);
+      if constexpr (sizeof(OT) == 2) {  // cvt.rn.bf16x2 == bfloat16.py RNE for finite values
+        __nv_bfloat162 h0 = __floats2bfloat162_rn(v[i], v[i + 1]), h1 = __floats2bfloat162_rn(v[i + 2], v[i + 3]);
+        __nv_bfloat162 h2 = __floats2bfloat162_rn(v[i + 4], v[i + 5]), h3 = __floats2bfloat162_rn(v[i + 6], v[i + 7]);
+        q.x = *reinterpret_cast<uint32_t*>(&h0); q.y = *reinterpret_cast<uint32_t*>(&h1);
+        q.z = *reinterpret_cast<uint32_t*>(&h2); q.w = *reinterpret_cast<uint32_t*>(&h3);
       } else {
         q.x = __float_as_uint(v[i]); q.y = __float_as_uint(v[i + 1]);
         q.z = __float_as_uint(v[i + 2]); q.w = __float_as_uint(v[i + 3]);
@@ -262,39 +353,168 @@ __device__ __forceinline__ void store_run(OT* y, int64_t e0, int64_t n_out, cons
   }
 }
 
-// fast decode, 32 elements per lane, G % 32 == 0.  OT: bf16/f32 (f64 -> generic)
+// fast decode (G % 32 == 0): lane = 32 consecutive elements (one metadata
+// record per lane), next tile's codes + record prefetched into registers,
+// values staged in smem (swizzled) so the warp stores 16-byte chunks
+// contiguously; reserved spikes are patched in the stage.
+template <int B>
+struct RunRegs {
+  uint32_t w[B];   // packed code words of the 32-element run (unit 0 words first)
+  uint32_t r[3];   // metadata record
+};
+
+template <int B>
+__device__ __forceinline__ void load_run(const uint8_t* pay, int64_t n, int64_t e0, int64_t grp, int rb,
+                                         int64_t meta_off, RunRegs<B>& rr) {
+#pragma unroll
+  for (int u = 0; u < n_units(B); ++u) {
+    const int W = unit_w(B, u), O = unit_off(B, u);
+    const uint8_t* p = pay + (n * O) / 8 + (e0 * W) / 8;  // 4W bytes, >= 4-byte aligned
+    uint32_t* w = rr.w + unit_off(B, u);
+    if (W == 8) {
+      const uint4 a = *reinterpret_cast<const uint4*>(p), b2 = *reinterpret_cast<const uint4*>(p + 16);
+      w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w; w[4] = b2.x; w[5] = b2.y; w[6] = b2.z; w[7] = b2.w;
+    } else if (W == 4) {
+      const uint4 a = *reinterpret_cast<const uint4*>(p);
+      w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+    } else if (W == 2) {
+      const uint2 a = *reinterpret_cast<const uint2*>(p);
+      w[0] = a.x; w[1] = a.y;
+    } else {
+      w[0] = *reinterpret_cast<const uint32_t*>(p);
+    }
+  }
+  load_record(pay + meta_off + grp * rb, rr.r, rb);
+}
+
+template <int B>
+__device__ __forceinline__ uint32_t code_of(const RunRegs<B>& rr, int k) {
+  uint32_t c = 0;
+#pragma unroll
+  for (int u = 0; u < n_units(B); ++u) {
+    const int W = unit_w(B, u), O = unit_off(B, u);
+    c |= ((rr.w[O + ((k * W) >> 5)] >> ((k * W) & 31)) & ((1u << W) - 1u)) << O;
+  }
+  return c;
+}
+
 template <typename OT, int B>
 __global__ void __launch_bounds__(256) k_decode_fast(const __grid_constant__ DecBatch b) {
-  const int lane = (int)lane_id();
+  constexpr int CPL = (32 * (int)sizeof(OT)) / 16;  // 16-byte chunks per lane (4 bf16 / 8 f32)
+  constexpr int TB = 32 * 32 * (int)sizeof(OT);     // staged bytes per warp tile
+  __shared__ __align__(16) uint8_t stage_all[8 * TB];
+  const int warp = (int)(threadIdx.x >> 5), lane = (int)lane_id();
+  uint8_t* st = stage_all + warp * TB;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < b.total; t += nw) {
-    const int ji = find_job(b, t);
-    const DecJob& jb = b.j[ji];
-    const int64_t e0 = (t - jb.t0) * 1024 + lane * 32;
-    if (e0 >= jb.n || e0 >= jb.n_out) continue;
-    DecCtx c;
-    c.n = jb.n; c.meta_off = jb.n * B / 8; c.B = B; c.G = b.G; c.sr = b.sr; c.intlog = b.intlog;
-    c.theta = b.theta; c.lut = b.lut; c.err = b.err;
-    const int64_t grp = e0 / b.G;
-    GroupMeta m = read_meta(jb.pay, grp, c);
-    uint32_t code[32];
-    load_codes32<B>(jb.pay, jb.n, e0, code);
-    float v[32];
-    if (!b.intlog) {
+  const int rb = rec_bytes(b.sr, b.intlog);
+  int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  RunRegs<B> cur, nxt;
+  auto fetch = [&](int64_t tt, RunRegs<B>& rr) {
+    if (tt >= b.total) return;
+    const DecJob& jb = b.j[find_job(b, tt)];
+    const int64_t e0 = (tt - jb.t0) * 1024 + lane * 32;
+    if (e0 < jb.n) load_run<B>(jb.pay, jb.n, e0, e0 / b.G, rb, jb.n * B / 8, rr);
+  };
+  fetch(t, cur);
+  for (; t < b.total; t += nw) {
+    fetch(t + nw, nxt);  // prefetch the next tile while this one is decoded
+    const DecJob& jb = b.j[find_job(b, t)];
+    const int64_t ebase = (t - jb.t0) * 1024;
+    const int64_t e0 = ebase + lane * 32;
+    const int64_t lim = jb.n_out;
+    if (e0 < jb.n) {
+      // ---- metadata (R10 layouts)
+      GroupMeta m;
+      m.imin = m.imax = -1;
+      m.smin = m.smax = 0.f;
+      if (!b.intlog) {
+        m.s32 = bf16_val(cur.r[0] & 0xFFFFu);
+        m.z32 = bf16_val(cur.r[0] >> 16);
+        if (b.sr) {
+          m.smin = bf16_val(cur.r[1] & 0xFFFFu);
+          m.smax = bf16_val(cur.r[1] >> 16);
+          const float fi = bf16_val(cur.r[2] & 0xFFFFu), fa = bf16_val(cur.r[2] >> 16);
+          if ((fi > -1.0f) && (fi < (float)b.G) && (fa > -1.0f) && (fa < (float)b.G)) {
+            m.imin = (int)fi; m.imax = (int)fa;
+          } else {
+            atomicOr(b.err, FC2_ERR_SPIKE_INDEX);
+          }
+        }
+      } else {
+        const int si = (int)(int8_t)(cur.r[0] & 0xFFu), zi = (int)(int8_t)((cur.r[0] >> 8) & 0xFFu);
+        m.s64 = si == -128 ? 0.0 : b.lut[si + 128];
+        m.o64 = __dmul_rn(-(double)zi, m.s64);
+        if (b.sr) {
+          m.smin = bf16_val(cur.r[0] >> 16);
+          m.smax = bf16_val(cur.r[1] & 0xFFFFu);
+          const int ii = (int)((cur.r[1] >> 16) & 0xFFu), ia = (int)(cur.r[1] >> 24);
+          if (ii < b.G && ia < b.G) { m.imin = ii; m.imax = ia; }
+          else atomicOr(b.err, FC2_ERR_SPIKE_INDEX);
+        }
+      }
+      // ---- values -> stage
+      float v[32];
+      if (!b.intlog) {
 #pragma unroll
-      for (int k = 0; k < 32; ++k) v[k] = __fmaf_rn(code_f32(code[k]), m.s32, m.z32);
-    } else {
+        for (int k = 0; k < 32; k += 2) {
+          float a0, a1;
+          add2(a0, a1, __uint_as_float(0x4B000000u | code_of<B>(cur, k)),
+               __uint_as_float(0x4B000000u | code_of<B>(cur, k + 1)), -8388608.0f, -8388608.0f);
+          fma2(v[k], v[k + 1], a0, a1, m.s32, m.s32, m.z32, m.z32);
+        }
+      } else {
 #pragma unroll
-      for (int k = 0; k < 32; ++k) v[k] = dq32(code[k], m, true);
+        for (int k = 0; k < 32; ++k) v[k] = dq32(code_of<B>(cur, k), m, true);
+      }
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) {
+        uint4 q;
+        if constexpr (sizeof(OT) == 2) {
+          __nv_bfloat162 h0 = __floats2bfloat162_rn(v[8 * j], v[8 * j + 1]);
+          __nv_bfloat162 h1 = __floats2bfloat162_rn(v[8 * j + 2], v[8 * j + 3]);
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(v[8 * j + 4], v[8 * j + 5]);
+          __nv_bfloat162 h3 = __floats2bfloat162_rn(v[8 * j + 6], v[8 * j + 7]);
+          q = make_uint4(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1),
+                         *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3));
+        } else {
+          q = make_uint4(__float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]), __float_as_uint(v[4 * j + 2]),
+                         __float_as_uint(v[4 * j + 3]));
+        }
+        *reinterpret_cast<uint4*>(st + swz<CPL>(CPL * lane + j) * 16) = q;
+      }
+      if (b.sr) {  // imin then imax (codec.py:559-561); positions inside this lane's run
+        const int il = (int)(e0 - (e0 / b.G) * b.G);
+        auto put = [&](int idx, float val) {
+          const int k = idx - il;
+          if (k >= 0 && k < 32) {
+            const int c = CPL * lane + k / (16 / (int)sizeof(OT));
+            const int off = (k % (16 / (int)sizeof(OT))) * (int)sizeof(OT);
+            *reinterpret_cast<OT*>(st + swz<CPL>(c) * 16 + off) = cvt_out<OT>(val);
+          }
+        };
+        if (m.imin >= 0) put(m.imin, m.smin);
+        if (m.imax >= 0) put(m.imax, m.smax);
+      }
     }
-    OT* y = reinterpret_cast<OT*>(jb.y);
-    store_run<OT>(y, e0, jb.n_out, v);
-    if (b.sr) {  // reserved values: imin then imax (same thread -> program order)
-      const int64_t g0 = grp * b.G;
-      const int64_t a = g0 + m.imin, z = g0 + m.imax;
-      if (m.imin >= 0 && a >= e0 && a < e0 + 32 && a < jb.n_out) y[a] = cvt_out<OT>(m.smin);
-      if (m.imax >= 0 && z >= e0 && z < e0 + 32 && z < jb.n_out) y[z] = cvt_out<OT>(m.smax);
+    __syncwarp();
+    // ---- coalesced copy-out (16-byte chunks), bounded by n_out
+    OT* y = reinterpret_cast<OT*>(jb.y) + ebase;
+    const int64_t valid = lim - ebase;  // elements of this tile to write
+    constexpr int EPC = 16 / (int)sizeof(OT);
+    const bool aligned = (reinterpret_cast<uintptr_t>(y) & 15u) == 0;
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) {
+      const int c = lane + 32 * j;  // linear chunk of the tile
+      if ((int64_t)(c + 1) * EPC <= valid && aligned) {
+        *reinterpret_cast<uint4*>(y + c * EPC) = *reinterpret_cast<const uint4*>(st + swz<CPL>(c) * 16);
+      } else {
+        for (int i = 0; i < EPC; ++i)
+          if ((int64_t)c * EPC + i < valid)
+            y[c * EPC + i] = *reinterpret_cast<const OT*>(st + swz<CPL>(c) * 16 + i * (int)sizeof(OT));
+      }
     }
+    __syncwarp();
+    cur = nxt;
   }
 }
 
@@ -351,16 +571,8 @@ __global__ void __launch_bounds__(kRedWarps * 32) k_reduce_fast(const __grid_con
     const int il = (int)(ec - grp * G);  // element offset of this lane inside its group
     for (int s = 0; s < a.nsrc; ++s) {
       GroupMeta m = read_meta(a.src[s], grp, dc);
-      uint32_t code[32];
-      load_codes32<B>(a.src[s], a.n, ec, code);
       float d[32];
-      if (!a.intlog) {
-#pragma unroll
-        for (int k = 0; k < 32; ++k) d[k] = __fmaf_rn(code_f32(code[k]), m.s32, m.z32);
-      } else {
-#pragma unroll
-        for (int k = 0; k < 32; ++k) d[k] = dq32(code[k], m, true);
-      }
+      dq_run32<B>(a.src[s], a.n, ec, m, a.intlog != 0, d);
       if constexpr (SR) {
         const bool hit_a = m.imin >= il && m.imin < il + 32;
         const bool hit_z = m.imax >= il && m.imax < il + 32;
@@ -417,7 +629,7 @@ struct EncFast {
       attr = true;
     }
     int64_t blocks = (b.total + kEncWarps - 1) / kEncWarps;
-    int64_t cap = (int64_t)num_sms() * 4;
+    int64_t cap = (int64_t)num_sms() * 8;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     kern<<<(unsigned)blocks, kEncWarps * 32, smem, st>>>(b);
@@ -471,10 +683,10 @@ struct Launchers {
   template <bool SR>
   static int enc(int dtype, int G, const EncBatch& b, cudaStream_t st) {
     switch (G) {
-      case 32: return dtype == FC2_BF16 ? EncFastBf16<B, SR, 32>::go(b, st) : EncFastF32<B, SR, 32>::go(b, st);
-      case 64: return dtype == FC2_BF16 ? EncFastBf16<B, SR, 64>::go(b, st) : EncFastF32<B, SR, 64>::go(b, st);
-      case 128: return dtype == FC2_BF16 ? EncFastBf16<B, SR, 128>::go(b, st) : EncFastF32<B, SR, 128>::go(b, st);
-      case 256: return dtype == FC2_BF16 ? EncFastBf16<B, SR, 256>::go(b, st) : EncFastF32<B, SR, 256>::go(b, st);
+      case 32: return dtype == FC2_BF16 ? EncGrp<B, SR, 32>::go(b, st) : EncFastF32<B, SR, 32>::go(b, st);
+      case 64: return dtype == FC2_BF16 ? EncGrp<B, SR, 64>::go(b, st) : EncFastF32<B, SR, 64>::go(b, st);
+      case 128: return dtype == FC2_BF16 ? EncGrp<B, SR, 128>::go(b, st) : EncFastF32<B, SR, 128>::go(b, st);
+      case 256: return dtype == FC2_BF16 ? EncGrp<B, SR, 256>::go(b, st) : EncFastF32<B, SR, 256>::go(b, st);
     }
     return set_err(FC2_ECONFIG, "no fast encoder for G=%d", G);
   }
