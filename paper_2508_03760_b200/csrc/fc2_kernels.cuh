@@ -501,16 +501,16 @@ __global__ void __launch_bounds__(256) k_decode_fast(const __grid_constant__ Dec
     OT* y = reinterpret_cast<OT*>(jb.y) + ebase;
     const int64_t valid = lim - ebase;  // elements of this tile to write
     constexpr int EPC = 16 / (int)sizeof(OT);
-    const bool aligned = (reinterpret_cast<uintptr_t>(y) & 15u) == 0;
+    if (valid >= 1024 && (reinterpret_cast<uintptr_t>(y) & 15u) == 0) {
 #pragma unroll
-    for (int j = 0; j < CPL; ++j) {
-      const int c = lane + 32 * j;  // linear chunk of the tile
-      if ((int64_t)(c + 1) * EPC <= valid && aligned) {
+      for (int j = 0; j < CPL; ++j) {
+        const int c = lane + 32 * j;
         *reinterpret_cast<uint4*>(y + c * EPC) = *reinterpret_cast<const uint4*>(st + swz<CPL>(c) * 16);
-      } else {
-        for (int i = 0; i < EPC; ++i)
-          if ((int64_t)c * EPC + i < valid)
-            y[c * EPC + i] = *reinterpret_cast<const OT*>(st + swz<CPL>(c) * 16 + i * (int)sizeof(OT));
+      }
+    } else {
+      for (int i = lane; i < valid && i < 1024; i += 32) {
+        const int c = i / EPC;
+        y[i] = *reinterpret_cast<const OT*>(st + swz<CPL>(c) * 16 + (i % EPC) * (int)sizeof(OT));
       }
     }
     __syncwarp();
