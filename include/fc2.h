@@ -104,7 +104,8 @@ int fc2_reduce_requant(const fc2_config* cfg, int32_t nsrc, const void* const* s
                        void* stream);
 
 /* Decode the N gathered shard payloads of a two-step AllReduce straight into
- * the bf16/f32 output, stripping padding (collectives.py:313-314). */
+ * the bf16/f32 output on the bf16 grid, stripping padding (collectives.py:313-314,
+ * 185-186). */
 int fc2_gather_decode(const fc2_config* cfg, int32_t nshards, const void* const* shard_payloads,
                       int64_t shard_len, void* y, int32_t y_dtype, int64_t n_out,
                       int32_t* dev_err, void* stream);
@@ -120,6 +121,38 @@ int fc2_unpack_codes(const uint8_t* planes, int64_t n, int32_t bitwidth, uint8_t
 /* bfloat16.py:16-36 on device arrays. */
 int fc2_f32_to_bf16_bits(const float* x, int64_t n, uint16_t* out, void* stream);
 int fc2_bf16_bits_to_f32(const uint16_t* x, int64_t n, float* out, void* stream);
+
+/* ---- one-process-per-GPU communicator (CUDA IPC symmetric buffers) ------ */
+typedef struct fc2_comm fc2_comm;
+
+/* Bytes of one IPC handle (cudaIpcMemHandle_t). */
+int fc2_comm_handle_bytes(void);
+/* Allocate this rank's symmetric buffer (`bytes` usable + 4 KB of barrier
+ * flags) on the current device and export its IPC handle into handle_out. */
+int fc2_comm_create(int32_t rank, int32_t world, int64_t bytes, fc2_comm** out, void* handle_out);
+/* Map every peer's buffer; handles = world * fc2_comm_handle_bytes() bytes
+ * (all ranks' handles in rank order, e.g. from an all_gather). */
+int fc2_comm_open_peers(fc2_comm* c, const void* handles);
+int fc2_comm_destroy(fc2_comm* c);
+/* Device pointer of peer's usable buffer (peer == own rank: local). */
+void* fc2_comm_buffer(fc2_comm* c, int32_t peer);
+/* Stream-ordered device barrier over all ranks (release/acquire system-scope
+ * flags in peer memory); on timeout sets FC2_ERR_TIMEOUT in dev_err. */
+int fc2_comm_barrier(fc2_comm* c, int32_t* dev_err, double timeout_s, void* stream);
+
+/* Two-step quantized AllReduce of n elements per rank (collectives.py:263-315)
+ * with the exchanges done as NVLink peer stores from the codec kernels.
+ * slot_bytes: per-shard slot size (>= footprint of the shard, multiple of 16);
+ * the buffer must hold 2 * world * slot_bytes. */
+int fc2_allreduce_2step(fc2_comm* c, const fc2_config* cfg, const void* x, int32_t x_dtype, void* y,
+                        int32_t y_dtype, int64_t n, int64_t slot_bytes, int32_t* dev_err, double timeout_s,
+                        void* stream);
+
+/* Quantized All2All (dispatch, collectives.py:428-482; combine = transposed
+ * matrix).  matrix: host int64[world*world] element counts.  The diagonal
+ * block is left to the caller (exact copy, collectives.py:466-468). */
+int fc2_a2a_q(fc2_comm* c, const fc2_config* cfg, const void* x, int32_t x_dtype, const int64_t* matrix,
+              void* y, int32_t y_dtype, int64_t region_off, int32_t* dev_err, double timeout_s, void* stream);
 
 /* Diagnostics. */
 const char* fc2_last_error(void);

@@ -303,8 +303,18 @@ int fc2_encode(const fc2_config* cfg, const void* x, int32_t x_dtype, int64_t n_
   return fc2_encode_batch(cfg, x_dtype, 1, &x, &n_valid, &n, &payload, dev_err, stream);
 }
 
+static int decode_batch_impl(const fc2_config* cfg, int32_t y_dtype, int32_t njobs, const void* const* payloads,
+                             const int64_t* n, void* const* ys, const int64_t* n_out, int32_t* dev_err,
+                             void* stream, int round_bf16);
+
 int fc2_decode_batch(const fc2_config* cfg, int32_t y_dtype, int32_t njobs, const void* const* payloads,
                      const int64_t* n, void* const* ys, const int64_t* n_out, int32_t* dev_err, void* stream) {
+  return decode_batch_impl(cfg, y_dtype, njobs, payloads, n, ys, n_out, dev_err, stream, 0);
+}
+
+static int decode_batch_impl(const fc2_config* cfg, int32_t y_dtype, int32_t njobs, const void* const* payloads,
+                             const int64_t* n, void* const* ys, const int64_t* n_out, int32_t* dev_err,
+                             void* stream, int round_bf16) {
   int rc = check_cfg(cfg);
   if (rc) return rc;
   if (njobs < 0 || njobs > FC2_MAX_JOBS) return set_err(FC2_ECONFIG, "njobs %d out of range", njobs);
@@ -318,6 +328,7 @@ int fc2_decode_batch(const fc2_config* cfg, int32_t y_dtype, int32_t njobs, cons
   for (int i = 0; i < njobs; ++i)
     if (reinterpret_cast<uintptr_t>(payloads[i]) & 15u) fastG = false;
   DecBatch b;
+  b.round_bf16 = round_bf16;
   b.nj = 0; b.B = B; b.G = G; b.sr = cfg->scheme == 1; b.intlog = cfg->scale_encoding; b.theta = cfg->theta;
   b.total = 0; b.lut = lut; b.err = dev_err;
   for (int i = 0; i < njobs; ++i) {
@@ -365,7 +376,7 @@ int fc2_gather_decode(const fc2_config* cfg, int32_t nshards, const void* const*
     no[i] = rem < 0 ? 0 : (rem > shard_len ? shard_len : rem);
     ys[i] = (uint8_t*)y + (size_t)i * shard_len * esz;
   }
-  return fc2_decode_batch(cfg, y_dtype, nshards, shard_payloads, ns, ys, no, dev_err, stream);
+  return decode_batch_impl(cfg, y_dtype, nshards, shard_payloads, ns, ys, no, dev_err, stream, 1);
 }
 
 int fc2_reduce_requant(const fc2_config* cfg, int32_t nsrc, const void* const* src_payloads, int64_t n, int32_t ndst,

@@ -1,0 +1,297 @@
+// fc2_comm.cu -- one-process-per-GPU communicator for the quantized collectives.
+//
+// Every rank owns one symmetric device buffer (cudaMalloc, exported with
+// cudaIpcGetMemHandle, opened by every peer).  Layout of each buffer:
+//
+//   [0, 4096)                      barrier flags: uint32 arrive[FC2_COMM_MAX]
+//   [4096, 4096 + N*slot)          landing slots  land[src]   (stage 1, my shard)
+//   [.., + N*slot)                 gather slots   gath[owner] (stage 2)
+//   [.., + a2a_bytes)              All2All receive region
+//
+// Two-step AllReduce on rank r (collectives.py:263-315, one call):
+//   1. one batched encode launch quantizes shard j of x straight into
+//      peer j's land[r] (NVLink peer stores from the kernel's copy-out);
+//   2. barrier;
+//   3. k_reduce decodes land[0..N-1] (local), sums in fp32 in rank order,
+//      re-encodes and stores the packed shard into every peer's gath[r];
+//   4. barrier;
+//   5. decode gath[0..N-1] (local) into the bf16/f32 output.
+// Buffer reuse across calls is safe with the two barriers.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <algorithm>
+#include <vector>
+
+#include "../../include/fc2.h"
+#include "fc2_common.cuh"
+
+namespace fc2 {
+int set_err(int code, const char* fmt, ...);
+int cuda_check(const char* what);
+}  // namespace fc2
+
+using namespace fc2;
+
+#define FC2_COMM_MAX 16
+#define FC2_FLAG_BYTES 4096
+
+struct fc2_comm {
+  int rank, world, device;
+  int64_t bytes;
+  uint8_t* local;
+  uint8_t* peer[FC2_COMM_MAX];
+  bool opened[FC2_COMM_MAX];
+  uint32_t epoch;
+};
+
+namespace {
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+struct BarrierArgs {
+  uint32_t* mine;                    // my arrive[] array
+  uint32_t* peers[FC2_COMM_MAX];     // peer p's arrive[] array (mapped)
+  int rank, world;
+  uint32_t epoch;
+  int32_t* err;
+  long long timeout_cycles;
+};
+
+// One thread per peer: publish "rank reached epoch" to peer p, then wait for
+// peer p's arrival in my array.  fence.sys first: every store this device made
+// before this kernel (earlier kernels on the stream) is ordered before the flag.
+__global__ void k_barrier(const __grid_constant__ BarrierArgs a) {
+  const int p = threadIdx.x;
+  if (p >= a.world) return;
+  __threadfence_system();
+  st_release_sys(a.peers[p] + a.rank, a.epoch);
+  const long long t0 = clock64();
+  while ((int32_t)(ld_acquire_sys(a.mine + p) - a.epoch) < 0) {
+    if (clock64() - t0 > a.timeout_cycles) {
+      atomicOr(a.err, FC2_ERR_TIMEOUT);
+      break;
+    }
+    __nanosleep(256);
+  }
+  __threadfence_system();
+}
+
+}  // namespace
+
+extern "C" {
+
+int fc2_comm_create(int32_t rank, int32_t world, int64_t bytes, fc2_comm** out, void* handle_out) {
+  if (world < 1 || world > FC2_COMM_MAX || rank < 0 || rank >= world)
+    return set_err(FC2_ECONFIG, "bad rank/world %d/%d (max %d ranks)", rank, world, FC2_COMM_MAX);
+  fc2_comm* c = new fc2_comm();
+  memset(c, 0, sizeof(*c));
+  c->rank = rank;
+  c->world = world;
+  cudaGetDevice(&c->device);
+  c->bytes = bytes + FC2_FLAG_BYTES;
+  if (cudaMalloc(&c->local, c->bytes) != cudaSuccess) {
+    delete c;
+    return set_err(FC2_ECUDA, "cudaMalloc(%lld) failed", (long long)c->bytes);
+  }
+  cudaMemset(c->local, 0, FC2_FLAG_BYTES);
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, c->local) != cudaSuccess) {
+    cudaFree(c->local);
+    delete c;
+    return set_err(FC2_ECUDA, "cudaIpcGetMemHandle failed");
+  }
+  memcpy(handle_out, &h, sizeof(h));
+  c->peer[rank] = c->local;
+  c->opened[rank] = false;
+  cudaDeviceSynchronize();
+  *out = c;
+  return FC2_OK;
+}
+
+int fc2_comm_handle_bytes(void) { return (int)sizeof(cudaIpcMemHandle_t); }
+
+int fc2_comm_open_peers(fc2_comm* c, const void* handles) {
+  const uint8_t* hs = (const uint8_t*)handles;
+  for (int p = 0; p < c->world; ++p) {
+    if (p == c->rank) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, hs + (size_t)p * sizeof(h), sizeof(h));
+    void* ptr = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return set_err(FC2_ECUDA, "cudaIpcOpenMemHandle(peer %d): %s", p, cudaGetErrorString(e));
+    c->peer[p] = (uint8_t*)ptr;
+    c->opened[p] = true;
+  }
+  return FC2_OK;
+}
+
+int fc2_comm_destroy(fc2_comm* c) {
+  if (!c) return FC2_OK;
+  cudaDeviceSynchronize();
+  for (int p = 0; p < c->world; ++p)
+    if (c->opened[p]) cudaIpcCloseMemHandle(c->peer[p]);
+  cudaFree(c->local);
+  delete c;
+  return FC2_OK;
+}
+
+void* fc2_comm_buffer(fc2_comm* c, int32_t peer) {
+  if (!c || peer < 0 || peer >= c->world) return nullptr;
+  return c->peer[peer] + FC2_FLAG_BYTES;
+}
+
+int fc2_comm_barrier(fc2_comm* c, int32_t* dev_err, double timeout_s, void* stream) {
+  BarrierArgs a;
+  a.mine = (uint32_t*)c->local;
+  for (int p = 0; p < c->world; ++p) a.peers[p] = (uint32_t*)c->peer[p];
+  a.rank = c->rank;
+  a.world = c->world;
+  a.epoch = ++c->epoch;
+  a.err = dev_err;
+  a.timeout_cycles = (long long)(timeout_s * 2.0e9);
+  k_barrier<<<1, 32, 0, (cudaStream_t)stream>>>(a);
+  return cuda_check("k_barrier");
+}
+
+int fc2_allreduce_2step(fc2_comm* c, const fc2_config* cfg, const void* x, int32_t x_dtype, void* y,
+                        int32_t y_dtype, int64_t n, int64_t slot_bytes, int32_t* dev_err, double timeout_s,
+                        void* stream) {
+  const int N = c->world, r = c->rank;
+  int rc = fc2_check_config(cfg);
+  if (rc) return rc;
+  const int64_t mult = (int64_t)N * cfg->group_size;
+  const int64_t padded = (n + mult - 1) / mult * mult;
+  const int64_t S = padded / N;
+  int64_t F = 0;
+  rc = fc2_footprint(cfg, S, &F);
+  if (rc) return rc;
+  if (F > slot_bytes || (slot_bytes & 15)) return set_err(FC2_ECONFIG, "slot too small for shard footprint");
+  if ((int64_t)2 * N * slot_bytes > c->bytes - FC2_FLAG_BYTES)
+    return set_err(FC2_ECONFIG, "communicator buffer too small");
+  const int esz = x_dtype == FC2_BF16 ? 2 : (x_dtype == FC2_F32 ? 4 : 8);
+  auto land = [&](int dst, int src) { return (void*)(c->peer[dst] + FC2_FLAG_BYTES + (int64_t)src * slot_bytes); };
+  auto gath = [&](int dst, int owner) {
+    return (void*)(c->peer[dst] + FC2_FLAG_BYTES + (int64_t)(N + owner) * slot_bytes);
+  };
+  // 1. quantize my N shards straight into the owners' landing slots
+  std::vector<const void*> xs(N);
+  std::vector<int64_t> nv(N), ns(N);
+  std::vector<void*> outs(N);
+  for (int j = 0; j < N; ++j) {
+    const int64_t valid = n - (int64_t)j * S;
+    nv[j] = valid < 0 ? 0 : (valid > S ? S : valid);
+    ns[j] = S;
+    xs[j] = nv[j] ? (const uint8_t*)x + (int64_t)j * S * esz : x;
+    outs[j] = land(j, r);
+  }
+  rc = fc2_encode_batch(cfg, x_dtype, N, xs.data(), nv.data(), ns.data(), outs.data(), dev_err, stream);
+  if (rc) return rc;
+  rc = fc2_comm_barrier(c, dev_err, timeout_s, stream);
+  if (rc) return rc;
+  // 3. reduce my shard from the N landing slots, push the packed result to everyone
+  std::vector<const void*> srcs(N);
+  std::vector<void*> dsts(N);
+  for (int s = 0; s < N; ++s) srcs[s] = land(r, s);
+  for (int p = 0; p < N; ++p) dsts[p] = gath(p, r);
+  rc = fc2_reduce_requant(cfg, N, srcs.data(), S, N, dsts.data(), dev_err, stream);
+  if (rc) return rc;
+  rc = fc2_comm_barrier(c, dev_err, timeout_s, stream);
+  if (rc) return rc;
+  // 5. decode every owner's shard into the output (padding stripped)
+  std::vector<const void*> gs(N);
+  for (int o = 0; o < N; ++o) gs[o] = gath(r, o);
+  return fc2_gather_decode(cfg, N, gs.data(), S, y, y_dtype, n, dev_err, stream);
+}
+
+// Quantized All2All over the symmetric buffers (collectives.py:428-482 for
+// dispatch; combine = the same call with the transposed matrix).
+// matrix: host int64[N*N], m[src*N + dst] = elements rank src sends to dst.
+// x: this rank's payload, blocks for dst = 0..N-1 back to back.
+// y: this rank's receive buffer, blocks from src = 0..N-1 back to back
+//    (y_dtype F32 or BF16); the diagonal block is NOT written here (exact copy,
+//    done by the caller).  region_off: byte offset of the All2All region.
+int fc2_a2a_q(fc2_comm* c, const fc2_config* cfg, const void* x, int32_t x_dtype, const int64_t* matrix,
+              void* y, int32_t y_dtype, int64_t region_off, int32_t* dev_err, double timeout_s, void* stream) {
+  const int N = c->world, r = c->rank;
+  int rc = fc2_check_config(cfg);
+  if (rc) return rc;
+  const int64_t G = cfg->group_size;
+  const int esz = x_dtype == FC2_BF16 ? 2 : (x_dtype == FC2_F32 ? 4 : 8);
+  const int ysz = y_dtype == FC2_BF16 ? 2 : (y_dtype == FC2_F32 ? 4 : 8);
+  // slot offset of the block src -> dst inside dst's region
+  auto slot_off = [&](int dst, int src, int64_t* F_out) -> int64_t {
+    int64_t off = 0;
+    for (int s = 0; s <= src; ++s) {
+      const int64_t m = matrix[(int64_t)s * N + dst];
+      int64_t F = 0;
+      if (s != dst && m > 0) fc2_footprint(cfg, (m + G - 1) / G * G, &F);
+      if (s == src) { *F_out = F; return off; }
+      off += (F + 15) / 16 * 16;
+    }
+    return off;
+  };
+  for (int d = 0; d < N; ++d) {  // capacity check of every receiver's region
+    int64_t F = 0;
+    int64_t end = slot_off(d, N - 1, &F) + F;
+    if (region_off + end + FC2_FLAG_BYTES > c->bytes) return set_err(FC2_ECONFIG, "a2a region too small");
+  }
+  std::vector<const void*> xs;
+  std::vector<int64_t> nv, ns;
+  std::vector<void*> outs;
+  int64_t soff = 0;
+  for (int d = 0; d < N; ++d) {
+    const int64_t m = matrix[(int64_t)r * N + d];
+    if (d != r && m > 0) {
+      int64_t F = 0;
+      const int64_t o = slot_off(d, r, &F);
+      xs.push_back((const uint8_t*)x + soff * esz);
+      nv.push_back(m);
+      ns.push_back((m + G - 1) / G * G);
+      outs.push_back(c->peer[d] + FC2_FLAG_BYTES + region_off + o);
+    }
+    soff += m;
+  }
+  for (size_t i = 0; i < xs.size(); i += FC2_MAX_JOBS) {
+    const int nj = (int)std::min<size_t>(FC2_MAX_JOBS, xs.size() - i);
+    rc = fc2_encode_batch(cfg, x_dtype, nj, xs.data() + i, nv.data() + i, ns.data() + i, outs.data() + i,
+                          dev_err, stream);
+    if (rc) return rc;
+  }
+  rc = fc2_comm_barrier(c, dev_err, timeout_s, stream);
+  if (rc) return rc;
+  std::vector<const void*> ps;
+  std::vector<int64_t> pn, po;
+  std::vector<void*> ys;
+  int64_t roff = 0;
+  for (int s = 0; s < N; ++s) {
+    const int64_t m = matrix[(int64_t)s * N + r];
+    if (s != r && m > 0) {
+      int64_t F = 0;
+      const int64_t o = slot_off(r, s, &F);
+      ps.push_back(c->local + FC2_FLAG_BYTES + region_off + o);
+      pn.push_back((m + G - 1) / G * G);
+      ys.push_back((uint8_t*)y + roff * ysz);
+      po.push_back(m);
+    }
+    roff += m;
+  }
+  for (size_t i = 0; i < ps.size(); i += FC2_MAX_JOBS) {
+    const int nj = (int)std::min<size_t>(FC2_MAX_JOBS, ps.size() - i);
+    rc = fc2_decode_batch(cfg, y_dtype, nj, ps.data() + i, pn.data() + i, ys.data() + i, po.data() + i, dev_err,
+                          stream);
+    if (rc) return rc;
+  }
+  // everyone has consumed its region before anyone writes the next call's blocks
+  return fc2_comm_barrier(c, dev_err, timeout_s, stream);
+}
+
+}  // extern "C"

@@ -40,6 +40,7 @@ struct DecJob {
 };
 struct DecBatch {
   int nj, B, G, sr, intlog, theta;
+  int round_bf16;  // snap float32 outputs to the bf16 grid (collectives.py:185-186)
   int64_t total;
   const double* lut;
   int32_t* err;
@@ -466,6 +467,12 @@ __global__ void __launch_bounds__(256) k_decode_fast(const __grid_constant__ Dec
 #pragma unroll
         for (int k = 0; k < 32; ++k) v[k] = dq32(code_of<B>(cur, k), m, true);
       }
+      if constexpr (sizeof(OT) == 4) {
+        if (b.round_bf16) {
+#pragma unroll
+          for (int k = 0; k < 32; ++k) v[k] = bf16_val(bf16_bits(v[k]));
+        }
+      }
 #pragma unroll
       for (int j = 0; j < CPL; ++j) {
         uint4 q;
@@ -485,6 +492,7 @@ __global__ void __launch_bounds__(256) k_decode_fast(const __grid_constant__ Dec
       if (b.sr) {  // imin then imax (codec.py:559-561); positions inside this lane's run
         const int il = (int)(e0 - (e0 / b.G) * b.G);
         auto put = [&](int idx, float val) {
+          if (sizeof(OT) == 4 && b.round_bf16) val = bf16_val(bf16_bits(val));
           const int k = idx - il;
           if (k >= 0 && k < 32) {
             const int c = CPL * lane + k / (16 / (int)sizeof(OT));
@@ -534,7 +542,9 @@ __global__ void __launch_bounds__(256) k_decode_gen(const __grid_constant__ DecB
     if constexpr (sizeof(OT) == 8) {
       y[e] = decode_elem64(jb.pay, e, c);
     } else {
-      y[e] = cvt_out<OT>(decode_elem32(jb.pay, e, c));
+      float v = decode_elem32(jb.pay, e, c);
+      if (b.round_bf16) v = bf16_val(bf16_bits(v));
+      y[e] = cvt_out<OT>(v);
     }
   }
 }

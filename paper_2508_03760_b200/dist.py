@@ -1,0 +1,261 @@
+"""SPMD quantized collectives: one process per GPU (the multi-GPU form of
+``two_step_allreduce_q`` / ``all2all_dispatch_q``, collectives.py:263-315,
+428-482).
+
+Two transports, same arithmetic and bit-identical results:
+
+* ``"ipc"`` (default): every rank maps every peer's symmetric buffer through
+  CUDA IPC (handles exchanged over the ``torch.distributed`` group); the
+  codec kernels store packed shards straight into peer memory over NVLink
+  and stream-ordered device barriers separate the stages
+  (``fc2_allreduce_2step`` / ``fc2_a2a_q`` in the C ABI).  No NCCL on the
+  data path.
+* ``"nccl"``: encode into a local send buffer, ``all_to_all_single`` /
+  ``all_gather_into_tensor`` of the packed bytes, reduce + requantize and
+  decode locally -- the "NCCL send/recv of packed bytes" alternative.
+
+The orchestration of the ``"nccl"`` transport is written against a small
+codec interface (:class:`CudaCodec`), which is what the CPU tests drive with
+gloo and a test-only codec double; the product codec is the CUDA library.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _device, _lib
+from .config import QuantConfig, footprint_bytes
+from .errors import ConfigError, DataError
+
+_SLOT_ALIGN = 16
+
+
+def _round_up(x: int, a: int) -> int:
+    return (x + a - 1) // a * a
+
+
+@dataclass(frozen=True)
+class TwoStepLayout:
+    """Shard geometry of the two-step AllReduce for n elements on N ranks
+    (collectives.py:275-276: zero-pad to a multiple of N*g, contiguous shards)."""
+
+    n: int
+    world: int
+    group_size: int
+    bitwidth: int
+    shard_bytes: int  # footprint of one packed shard
+    slot_bytes: int   # shard_bytes rounded up to 16
+
+    @staticmethod
+    def make(n: int, world: int, config: QuantConfig) -> "TwoStepLayout":
+        if world < 1:
+            raise ConfigError("world must be >= 1")
+        mult = world * config.group_size
+        padded = _round_up(max(n, 0), mult)
+        S = padded // world
+        F = footprint_bytes(config, S)
+        return TwoStepLayout(n, world, config.group_size, config.bitwidth, F,
+                             _round_up(max(F, 1), _SLOT_ALIGN))
+
+    @property
+    def padded(self) -> int:
+        return _round_up(self.n, self.world * self.group_size)
+
+    @property
+    def shard_len(self) -> int:
+        return self.padded // self.world
+
+    def valid(self, shard: int) -> int:
+        """Real (unpadded) elements of shard j."""
+        return max(0, min(self.shard_len, self.n - shard * self.shard_len))
+
+
+def a2a_slot_offsets(matrix: np.ndarray, config: QuantConfig, dst: int) -> list[int]:
+    """Byte offset of each source's packed block inside rank dst's receive
+    region (same rule as fc2_a2a_q)."""
+    N = matrix.shape[0]
+    g = config.group_size
+    offs, off = [], 0
+    for s in range(N):
+        offs.append(off)
+        m = int(matrix[s, dst])
+        if s != dst and m > 0:
+            off += _round_up(footprint_bytes(config, _round_up(m, g)), _SLOT_ALIGN)
+    offs.append(off)
+    return offs
+
+
+class CudaCodec:
+    """The CUDA library behind the transport-agnostic orchestration."""
+
+    def __init__(self, config: QuantConfig, device):
+        self.cfg = config
+        self.device = device
+        self.err = torch.zeros(1, dtype=torch.int32, device=device)
+        if config.int_log:
+            _device.ensure_intlog(config.theta, device)
+
+    def empty(self, nbytes: int) -> torch.Tensor:
+        return torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+
+    def encode_shards(self, x: torch.Tensor, lay: TwoStepLayout, send: torch.Tensor) -> None:
+        """Shard j of x -> send[j*slot : ...] (all shards in one launch)."""
+        esz = x.element_size()
+        jobs = [((x.data_ptr() + j * lay.shard_len * esz) if lay.valid(j) else x.data_ptr(),
+                 lay.valid(j), lay.shard_len, send.data_ptr() + j * lay.slot_bytes) for j in range(lay.world)]
+        from .collectives import _encode_jobs
+        _encode_jobs(self.cfg, _device.dtype_code(x), jobs, self.err)
+
+    def reduce(self, recv: torch.Tensor, lay: TwoStepLayout, out: torch.Tensor) -> None:
+        """Decode the N packed copies of my shard, fp32 rank-order sum, re-encode."""
+        from .collectives import reduce_requant
+        reduce_requant(self.cfg, [recv.data_ptr() + s * lay.slot_bytes for s in range(lay.world)],
+                       lay.shard_len, [out.data_ptr()], self.err)
+
+    def decode_gathered(self, gath: torch.Tensor, lay: TwoStepLayout, y: torch.Tensor) -> None:
+        c = self.cfg.c_struct()
+        _lib.check(_lib.lib().fc2_gather_decode(
+            ctypes.byref(c), lay.world, _lib.ptr_array([gath.data_ptr() + o * lay.slot_bytes
+                                                        for o in range(lay.world)]),
+            lay.shard_len, y.data_ptr(), _device.dtype_code(y), lay.n, self.err.data_ptr(),
+            _device.stream_handle()))
+
+    def check(self) -> None:
+        _device.check_err(self.err)
+
+
+def two_step_via_collectives(x: torch.Tensor, codec, lay: TwoStepLayout, group=None,
+                             out: torch.Tensor | None = None) -> torch.Tensor:
+    """Two-step AllReduce with torch.distributed collectives moving the packed
+    bytes (collectives.py:278-314):
+      encode N shards -> all_to_all (packed) -> reduce + requantize my shard ->
+      all_gather (packed) -> decode all shards."""
+    N, slot = lay.world, lay.slot_bytes
+    send = codec.empty(N * slot)
+    recv = codec.empty(N * slot)
+    codec.encode_shards(x, lay, send)
+    dist.all_to_all_single(recv, send, group=group)
+    mine = codec.empty(slot)
+    codec.reduce(recv, lay, mine)
+    gath = codec.empty(N * slot)
+    dist.all_gather_into_tensor(gath, mine, group=group)
+    y = out if out is not None else torch.empty(lay.n, dtype=x.dtype, device=x.device)
+    codec.decode_gathered(gath, lay, y)
+    return y
+
+
+class QComm:
+    """Quantized collectives over one process group (one process per GPU).
+
+    ``max_elems`` sizes the symmetric buffers for AllReduce payloads;
+    ``a2a_bytes`` reserves the All2All receive region.
+    """
+
+    def __init__(self, group=None, max_elems: int = 1 << 25, config: QuantConfig | None = None,
+                 transport: str = "ipc", a2a_bytes: int = 0, timeout_s: float = 60.0):
+        self.device = _device.require_cuda()
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.cfg = config or QuantConfig(4, group_size=128, chunk_size=128)
+        self.transport = transport
+        self.timeout_s = float(timeout_s)
+        self.max_lay = TwoStepLayout.make(max_elems, self.world, self.cfg)
+        self.a2a_off = 2 * self.world * self.max_lay.slot_bytes
+        self.codec = CudaCodec(self.cfg, self.device)
+        self.err = self.codec.err
+        self._c = None
+        if transport not in ("ipc", "nccl"):
+            raise ConfigError(f"unknown transport {transport!r}")
+        if transport == "ipc":
+            lib = _lib.lib()
+            hb = lib.fc2_comm_handle_bytes()
+            handle = (ctypes.c_uint8 * hb)()
+            ptr = ctypes.c_void_p()
+            nbytes = self.a2a_off + _round_up(int(a2a_bytes), _SLOT_ALIGN)
+            _lib.check(lib.fc2_comm_create(self.rank, self.world, nbytes, ctypes.byref(ptr),
+                                           ctypes.cast(handle, ctypes.c_void_p)))
+            self._c = ptr
+            handles = [None] * self.world
+            dist.all_gather_object(handles, bytes(handle), group=group)
+            allh = (ctypes.c_uint8 * (hb * self.world)).from_buffer_copy(b"".join(handles))
+            _lib.check(lib.fc2_comm_open_peers(self._c, ctypes.cast(allh, ctypes.c_void_p)))
+            dist.barrier(group=group)
+
+    @property
+    def shard_len(self) -> int:
+        return self.max_lay.shard_len
+
+    def all_reduce(self, x: torch.Tensor, out: torch.Tensor | None = None, check: bool = False) -> torch.Tensor:
+        """Two-step quantized AllReduce of a 1-D bf16/f32 CUDA tensor; every
+        rank gets the identical bf16-grid result (collectives.py:313-314)."""
+        x = x.reshape(-1)
+        if not x.is_contiguous():
+            x = x.contiguous()
+        n = x.numel()
+        if n > self.max_lay.n:
+            raise DataError(f"payload of {n} elements exceeds the communicator's {self.max_lay.n}")
+        y = out if out is not None else torch.empty(n, dtype=x.dtype, device=x.device)
+        lay = TwoStepLayout.make(n, self.world, self.cfg)
+        if self.transport == "ipc":
+            c = self.cfg.c_struct()
+            _lib.check(_lib.lib().fc2_allreduce_2step(
+                self._c, ctypes.byref(c), x.data_ptr(), _device.dtype_code(x), y.data_ptr(),
+                _device.dtype_code(y), n, self.max_lay.slot_bytes, self.err.data_ptr(), self.timeout_s,
+                _device.stream_handle()))
+        else:
+            two_step_via_collectives(x, self.codec, lay, self.group, y)
+        if check:
+            self.codec.check()
+        return y
+
+    def all2all(self, x: torch.Tensor, matrix, out: torch.Tensor | None = None,
+                out_dtype: torch.dtype = torch.float32, check: bool = False) -> torch.Tensor:
+        """Quantized All2All (dispatch; combine = transposed matrix).
+
+        ``matrix[src][dst]`` = elements src sends to dst (known on all ranks).
+        ``x`` holds this rank's blocks for dst 0..N-1 back to back; the result
+        holds the blocks from src 0..N-1 back to back: exact copy on the
+        diagonal, QDQ'd (zero-padded to a group multiple) elsewhere."""
+        if self.transport != "ipc":
+            raise ConfigError("all2all is implemented on the ipc transport")
+        m = np.ascontiguousarray(np.asarray(matrix, dtype=np.int64))
+        N, r = self.world, self.rank
+        if m.shape != (N, N) or np.any(m < 0):
+            raise ConfigError(f"dispatch matrix must be a non-negative {N}x{N} array")
+        if int(m[r].sum()) != x.numel():
+            raise ConfigError("dispatch row does not match the payload size")
+        n_out = int(m[:, r].sum())
+        y = out if out is not None else torch.empty(n_out, dtype=out_dtype, device=x.device)
+        x = x.reshape(-1).contiguous()
+        c = self.cfg.c_struct()
+        mp = m.reshape(-1)
+        _lib.check(_lib.lib().fc2_a2a_q(
+            self._c, ctypes.byref(c), x.data_ptr(), _device.dtype_code(x),
+            mp.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), y.data_ptr(), _device.dtype_code(y),
+            self.a2a_off, self.err.data_ptr(), self.timeout_s, _device.stream_handle()))
+        # diagonal block: exact copy (collectives.py:466-468)
+        so = int(m[r, :r].sum())
+        ro = int(m[:r, r].sum())
+        d = int(m[r, r])
+        if d:
+            y[ro:ro + d].copy_(x[so:so + d])
+        if check:
+            self.codec.check()
+        return y
+
+    def close(self) -> None:
+        if self._c is not None:
+            _lib.lib().fc2_comm_destroy(self._c)
+            self._c = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,99 @@
+"""The SPMD CUDA-IPC path on a real GPU: several processes share cuda:0
+(CUDA IPC works between processes on one device), torch.distributed/gloo is
+only the handle-exchange plumbing, the data moves through the mapped
+symmetric buffers exactly as it would over NVLink on a multi-GPU box.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import paper_2508_03760_b200 as fc
+from oracle import fc2_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, case, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2508_03760_b200.dist import QComm
+
+        torch.cuda.set_device(0)
+        kind, n, bits, g, sr, seed = case
+        cfg = fc.QuantConfig(bits, group_size=g, scheme=fc.Scheme.SPIKE_RESERVING if sr else fc.Scheme.RTN,
+                             chunk_size=g)
+        seeds = O.child_seeds(seed, world)
+        if kind == "allreduce":
+            comm = QComm(max_elems=n, config=cfg, timeout_s=120.0)
+            x = torch.from_numpy(O.bf16_snap(O.spiky(n, seeds[rank])).astype(np.float32)).cuda()
+            outs = []
+            for dt in (torch.float32, torch.bfloat16):
+                y = comm.all_reduce(x.to(dt), check=True)
+                outs.append(y.float().cpu().numpy().tobytes())
+            q.put((rank, outs))
+        else:
+            rng = np.random.default_rng(seed)
+            m = rng.integers(0, 3, (world, world)) * 512 + rng.integers(0, 200, (world, world))
+            cap = sum(-(-fc.footprint_bytes(cfg, -(-int(v) // g) * g) // 16) * 16 for v in m.reshape(-1)) + 4096
+            comm = QComm(max_elems=g * world, config=cfg, a2a_bytes=cap, timeout_s=120.0)
+            xr = O.bf16_snap(np.random.default_rng(seeds[rank]).normal(0, 1, int(m[rank].sum()))).astype(np.float32)
+            y = comm.all2all(torch.from_numpy(xr).cuda(), m, check=True)
+            q.put((rank, [y.cpu().numpy().tobytes(), m.tobytes()]))
+        torch.cuda.synchronize()
+        comm.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, case):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return got
+
+
+@pytest.mark.parametrize("world,n,bits,g,sr", [(2, 100003, 4, 128, True), (4, 1 << 16, 3, 128, True),
+                                               (2, 8192, 2, 32, False)])
+def test_ipc_two_step_matches_reference_algorithm(world, n, bits, g, sr):
+    got = _run(world, ("allreduce", n, bits, g, sr, 5))
+    payloads = [O.bf16_snap(O.spiky(n, s)).astype(np.float32) for s in O.child_seeds(5, world)]
+    want, _ = O.two_step(payloads, bits, g, sr)
+    for r in range(world):
+        for blob in got[r]:  # float32 and bf16 outputs
+            assert np.array_equal(np.frombuffer(blob, dtype=np.float32), want[0])
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ipc_all2all_matches_reference_algorithm(world):
+    got = _run(world, ("a2a", 0, 4, 128, True, 9))
+    m = np.frombuffer(got[0][1], dtype=np.int64).reshape(world, world)
+    seeds = O.child_seeds(9, world)
+    payloads = [O.bf16_snap(np.random.default_rng(seeds[r]).normal(0, 1, int(m[r].sum()))).astype(np.float32)
+                for r in range(world)]
+    want = O.a2a_dispatch(payloads, 4, 128, True, m)
+    for d in range(world):
+        y = np.frombuffer(got[d][0], dtype=np.float32)
+        assert np.array_equal(y, np.concatenate([want[d][s] for s in range(world)]))
