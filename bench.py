@@ -160,6 +160,52 @@ def time_roundtrip(fc, x, cfg, steps, warmup, flush):
     return enc, dec, F, launches, (pay, y)
 
 
+def two_step_stage_times(fc, x, cfg, flush, steps, N=8):
+    import torch
+
+    from paper_2508_03760_b200.collectives import reduce_requant
+
+    n = x.numel()
+    S = n // N
+    F = fc.footprint_bytes(cfg, S)
+    slot = (F + 15) // 16 * 16
+    land = torch.empty(N * slot, dtype=torch.uint8, device=x.device)
+    for s in range(N):  # 8 different packed sources (the shards of this rank's tensor)
+        fc.encode_payload(x[s * S:(s + 1) * S], cfg, S, out=land[s * slot:s * slot + F])
+    gath = torch.empty(N * slot, dtype=torch.uint8, device=x.device)
+    err = torch.zeros(1, dtype=torch.int32, device=x.device)
+    y = torch.empty(n, dtype=torch.bfloat16, device=x.device)
+    import ctypes
+
+    c = cfg.c_struct()
+    lib = fc._lib.lib()
+
+    def red():
+        reduce_requant(cfg, [land.data_ptr() + s * slot for s in range(N)], S, [gath.data_ptr()], err)
+
+    def gat():
+        fc._lib.check(lib.fc2_gather_decode(ctypes.byref(c), N, fc._lib.ptr_array(
+            [land.data_ptr() + o * slot for o in range(N)]), S, y.data_ptr(), 0, n, err.data_ptr(),
+            torch.cuda.current_stream().cuda_stream))
+
+    out = {}
+    for name, fn, nbytes in (("reduce_requant_8src", red, N * F + F), ("gather_decode_8shards", gat, N * F + 2 * n)):
+        for _ in range(2):
+            fn()
+        ts = []
+        for _ in range(steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        t = statistics.mean(ts)
+        out[name] = {"us": round(t * 1e3, 2), "bytes": nbytes, "GBps": round(nbytes / (t * 1e-3) / 1e9, 1)}
+    return out
+
+
 def time_e2e(fc, x_host, cfg, steps, warmup):
     """Host-buffer round trip through the public API: pinned bf16 in -> H2D ->
     encode -> payload D2H (the wire bytes) -> decode -> bf16 D2H."""
@@ -265,6 +311,10 @@ def run_codec(args):
                                         "encode_GBps": round((2 * n + Fb) / (te * 1e-3) / 1e9, 1),
                                         "decode_GBps": round((Fb + 2 * n) / (td * 1e-3) / 1e9, 1),
                                         "payload_bytes": Fb}
+    # per-rank kernels of the N=8 two-step AllReduce (BASELINE configs[2]) timed
+    # on one GPU: stage-2 reduce+requant of one 4 Mi-element shard from 8
+    # packed sources, and the final gather-decode of 8 shards to bf16
+    stages = two_step_stage_times(fc, x, cfg, flush, max(3, args.steps // 2))
     # end to end through host buffers
     x_host = x.cpu().pin_memory()
     e2e_ms, h2d, d2h = time_e2e(fc, x_host, cfg, max(3, args.steps), 2)
@@ -296,6 +346,7 @@ def run_codec(args):
             "sample": f"full workload ({n} elements) x {args.cpu_reps}, oracle/fc2_oracle.py "
                       f"(numpy restatement of codec.py), {cpu_dt:.2f} s per round trip"},
         "sweep": sweep,
+        "two_step_n8_per_rank_kernels": stages,
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }

@@ -341,7 +341,7 @@ static int decode_batch_impl(const fc2_config* cfg, int32_t y_dtype, int32_t njo
     j.n = n[i];
     j.n_out = n_out[i];
     j.t0 = b.total;
-    b.total += fastG ? (n[i] + 1023) / 1024 : n_out[i];
+    b.total += fastG ? (n[i] + 4095) / 4096 : n_out[i];
   }
   if (!b.nj) return FC2_OK;
   if (fastG) {

@@ -145,6 +145,17 @@ __device__ __forceinline__ void top_add(TopState& s, uint32_t w) {
   s.b1 = __hmax2_nan(s.b1, x);
 }
 
+// merge two independent top-2 states (multiset union)
+template <bool SR>
+__device__ __forceinline__ void top_merge(TopState& s, const TopState& o) {
+  if constexpr (SR) {
+    s.a2 = __hmin2_nan(__hmax2_nan(s.a1, o.a1), __hmin2_nan(s.a2, o.a2));
+    s.b2 = __hmax2_nan(__hmin2_nan(s.b1, o.b1), __hmax2_nan(s.b2, o.b2));
+  }
+  s.a1 = __hmin2_nan(s.a1, o.a1);
+  s.b1 = __hmax2_nan(s.b1, o.b1);
+}
+
 template <bool SR>
 __device__ __forceinline__ void top_final(const TopState& s, float& mn1, float& mn2, float& mx1, float& mx2) {
   float l1 = __low2float(s.a1), h1 = __high2float(s.a1);
@@ -173,13 +184,14 @@ __device__ __forceinline__ void quant_runs(const uint8_t* ist, uint8_t* ost, con
   using FX = Fix<FB>;
   const int lane = (int)lane_id();
   constexpr int L = (1 << B) - 1;
-#pragma unroll 1
+#pragma unroll 2
   for (int r = 0; r < RUNS; ++r) {
     LaneWords<B> lw;
     lw.clear();
-    uint32_t tm = 0;
+    uint32_t tmj[2] = {0u, 0u};  // two accumulators: shorter dependency chains
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
+      uint32_t& tm = tmj[j & 1];
       const uint4 q = *reinterpret_cast<const uint4*>(ist + IT::in_pos(lane, 4 * r + j) * 16);
       const uint32_t ww[4] = {q.x, q.y, q.z, q.w};
       uint32_t X[8];
@@ -219,7 +231,7 @@ __device__ __forceinline__ void quant_runs(const uint8_t* ist, uint8_t* ost, con
     }
     // exact float64 recompute of near-tie elements (rare), patched in smem;
     // split layout: bit i < 16 -> element 2i, bit 16 + i -> element 2i + 1
-    tm = (p.exact ? 0xffffffffu : tm) & (active ? 0xffffffffu : 0u);
+    uint32_t tm = (p.exact ? 0xffffffffu : (tmj[0] | tmj[1])) & (active ? 0xffffffffu : 0u);
     while (tm) {
       const int k = __ffs(tm) - 1;
       tm &= tm - 1;
@@ -249,40 +261,46 @@ __device__ __forceinline__ void encode_tile_bf16(const uint8_t* ist, uint8_t* os
   using FX = Fix<FB>;
 
   // ---- pass 1: statistics; ra / rz = run where the running min / max last
-  // strictly improved == run holding the first occurrence of the extreme ----
-  TopState ts;
+  // strictly improved == run holding the first occurrence of the extreme.
+  // Two independent accumulator sets (even / odd chunks) halve the
+  // dependency chains; they are merged per run for the running extremes.
+  TopState ts, tt;
   int ra = 0, rz = 0;
   {
-    uint4 q = chunk(0);
-    top_init(ts, q.x);
-    top_add<SR>(ts, q.y); top_add<SR>(ts, q.z); top_add<SR>(ts, q.w);
-#pragma unroll
-    for (int j = 1; j < 4; ++j) {
-      q = chunk(j);
-      top_add<SR>(ts, q.x); top_add<SR>(ts, q.y); top_add<SR>(ts, q.z); top_add<SR>(ts, q.w);
-    }
+    const uint4 q0 = chunk(0), q1 = chunk(1);
+    top_init(ts, q0.x);
+    top_add<SR>(ts, q0.y); top_add<SR>(ts, q0.z); top_add<SR>(ts, q0.w);
+    top_init(tt, q1.x);
+    top_add<SR>(tt, q1.y); top_add<SR>(tt, q1.z); top_add<SR>(tt, q1.w);
+    const uint4 q2 = chunk(2), q3 = chunk(3);
+    top_add<SR>(ts, q2.x); top_add<SR>(ts, q2.y); top_add<SR>(ts, q2.z); top_add<SR>(ts, q2.w);
+    top_add<SR>(tt, q3.x); top_add<SR>(tt, q3.y); top_add<SR>(tt, q3.z); top_add<SR>(tt, q3.w);
   }
   float rmin = 0.f, rmax = 0.f;
   if constexpr (SR) {
-    rmin = fmin_nan(__low2float(ts.a1), __high2float(ts.a1));
-    rmax = fmax_nan(__low2float(ts.b1), __high2float(ts.b1));
+    rmin = fmin_nan(fmin_nan(__low2float(ts.a1), __high2float(ts.a1)), fmin_nan(__low2float(tt.a1), __high2float(tt.a1)));
+    rmax = fmax_nan(fmax_nan(__low2float(ts.b1), __high2float(ts.b1)), fmax_nan(__low2float(tt.b1), __high2float(tt.b1)));
   }
 #pragma unroll 1
   for (int r = 1; r < RUNS; ++r) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint4 q = chunk(4 * r + j);
-      top_add<SR>(ts, q.x); top_add<SR>(ts, q.y); top_add<SR>(ts, q.z); top_add<SR>(ts, q.w);
+    for (int j = 0; j < 4; j += 2) {
+      const uint4 q = chunk(4 * r + j), p2 = chunk(4 * r + j + 1);
+      top_add<SR>(ts, q.x); top_add<SR>(tt, p2.x); top_add<SR>(ts, q.y); top_add<SR>(tt, p2.y);
+      top_add<SR>(ts, q.z); top_add<SR>(tt, p2.z); top_add<SR>(ts, q.w); top_add<SR>(tt, p2.w);
     }
     if constexpr (SR) {
-      const float nmin = fmin_nan(__low2float(ts.a1), __high2float(ts.a1));
-      const float nmax = fmax_nan(__low2float(ts.b1), __high2float(ts.b1));
+      const float nmin = fmin_nan(fmin_nan(__low2float(ts.a1), __high2float(ts.a1)),
+                                  fmin_nan(__low2float(tt.a1), __high2float(tt.a1)));
+      const float nmax = fmax_nan(fmax_nan(__low2float(ts.b1), __high2float(ts.b1)),
+                                  fmax_nan(__low2float(tt.b1), __high2float(tt.b1)));
       if (nmin < rmin) ra = r;
       if (nmax > rmax) rz = r;
       rmin = nmin;
       rmax = nmax;
     }
   }
+  top_merge<SR>(ts, tt);
   float mn1, mn2, mx1, mx2;
   top_final<SR>(ts, mn1, mn2, mx1, mx2);
   const bool finite = isfinite(mn1) && isfinite(mx1);

@@ -274,7 +274,7 @@ struct EncGrp {
       attr = true;
     }
     int64_t blocks = (b.total + WARPS - 1) / WARPS;
-    int64_t cap = (int64_t)num_sms() * (G <= 128 ? 3 : 3);
+    int64_t cap = (int64_t)num_sms() * 64;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     kern<<<(unsigned)blocks, WARPS * 32, SMEM, st>>>(b);
@@ -399,131 +399,277 @@ __device__ __forceinline__ uint32_t code_of(const RunRegs<B>& rr, int k) {
   return c;
 }
 
+// Decode v4: warp tile = 4096 elements, lane = 128 consecutive elements
+// (4 runs of 32).  The tile's code planes are cp.async-staged (2 stages,
+// XOR-swizzled per-lane words); the lane's metadata record(s) come straight
+// from global (one record per lane when G >= 128); values are staged in smem
+// and written back with coalesced 16-byte stores.  Requires G % 32 == 0.
+constexpr int kDecWarps = 4;
+constexpr int kDecElems = 128;            // elements per lane (4 runs of 32)
+constexpr int kDecTile = 32 * kDecElems;  // elements per warp tile
+
+template <int B>
+struct DecIn {
+  // unit u of the tile: kDecTile*W/8 bytes = per lane kDecElems*W/8 bytes
+  __host__ __device__ static constexpr int off(int u) {
+    return u == 0 ? 0 : off(u - 1) + kDecTile * unit_w(B, u - 1) / 8;
+  }
+  static constexpr int BYTES = kDecTile * B / 8;
+  // lane l's bytes of unit u: [16*W*l, 16*W*(l+1)); chunk k of lane l (16 B):
+  // swizzled slot so that both the coalesced fill and the per-lane reads are
+  // bank-conflict free
+  template <int W>
+  __device__ static __forceinline__ int slot(int l, int k) {
+    constexpr int CPL = W;  // 16*W bytes per lane = W chunks
+    if constexpr (CPL == 1) return l;
+    else return (l * CPL + k) ^ (((l * CPL + k) >> 3) & (CPL - 1));
+  }
+};
+
 template <typename OT, int B>
-__global__ void __launch_bounds__(256) k_decode_fast(const __grid_constant__ DecBatch b) {
-  constexpr int CPL = (32 * (int)sizeof(OT)) / 16;  // 16-byte chunks per lane (4 bf16 / 8 f32)
-  constexpr int TB = 32 * 32 * (int)sizeof(OT);     // staged bytes per warp tile
-  __shared__ __align__(16) uint8_t stage_all[8 * TB];
+__global__ void __launch_bounds__(kDecWarps * 32) k_decode_fast(const __grid_constant__ DecBatch b) {
+  constexpr int ESZ = (int)sizeof(OT);
+  constexpr int OUT_BYTES = kDecTile * ESZ;
+  constexpr int PER_WARP = 2 * DecIn<B>::BYTES + OUT_BYTES;
+  extern __shared__ __align__(16) uint8_t dsm[];
   const int warp = (int)(threadIdx.x >> 5), lane = (int)lane_id();
-  uint8_t* st = stage_all + warp * TB;
-  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  uint8_t* in0 = dsm + warp * PER_WARP;
+  uint8_t* ost = in0 + 2 * DecIn<B>::BYTES;
+  const int64_t nw = (int64_t)gridDim.x * kDecWarps;
   const int rb = rec_bytes(b.sr, b.intlog);
-  int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-  RunRegs<B> cur, nxt;
-  auto fetch = [&](int64_t tt, RunRegs<B>& rr) {
+  const int G = b.G;
+
+  // cp.async the code planes of tile tt into stage buffer st (zero-fill past n)
+  auto issue = [&](int64_t tt, uint8_t* st) {
     if (tt >= b.total) return;
     const DecJob& jb = b.j[find_job(b, tt)];
-    const int64_t e0 = (tt - jb.t0) * 1024 + lane * 32;
-    if (e0 < jb.n) load_run<B>(jb.pay, jb.n, e0, e0 / b.G, rb, jb.n * B / 8, rr);
+    const int64_t e0 = (tt - jb.t0) * kDecTile;
+#pragma unroll
+    for (int u = 0; u < n_units(B); ++u) {
+      const int W = unit_w(B, u), O = unit_off(B, u);
+      const uint8_t* src = jb.pay + (jb.n * O) / 8 + e0 * W / 8;
+      const int64_t avail = (jb.n - e0) * W / 8;  // bytes of this plane left in the chunk
+      const int total = kDecTile * W / 8;         // 512 * W bytes = 32 * W chunks
+      const bool full = avail >= 512 * W;
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        const int c = lane + 32 * k;  // linear chunk of the tile segment
+        const int l = c / W, kk = c % W;
+        int bytes = 16;
+        if (!full) {
+          const int64_t v = avail - (int64_t)c * 16;
+          bytes = v <= 0 ? 0 : (v >= 16 ? 16 : (int)v);
+        }
+        uint8_t* dst = st + DecIn<B>::off(u) + 16 * (W == 1 ? DecIn<B>::template slot<1>(l, kk)
+                                                 : W == 2 ? DecIn<B>::template slot<2>(l, kk)
+                                                 : W == 4 ? DecIn<B>::template slot<4>(l, kk)
+                                                          : DecIn<B>::template slot<8>(l, kk));
+        cp_async16(dst, bytes ? (const void*)(src + 16 * c) : (const void*)jb.pay, bytes);
+      }
+    }
   };
-  fetch(t, cur);
+
+  int64_t t = (int64_t)blockIdx.x * kDecWarps + warp;
+  issue(t, in0);
+  cp_async_commit();
+  int stage = 0;
   for (; t < b.total; t += nw) {
-    fetch(t + nw, nxt);  // prefetch the next tile while this one is decoded
     const DecJob& jb = b.j[find_job(b, t)];
-    const int64_t ebase = (t - jb.t0) * 1024;
-    const int64_t e0 = ebase + lane * 32;
-    const int64_t lim = jb.n_out;
-    if (e0 < jb.n) {
-      // ---- metadata (R10 layouts)
+    const int64_t ebase = (t - jb.t0) * kDecTile;
+    const int64_t e0 = ebase + (int64_t)lane * kDecElems;
+    const uint8_t* st = in0 + stage * DecIn<B>::BYTES;
+    // metadata record of this lane's first group (in flight with the codes)
+    uint32_t rec[3] = {0, 0, 0};
+    int64_t grp = e0 / G;
+    const bool live = e0 < jb.n;
+    if (live) load_record(jb.pay + jb.n * B / 8 + grp * rb, rec, rb);
+    issue(t + nw, in0 + (stage ^ 1) * DecIn<B>::BYTES);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncwarp();
+    if (live) {
+      constexpr int CPR = 32 * (int)sizeof(OT) / 16;  // output chunks per run
+      constexpr int CPLn = 4 * CPR;                    // output chunks per lane
       GroupMeta m;
-      m.imin = m.imax = -1;
-      m.smin = m.smax = 0.f;
-      if (!b.intlog) {
-        m.s32 = bf16_val(cur.r[0] & 0xFFFFu);
-        m.z32 = bf16_val(cur.r[0] >> 16);
-        if (b.sr) {
-          m.smin = bf16_val(cur.r[1] & 0xFFFFu);
-          m.smax = bf16_val(cur.r[1] >> 16);
-          const float fi = bf16_val(cur.r[2] & 0xFFFFu), fa = bf16_val(cur.r[2] >> 16);
-          if ((fi > -1.0f) && (fi < (float)b.G) && (fa > -1.0f) && (fa < (float)b.G)) {
-            m.imin = (int)fi; m.imax = (int)fa;
-          } else {
-            atomicOr(b.err, FC2_ERR_SPIKE_INDEX);
+      auto decode_meta = [&]() {
+        m.imin = m.imax = -1;
+        m.smin = m.smax = 0.f;
+        m.s64 = 0.0; m.o64 = 0.0;
+        if (!b.intlog) {
+          m.s32 = bf16_val(rec[0] & 0xFFFFu);
+          m.z32 = bf16_val(rec[0] >> 16);
+          if (b.sr) {
+            m.smin = bf16_val(rec[1] & 0xFFFFu);
+            m.smax = bf16_val(rec[1] >> 16);
+            const float fi = bf16_val(rec[2] & 0xFFFFu), fa = bf16_val(rec[2] >> 16);
+            if ((fi > -1.0f) && (fi < (float)G) && (fa > -1.0f) && (fa < (float)G)) {
+              m.imin = (int)fi; m.imax = (int)fa;
+            } else {
+              atomicOr(b.err, FC2_ERR_SPIKE_INDEX);
+            }
+          }
+        } else {
+          const int si = (int)(int8_t)(rec[0] & 0xFFu), zi = (int)(int8_t)((rec[0] >> 8) & 0xFFu);
+          m.s64 = si == -128 ? 0.0 : b.lut[si + 128];
+          m.o64 = __dmul_rn(-(double)zi, m.s64);
+          m.s32 = 0.f; m.z32 = 0.f;
+          if (b.sr) {
+            m.smin = bf16_val(rec[0] >> 16);
+            m.smax = bf16_val(rec[1] & 0xFFFFu);
+            const int ii = (int)((rec[1] >> 16) & 0xFFu), ia = (int)(rec[1] >> 24);
+            if (ii < G && ia < G) { m.imin = ii; m.imax = ia; }
+            else atomicOr(b.err, FC2_ERR_SPIKE_INDEX);
           }
         }
-      } else {
-        const int si = (int)(int8_t)(cur.r[0] & 0xFFu), zi = (int)(int8_t)((cur.r[0] >> 8) & 0xFFu);
-        m.s64 = si == -128 ? 0.0 : b.lut[si + 128];
-        m.o64 = __dmul_rn(-(double)zi, m.s64);
-        if (b.sr) {
-          m.smin = bf16_val(cur.r[0] >> 16);
-          m.smax = bf16_val(cur.r[1] & 0xFFFFu);
-          const int ii = (int)((cur.r[1] >> 16) & 0xFFu), ia = (int)(cur.r[1] >> 24);
-          if (ii < b.G && ia < b.G) { m.imin = ii; m.imax = ia; }
-          else atomicOr(b.err, FC2_ERR_SPIKE_INDEX);
-        }
-      }
-      // ---- values -> stage
-      float v[32];
-      if (!b.intlog) {
-#pragma unroll
-        for (int k = 0; k < 32; k += 2) {
-          float a0, a1;
-          add2(a0, a1, __uint_as_float(0x4B000000u | code_of<B>(cur, k)),
-               __uint_as_float(0x4B000000u | code_of<B>(cur, k + 1)), -8388608.0f, -8388608.0f);
-          fma2(v[k], v[k + 1], a0, a1, m.s32, m.s32, m.z32, m.z32);
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < 32; ++k) v[k] = dq32(code_of<B>(cur, k), m, true);
-      }
-      if constexpr (sizeof(OT) == 4) {
-        if (b.round_bf16) {
-#pragma unroll
-          for (int k = 0; k < 32; ++k) v[k] = bf16_val(bf16_bits(v[k]));
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < CPL; ++j) {
-        uint4 q;
-        if constexpr (sizeof(OT) == 2) {
-          __nv_bfloat162 h0 = __floats2bfloat162_rn(v[8 * j], v[8 * j + 1]);
-          __nv_bfloat162 h1 = __floats2bfloat162_rn(v[8 * j + 2], v[8 * j + 3]);
-          __nv_bfloat162 h2 = __floats2bfloat162_rn(v[8 * j + 4], v[8 * j + 5]);
-          __nv_bfloat162 h3 = __floats2bfloat162_rn(v[8 * j + 6], v[8 * j + 7]);
-          q = make_uint4(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1),
-                         *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3));
-        } else {
-          q = make_uint4(__float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]), __float_as_uint(v[4 * j + 2]),
-                         __float_as_uint(v[4 * j + 3]));
-        }
-        *reinterpret_cast<uint4*>(st + swz<CPL>(CPL * lane + j) * 16) = q;
-      }
-      if (b.sr) {  // imin then imax (codec.py:559-561); positions inside this lane's run
-        const int il = (int)(e0 - (e0 / b.G) * b.G);
+      };
+      // reserved values of the group that starts at element gs (if inside this lane's span)
+      auto patch_spikes = [&](int64_t gs) {
         auto put = [&](int idx, float val) {
           if (sizeof(OT) == 4 && b.round_bf16) val = bf16_val(bf16_bits(val));
-          const int k = idx - il;
-          if (k >= 0 && k < 32) {
-            const int c = CPL * lane + k / (16 / (int)sizeof(OT));
-            const int off = (k % (16 / (int)sizeof(OT))) * (int)sizeof(OT);
-            *reinterpret_cast<OT*>(st + swz<CPL>(c) * 16 + off) = cvt_out<OT>(val);
+          const int64_t k = gs + idx - e0;  // lane-relative element
+          if (k >= 0 && k < kDecElems && gs + idx < jb.n) {
+            const int c = CPLn * lane + (int)k / (16 / (int)sizeof(OT));
+            *reinterpret_cast<OT*>(ost + 16 * (c ^ ((c >> 3) & 7)) + ((int)k % (16 / (int)sizeof(OT))) * (int)sizeof(OT)) =
+                cvt_out<OT>(val);
           }
         };
         if (m.imin >= 0) put(m.imin, m.smin);
         if (m.imax >= 0) put(m.imax, m.smax);
-      }
-    }
-    __syncwarp();
-    // ---- coalesced copy-out (16-byte chunks), bounded by n_out
-    OT* y = reinterpret_cast<OT*>(jb.y) + ebase;
-    const int64_t valid = lim - ebase;  // elements of this tile to write
-    constexpr int EPC = 16 / (int)sizeof(OT);
-    if (valid >= 1024 && (reinterpret_cast<uintptr_t>(y) & 15u) == 0) {
+      };
+      decode_meta();
+#pragma unroll 1
+      for (int r = 0; r < 4; ++r) {
+        const int64_t er = e0 + 32 * r;
+        if (er >= jb.n) break;
+        const int64_t g_r = er / G;
+        if (g_r != grp) {  // next group (G < 128): finish the previous one first
+          if (b.sr) patch_spikes(grp * G);
+          grp = g_r;
+          load_record(jb.pay + jb.n * B / 8 + grp * rb, rec, rb);
+          decode_meta();
+        }
+        // ---- codes of this 32-element run from the stage
+        RunRegs<B> rr;
 #pragma unroll
-      for (int j = 0; j < CPL; ++j) {
-        const int c = lane + 32 * j;
-        *reinterpret_cast<uint4*>(y + c * EPC) = *reinterpret_cast<const uint4*>(st + swz<CPL>(c) * 16);
+        for (int u = 0; u < n_units(B); ++u) {
+          const int W = unit_w(B, u), O = unit_off(B, u);
+          const uint8_t* base = st + DecIn<B>::off(u);
+          if (W == 8) {
+            const int k0 = 2 * r;
+            const uint4 q0 = *reinterpret_cast<const uint4*>(base + 16 * DecIn<B>::template slot<8>(lane, k0));
+            const uint4 q1 = *reinterpret_cast<const uint4*>(base + 16 * DecIn<B>::template slot<8>(lane, k0 + 1));
+            rr.w[O + 0] = q0.x; rr.w[O + 1] = q0.y; rr.w[O + 2] = q0.z; rr.w[O + 3] = q0.w;
+            rr.w[O + 4] = q1.x; rr.w[O + 5] = q1.y; rr.w[O + 6] = q1.z; rr.w[O + 7] = q1.w;
+          } else if (W == 4) {
+            const uint4 q0 = *reinterpret_cast<const uint4*>(base + 16 * DecIn<B>::template slot<4>(lane, r));
+            rr.w[O + 0] = q0.x; rr.w[O + 1] = q0.y; rr.w[O + 2] = q0.z; rr.w[O + 3] = q0.w;
+          } else if (W == 2) {
+            const uint2 q0 = *reinterpret_cast<const uint2*>(base + 16 * DecIn<B>::template slot<2>(lane, r >> 1) + 8 * (r & 1));
+            rr.w[O + 0] = q0.x; rr.w[O + 1] = q0.y;
+          } else {
+            rr.w[O] = *reinterpret_cast<const uint32_t*>(base + 16 * DecIn<B>::template slot<1>(lane, 0) + 4 * r);
+          }
+        }
+        // ---- codes -> exact floats (2^23 + code, as bit patterns)
+        uint32_t cf[32];
+        if constexpr (B == 4) {  // nibbles: PRMT byte k of (w & 0x0F..) into 0x4B0000cc
+#pragma unroll
+          for (int wd = 0; wd < 4; ++wd) {
+            const uint32_t ev = rr.w[wd] & 0x0F0F0F0Fu, od = (rr.w[wd] >> 4) & 0x0F0F0F0Fu;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              cf[8 * wd + 2 * k] = __byte_perm(ev, 0x4B000000u, 0x7650 + k);
+              cf[8 * wd + 2 * k + 1] = __byte_perm(od, 0x4B000000u, 0x7650 + k);
+            }
+          }
+        } else if constexpr (B == 8) {
+#pragma unroll
+          for (int wd = 0; wd < 8; ++wd)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) cf[4 * wd + k] = __byte_perm(rr.w[wd], 0x4B000000u, 0x7650 + k);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 32; ++k) cf[k] = 0x4B000000u | code_of<B>(rr, k);
+        }
+        // ---- values
+        float v[32];
+        if (!b.intlog) {
+#pragma unroll
+          for (int k = 0; k < 32; k += 2) {
+            float a0, a1;
+            add2(a0, a1, __uint_as_float(cf[k]), __uint_as_float(cf[k + 1]), -8388608.0f, -8388608.0f);
+            fma2(v[k], v[k + 1], a0, a1, m.s32, m.s32, m.z32, m.z32);
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 32; ++k) v[k] = dq32(cf[k] & 0xFFu, m, true);
+        }
+        if constexpr (sizeof(OT) == 4) {
+          if (b.round_bf16) {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) v[k] = bf16_val(bf16_bits(v[k]));
+          }
+        }
+        // ---- stage: this run's CPR chunks of the lane segment
+        const int cbase = CPLn * lane + CPR * r;
+#pragma unroll
+        for (int j = 0; j < CPR; ++j) {
+          uint4 q;
+          if constexpr (sizeof(OT) == 2) {
+            __nv_bfloat162 h0 = __floats2bfloat162_rn(v[8 * j], v[8 * j + 1]);
+            __nv_bfloat162 h1 = __floats2bfloat162_rn(v[8 * j + 2], v[8 * j + 3]);
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(v[8 * j + 4], v[8 * j + 5]);
+            __nv_bfloat162 h3 = __floats2bfloat162_rn(v[8 * j + 6], v[8 * j + 7]);
+            q = make_uint4(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1),
+                           *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3));
+          } else {
+            q = make_uint4(__float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]), __float_as_uint(v[4 * j + 2]),
+                           __float_as_uint(v[4 * j + 3]));
+          }
+          const int c = cbase + j;
+          *reinterpret_cast<uint4*>(ost + 16 * (c ^ ((c >> 3) & 7))) = q;
+        }
       }
+      if (b.sr) patch_spikes(grp * G);
+    }
+    __syncwarp();
+    // ---- coalesced copy-out, bounded by n_out
+    OT* y = reinterpret_cast<OT*>(jb.y) + ebase;
+    const int64_t valid = jb.n_out - ebase;
+    constexpr int EPC = 16 / ESZ;
+    constexpr int NCH = kDecTile / EPC;
+    if (valid >= kDecTile && (reinterpret_cast<uintptr_t>(y) & 15u) == 0) {
+#pragma unroll 4
+      for (int c = lane; c < NCH; c += 32)
+        *reinterpret_cast<uint4*>(y + c * EPC) = *reinterpret_cast<const uint4*>(ost + 16 * (c ^ ((c >> 3) & 7)));
     } else {
-      for (int i = lane; i < valid && i < 1024; i += 32) {
+      for (int i = lane; i < valid && i < kDecTile; i += 32) {
         const int c = i / EPC;
-        y[i] = *reinterpret_cast<const OT*>(st + swz<CPL>(c) * 16 + (i % EPC) * (int)sizeof(OT));
+        y[i] = *reinterpret_cast<const OT*>(ost + 16 * (c ^ ((c >> 3) & 7)) + (i % EPC) * ESZ);
       }
     }
     __syncwarp();
-    cur = nxt;
+    stage ^= 1;
   }
+  cp_async_wait<0>();
+}
+
+template <typename OT, int B>
+int launch_decode_fast(const DecBatch& b, cudaStream_t st) {
+  constexpr int SMEM = kDecWarps * (2 * DecIn<B>::BYTES + kDecTile * (int)sizeof(OT));
+  auto kern = k_decode_fast<OT, B>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    attr = true;
+  }
+  // one tile per warp: the block scheduler balances the tail (no persistent loop)
+  int64_t blocks = (b.total + kDecWarps - 1) / kDecWarps;
+  const int64_t cap = (int64_t)num_sms() * 64;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  kern<<<(unsigned)blocks, kDecWarps * 32, SMEM, st>>>(b);
+  return cuda_check("k_decode_fast");
 }
 
 // generic decode: thread per element (any G, any output type)
@@ -720,9 +866,9 @@ struct Launchers {
     return sr ? Launchers<BB>::red<true>(G, a, st) : Launchers<BB>::red<false>(G, a, st);     \
   }                                                                                            \
   template <> int launch_dec_fast<BB>(int dtype, int64_t blocks, const DecBatch& b, cudaStream_t st) { \
-    if (dtype == FC2_BF16) k_decode_fast<__nv_bfloat16, BB><<<(unsigned)blocks, 256, 0, st>>>(b); \
-    else k_decode_fast<float, BB><<<(unsigned)blocks, 256, 0, st>>>(b);                        \
-    return cuda_check("k_decode_fast");                                                        \
+    (void)blocks;                                                                              \
+    return dtype == FC2_BF16 ? launch_decode_fast<__nv_bfloat16, BB>(b, st)                     \
+                             : launch_decode_fast<float, BB>(b, st);                            \
   }
 
 }  // namespace fc2
