@@ -8,6 +8,7 @@
 #include "fc2_decode.cuh"
 #include "fc2_encode.cuh"
 #include "fc2_encode_group.cuh"
+#include "fc2_reduce_group.cuh"
 
 namespace fc2 {
 
@@ -807,6 +808,169 @@ struct EncFast {
     else { FC2_G_CASES(BB, false) }           \
     break;
 
+// ---------------------------------------------------------------------------
+// reduce + requantize, lane-per-group (fc2_reduce_group.cuh)
+// ---------------------------------------------------------------------------
+
+template <int B>
+__device__ __forceinline__ void load_run_words(const uint8_t* pay, int64_t n, int64_t e, uint32_t* w) {
+#pragma unroll
+  for (int u = 0; u < n_units(B); ++u) {
+    const int W = unit_w(B, u), O = unit_off(B, u);
+    const uint8_t* p = pay + (n * O) / 8 + (e * W) / 8;
+    if (W == 8) {
+      const uint4 q0 = *reinterpret_cast<const uint4*>(p), q1 = *reinterpret_cast<const uint4*>(p + 16);
+      w[O] = q0.x; w[O + 1] = q0.y; w[O + 2] = q0.z; w[O + 3] = q0.w;
+      w[O + 4] = q1.x; w[O + 5] = q1.y; w[O + 6] = q1.z; w[O + 7] = q1.w;
+    } else if (W == 4) {
+      const uint4 q0 = *reinterpret_cast<const uint4*>(p);
+      w[O] = q0.x; w[O + 1] = q0.y; w[O + 2] = q0.z; w[O + 3] = q0.w;
+    } else if (W == 2) {
+      const uint2 q0 = *reinterpret_cast<const uint2*>(p);
+      w[O] = q0.x; w[O + 1] = q0.y;
+    } else {
+      w[O] = *reinterpret_cast<const uint32_t*>(p);
+    }
+  }
+}
+
+template <int B, bool SR, int G, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_reduce_grp(const __grid_constant__ ReduceArgs a) {
+  using IT = GTile<float, G>;
+  constexpr int RUNS = G / 32;
+  constexpr int PER_WARP = IT::IN_BYTES + OutStage<B, G>::BYTES;
+  constexpr int BATCH = B <= 4 ? kRedMaxSrc : kRedMaxSrc / 2;  // sources whose codes are in flight together
+  extern __shared__ __align__(16) uint8_t rsm[];
+  const int warp = (int)(threadIdx.x >> 5), lane = (int)lane_id();
+  uint8_t* tile = rsm + warp * PER_WARP;
+  uint8_t* ost = tile + IT::IN_BYTES;
+  const int64_t nw = (int64_t)gridDim.x * WARPS;
+  const int64_t ngroups = a.n / G;
+  const int rb = rec_bytes(SR, a.intlog != 0);
+  const int64_t meta_off = a.n * B / 8;
+  EncCtx cx;
+  cx.n = a.n; cx.meta_off = meta_off; cx.intlog = a.intlog; cx.theta = a.theta; cx.lut = a.lut; cx.err = a.err;
+  for (int64_t t = (int64_t)blockIdx.x * WARPS + warp; t < a.total; t += nw) {
+    const int64_t tg0 = t * 32, g = tg0 + lane;
+    const bool active = g < ngroups;
+    const int64_t gc = active ? g : 0;
+    const int ng = (int)min((int64_t)32, ngroups - tg0);
+    // raw metadata records of every source for this group
+    uint32_t rec[kRedMaxSrc][3];
+#pragma unroll
+    for (int s = 0; s < kRedMaxSrc; ++s)
+      if (s < a.nsrc) load_record(a.src[s] + meta_off + gc * rb, rec[s], rb);
+#pragma unroll 1
+    for (int r = 0; r < RUNS; ++r) {
+      const int64_t er = gc * G + 32 * r;
+      float acc[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) acc[k] = 0.0f;  // acc = zeros(float32) (collectives.py:293)
+#pragma unroll
+      for (int s0 = 0; s0 < kRedMaxSrc; s0 += BATCH) {
+        uint32_t cw[BATCH][B];
+#pragma unroll
+        for (int i = 0; i < BATCH; ++i)
+          if (s0 + i < a.nsrc) load_run_words<B>(a.src[s0 + i], a.n, er, cw[i]);
+#pragma unroll
+        for (int i = 0; i < BATCH; ++i) {
+          const int s = s0 + i;
+          if (s >= a.nsrc) break;
+          // metadata of source s (R10 layouts)
+          float s32 = 0.f, z32 = 0.f, smin = 0.f, smax = 0.f;
+          double s64 = 0.0, o64 = 0.0;
+          int imin = -1, imax = -1;
+          if (!a.intlog) {
+            s32 = bf16_val(rec[s][0] & 0xFFFFu);
+            z32 = bf16_val(rec[s][0] >> 16);
+            if constexpr (SR) {
+              smin = bf16_val(rec[s][1] & 0xFFFFu);
+              smax = bf16_val(rec[s][1] >> 16);
+              const float fi = bf16_val(rec[s][2] & 0xFFFFu), fa = bf16_val(rec[s][2] >> 16);
+              if ((fi > -1.0f) && (fi < (float)G) && (fa > -1.0f) && (fa < (float)G)) {
+                imin = (int)fi; imax = (int)fa;
+              } else if (active && r == 0) {
+                atomicOr(a.err, FC2_ERR_SPIKE_INDEX);
+              }
+            }
+          } else {
+            const int si = (int)(int8_t)(rec[s][0] & 0xFFu), zi = (int)(int8_t)((rec[s][0] >> 8) & 0xFFu);
+            s64 = si == -128 ? 0.0 : a.lut[si + 128];
+            o64 = __dmul_rn(-(double)zi, s64);
+            if constexpr (SR) {
+              smin = bf16_val(rec[s][0] >> 16);
+              smax = bf16_val(rec[s][1] & 0xFFFFu);
+              const int ii = (int)((rec[s][1] >> 16) & 0xFFu), ia = (int)(rec[s][1] >> 24);
+              if (ii < G && ia < G) { imin = ii; imax = ia; }
+              else if (active && r == 0) atomicOr(a.err, FC2_ERR_SPIKE_INDEX);
+            }
+          }
+          uint32_t cf[32];
+          run_code_floats<B>(cw[i], cf);
+          float d[32];
+          if (!a.intlog) {
+#pragma unroll
+            for (int k = 0; k < 32; k += 2) {
+              float c0, c1;
+              add2(c0, c1, __uint_as_float(cf[k]), __uint_as_float(cf[k + 1]), -8388608.0f, -8388608.0f);
+              fma2(d[k], d[k + 1], c0, c1, s32, s32, z32, z32);
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < 32; ++k)
+              d[k] = __double2float_rn(__dadd_rn(__dmul_rn((double)(cf[k] & 0xFFu), s64), o64));
+          }
+          if constexpr (SR) {  // reserved values: imin then imax, via the lane's run region
+            const int ka = imin - 32 * r, kz = imax - 32 * r;
+            const bool ha = ka >= 0 && ka < 32, hz = kz >= 0 && kz < 32;
+            if (__any_sync(0xffffffffu, ha || hz)) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                *reinterpret_cast<float4*>(tile + IT::in_pos(lane, 8 * r + j) * 16) =
+                    make_float4(d[4 * j], d[4 * j + 1], d[4 * j + 2], d[4 * j + 3]);
+              if (ha) *reinterpret_cast<float*>(tile + IT::in_pos(lane, 8 * r + (ka >> 2)) * 16 + (ka & 3) * 4) = smin;
+              if (hz) *reinterpret_cast<float*>(tile + IT::in_pos(lane, 8 * r + (kz >> 2)) * 16 + (kz & 3) * 4) = smax;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float4 q = *reinterpret_cast<const float4*>(tile + IT::in_pos(lane, 8 * r + j) * 16);
+                d[4 * j] = q.x; d[4 * j + 1] = q.y; d[4 * j + 2] = q.z; d[4 * j + 3] = q.w;
+              }
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < 32; k += 2) add2(acc[k], acc[k + 1], acc[k], acc[k + 1], d[k], d[k + 1]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        *reinterpret_cast<float4*>(tile + IT::in_pos(lane, 8 * r + j) * 16) =
+            make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+    }
+    __syncwarp();
+    encode_tile_f32<B, SR, G>(tile, ost, active, g, cx, a.dst, a.ndst, tg0, ng);
+  }
+}
+
+template <int B, bool SR, int G>
+struct RedGrp {
+  static constexpr int WARPS = G <= 128 ? 4 : 2;
+  static constexpr int SMEM = WARPS * (GTile<float, G>::IN_BYTES + OutStage<B, G>::BYTES);
+  static int go(const ReduceArgs& a0, cudaStream_t st) {
+    ReduceArgs a = a0;
+    a.total = (a.n / G + 31) / 32;
+    auto kern = k_reduce_grp<B, SR, G, WARPS>;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+      attr = true;
+    }
+    int64_t blocks = (a.total + WARPS - 1) / WARPS;
+    if (blocks < 1) blocks = 1;
+    kern<<<(unsigned)blocks, WARPS * 32, SMEM, st>>>(a);
+    return cuda_check("k_reduce_grp");
+  }
+};
+
 template <int B, bool SR, int G>
 struct EncFastBf16 {
   static int go(const EncBatch& b, cudaStream_t st) { return EncFast<B, SR, G>::template launch<__nv_bfloat16>(b, st); }
@@ -848,6 +1012,17 @@ struct Launchers {
   }
   template <bool SR>
   static int red(int G, const ReduceArgs& a, cudaStream_t st) {
+    bool grp = a.nsrc <= kRedMaxSrc;
+    for (int s = 0; s < a.nsrc; ++s)
+      if (reinterpret_cast<uintptr_t>(a.src[s]) & 15u) grp = false;
+    if (grp) {
+      switch (G) {
+        case 32: return RedGrp<B, SR, 32>::go(a, st);
+        case 64: return RedGrp<B, SR, 64>::go(a, st);
+        case 128: return RedGrp<B, SR, 128>::go(a, st);
+        case 256: return RedGrp<B, SR, 256>::go(a, st);
+      }
+    }
     switch (G) {
       case 32: return RedFast<B, SR, 32>::go(a, st);
       case 64: return RedFast<B, SR, 64>::go(a, st);
