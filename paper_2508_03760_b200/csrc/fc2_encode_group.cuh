@@ -20,14 +20,20 @@
 
 namespace fc2 {
 
-template <typename T, int G>
+template <typename T, int G, int LPG = 1>
 struct GTile {
   static constexpr int CPG = G * (int)sizeof(T) / 16;   // input chunks per group
   static constexpr int IN_BYTES = 32 * G * (int)sizeof(T);
-  // input swizzle: chunk c of group g -> slot g*CPG + (c ^ (g & m)), m < 8
+  // input swizzle: chunk c of group g -> slot g*CPG + (c ^ s).  With LPG lanes
+  // per group, s mixes in the reading lane (g*LPG + part) so that 8 lanes
+  // reading "their" chunk hit 8 different 16-byte bank groups.
   static constexpr int IM = CPG >= 8 ? 7 : CPG - 1;
   __device__ static __forceinline__ int in_pos(int g, int c) {
-    return g * CPG + (c ^ (CPG >= 8 ? (g & 7) : ((g >> (CPG == 4 ? 1 : (CPG == 2 ? 2 : 3))) & IM)));
+    if constexpr (CPG >= 8) {
+      return g * CPG + (c ^ ((g * LPG + c / (CPG / LPG)) & 7));
+    } else {
+      return g * CPG + (c ^ ((g >> (CPG == 4 ? 1 : (CPG == 2 ? 2 : 3))) & IM));
+    }
   }
 };
 
@@ -60,27 +66,27 @@ struct OTile {
   }
 };
 
-template <int B, int G>
-struct OutStage {
+template <int B, int G, int GPT = 32>
+struct OutStage {  // GPT groups per tile
   static constexpr int NU = n_units(B);
   __host__ __device__ static constexpr int off(int u) {
-    return u == 0 ? 0 : off(u - 1) + 32 * G * unit_w(B, u - 1) / 8;
+    return u == 0 ? 0 : off(u - 1) + GPT * G * unit_w(B, u - 1) / 8;
   }
-  static constexpr int BYTES = 32 * G * B / 8;
+  static constexpr int BYTES = GPT * G * B / 8;
 };
 
-// patch element e (group-relative) of lane g with code c in the output stage
-template <int B, int G>
+// patch element e (group-relative) of group g with code c in the output stage
+template <int B, int G, int GPT = 32>
 __device__ __forceinline__ void stage_patch(uint8_t* ost, int g, int e, int c) {
 #pragma unroll
   for (int u = 0; u < n_units(B); ++u) {
     const int W = unit_w(B, u), O = unit_off(B, u);
     const int bit = e * W;
     uint8_t* p;
-    if (W == 1) p = ost + OutStage<B, G>::off(u) + OTile<G, 1>::byte_pos(g, bit >> 3);
-    else if (W == 2) p = ost + OutStage<B, G>::off(u) + OTile<G, 2>::byte_pos(g, bit >> 3);
-    else if (W == 4) p = ost + OutStage<B, G>::off(u) + OTile<G, 4>::byte_pos(g, bit >> 3);
-    else p = ost + OutStage<B, G>::off(u) + OTile<G, 8>::byte_pos(g, bit >> 3);
+    if (W == 1) p = ost + OutStage<B, G, GPT>::off(u) + OTile<G, 1>::byte_pos(g, bit >> 3);
+    else if (W == 2) p = ost + OutStage<B, G, GPT>::off(u) + OTile<G, 2>::byte_pos(g, bit >> 3);
+    else if (W == 4) p = ost + OutStage<B, G, GPT>::off(u) + OTile<G, 4>::byte_pos(g, bit >> 3);
+    else p = ost + OutStage<B, G, GPT>::off(u) + OTile<G, 8>::byte_pos(g, bit >> 3);
     const uint32_t m = ((1u << W) - 1u) << (bit & 7);
     const uint32_t v = (((uint32_t)c >> O) << (bit & 7)) & m;
     *p = (uint8_t)((*p & ~m) | v);
@@ -175,24 +181,26 @@ __device__ __forceinline__ void top_final(const TopState& s, float& mn1, float& 
 // time (MODE 0: folded fma, 1: explicit v - off, 2: INT_LOG clamped).
 // Writes packed words into the output stage, returns per-run tie masks in
 // split layout (bit i < 16: element 2i; bit 16 + i: element 2i + 1).
-template <int B, int G, int MODE>
+template <int B, int G, int MODE, int LPG>
 __device__ __forceinline__ void quant_runs(const uint8_t* ist, uint8_t* ost, const GroupParams& p, float Lh,
                                            bool active) {
-  using IT = GTile<__nv_bfloat16, G>;
-  constexpr int RUNS = G / 32;
+  using IT = GTile<__nv_bfloat16, G, LPG>;
+  constexpr int GPT = 32 / LPG;
+  constexpr int RUNS = G / 32 / LPG;  // runs of this lane
+  const int gl = (int)lane_id() / LPG, r0 = ((int)lane_id() % LPG) * RUNS;
   constexpr int FB = FixFor<B>::FB;
   using FX = Fix<FB>;
-  const int lane = (int)lane_id();
   constexpr int L = (1 << B) - 1;
 #pragma unroll 2
-  for (int r = 0; r < RUNS; ++r) {
+  for (int rr = 0; rr < RUNS; ++rr) {
+    const int r = r0 + rr;  // run index inside the group
     LaneWords<B> lw;
     lw.clear();
     uint32_t tmj[2] = {0u, 0u};  // two accumulators: shorter dependency chains
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       uint32_t& tm = tmj[j & 1];
-      const uint4 q = *reinterpret_cast<const uint4*>(ist + IT::in_pos(lane, 4 * r + j) * 16);
+      const uint4 q = *reinterpret_cast<const uint4*>(ist + IT::in_pos(gl, 4 * r + j) * 16);
       const uint32_t ww[4] = {q.x, q.y, q.z, q.w};
       uint32_t X[8];
 #pragma unroll
@@ -222,12 +230,12 @@ __device__ __forceinline__ void quant_runs(const uint8_t* ist, uint8_t* ost, con
 #pragma unroll
     for (int u = 0; u < n_units(B); ++u) {
       const int W = unit_w(B, u);
-      uint8_t* base = ost + OutStage<B, G>::off(u);
+      uint8_t* base = ost + OutStage<B, G, GPT>::off(u);
       const uint32_t* w = lw.w + LaneWords<B>::base(u);
-      if (W == 1) stage_words<G, 1>(base, lane, r, w);
-      else if (W == 2) stage_words<G, 2>(base, lane, r, w);
-      else if (W == 4) stage_words<G, 4>(base, lane, r, w);
-      else stage_words<G, 8>(base, lane, r, w);
+      if (W == 1) stage_words<G, 1>(base, gl, r, w);
+      else if (W == 2) stage_words<G, 2>(base, gl, r, w);
+      else if (W == 4) stage_words<G, 4>(base, gl, r, w);
+      else stage_words<G, 8>(base, gl, r, w);
     }
     // exact float64 recompute of near-tie elements (rare), patched in smem;
     // split layout: bit i < 16 -> element 2i, bit 16 + i -> element 2i + 1
@@ -237,8 +245,8 @@ __device__ __forceinline__ void quant_runs(const uint8_t* ist, uint8_t* ost, con
       tm &= tm - 1;
       const int e = 32 * r + (k < 16 ? 2 * k : 2 * (k - 16) + 1);
       const float v = __uint_as_float(
-          (uint32_t)*reinterpret_cast<const uint16_t*>(ist + IT::in_pos(lane, e >> 3) * 16 + (e & 7) * 2) << 16);
-      stage_patch<B, G>(ost, lane, e, exact_code((double)v, p.off, p.div, L));
+          (uint32_t)*reinterpret_cast<const uint16_t*>(ist + IT::in_pos(gl, e >> 3) * 16 + (e & 7) * 2) << 16);
+      stage_patch<B, G, GPT>(ost, gl, e, exact_code((double)v, p.off, p.div, L));
     }
   }
 }
@@ -247,16 +255,18 @@ __device__ __forceinline__ void quant_runs(const uint8_t* ist, uint8_t* ost, con
 // the kernel body for one warp tile (bf16 input)
 // ---------------------------------------------------------------------------
 
-template <int B, bool SR, int G>
+template <int B, bool SR, int G, int LPG>
 __device__ __forceinline__ void encode_tile_bf16(const uint8_t* ist, uint8_t* ost, bool active, int64_t g_abs,
                                                  const EncCtx& cx, uint8_t* out, int64_t tile_g0, int ng) {
-  using IT = GTile<__nv_bfloat16, G>;
-  constexpr int CPG = IT::CPG;  // 8 bf16 per chunk
+  using IT = GTile<__nv_bfloat16, G, LPG>;
+  constexpr int GPT = 32 / LPG;
   constexpr int L = (1 << B) - 1;
   const int lane = (int)lane_id();
-  auto chunk = [&](int c) -> uint4 { return *reinterpret_cast<const uint4*>(ist + IT::in_pos(lane, c) * 16); };
+  const int gl = lane / LPG, li = lane % LPG;   // group of the tile, part of the group
+  constexpr int RUNS = G / 32 / LPG;            // 32-element runs of this lane
+  const int r0 = li * RUNS;                     // first run (group-relative)
+  auto chunk = [&](int c) -> uint4 { return *reinterpret_cast<const uint4*>(ist + IT::in_pos(gl, c) * 16); };
 
-  constexpr int RUNS = G / 32;
   constexpr int FB = FixFor<B>::FB;
   using FX = Fix<FB>;
 
@@ -265,14 +275,14 @@ __device__ __forceinline__ void encode_tile_bf16(const uint8_t* ist, uint8_t* os
   // Two independent accumulator sets (even / odd chunks) halve the
   // dependency chains; they are merged per run for the running extremes.
   TopState ts, tt;
-  int ra = 0, rz = 0;
+  int ra = r0, rz = r0;
   {
-    const uint4 q0 = chunk(0), q1 = chunk(1);
+    const uint4 q0 = chunk(4 * r0), q1 = chunk(4 * r0 + 1);
     top_init(ts, q0.x);
     top_add<SR>(ts, q0.y); top_add<SR>(ts, q0.z); top_add<SR>(ts, q0.w);
     top_init(tt, q1.x);
     top_add<SR>(tt, q1.y); top_add<SR>(tt, q1.z); top_add<SR>(tt, q1.w);
-    const uint4 q2 = chunk(2), q3 = chunk(3);
+    const uint4 q2 = chunk(4 * r0 + 2), q3 = chunk(4 * r0 + 3);
     top_add<SR>(ts, q2.x); top_add<SR>(ts, q2.y); top_add<SR>(ts, q2.z); top_add<SR>(ts, q2.w);
     top_add<SR>(tt, q3.x); top_add<SR>(tt, q3.y); top_add<SR>(tt, q3.z); top_add<SR>(tt, q3.w);
   }
@@ -282,7 +292,7 @@ __device__ __forceinline__ void encode_tile_bf16(const uint8_t* ist, uint8_t* os
     rmax = fmax_nan(fmax_nan(__low2float(ts.b1), __high2float(ts.b1)), fmax_nan(__low2float(tt.b1), __high2float(tt.b1)));
   }
 #pragma unroll 1
-  for (int r = 1; r < RUNS; ++r) {
+  for (int r = r0 + 1; r < r0 + RUNS; ++r) {
 #pragma unroll
     for (int j = 0; j < 4; j += 2) {
       const uint4 q = chunk(4 * r + j), p2 = chunk(4 * r + j + 1);
@@ -303,12 +313,26 @@ __device__ __forceinline__ void encode_tile_bf16(const uint8_t* ist, uint8_t* os
   top_merge<SR>(ts, tt);
   float mn1, mn2, mx1, mx2;
   top_final<SR>(ts, mn1, mn2, mx1, mx2);
+  const float lmin = mn1, lmax = mx1;  // this lane's own extremes
+#pragma unroll
+  for (int o = 1; o < LPG; o <<= 1) {  // merge the LPG parts of the group
+    const float a1 = __shfl_xor_sync(0xffffffffu, mn1, o), b1 = __shfl_xor_sync(0xffffffffu, mx1, o);
+    if constexpr (SR) {
+      const float a2 = __shfl_xor_sync(0xffffffffu, mn2, o), b2 = __shfl_xor_sync(0xffffffffu, mx2, o);
+      mn2 = fmin_nan(fmax_nan(mn1, a1), fmin_nan(mn2, a2));
+      mx2 = fmax_nan(fmin_nan(mx1, b1), fmax_nan(mx2, b2));
+    }
+    mn1 = fmin_nan(mn1, a1);
+    mx1 = fmax_nan(mx1, b1);
+  }
+  if (!SR) { mn2 = mn1; mx2 = mx1; }
   const bool finite = isfinite(mn1) && isfinite(mx1);
-  if (active && !finite) atomicOr(cx.err, FC2_ERR_NONFINITE);
+  if (active && !finite && li == 0) atomicOr(cx.err, FC2_ERR_NONFINITE);
 
   // ---- spikes: first argmin / argmax (codec.py:259-266) ---------------------
   // The running minimum first equals the group minimum in the run holding its
-  // first occurrence; only that run is searched.
+  // first occurrence; only that run is searched (by the lane whose part holds
+  // the group extreme), then the lowest index over the group's lanes wins.
   int imin = 0, imax = 1;
   uint32_t smin_bits = 0, smax_bits = 0;
   if constexpr (SR) {
@@ -327,14 +351,20 @@ __device__ __forceinline__ void encode_tile_bf16(const uint8_t* ist, uint8_t* os
       const int f = min(lo ? 2 * (__ffs(lo) - 1) : 64, hi ? 2 * (__ffs(hi) - 1) + 1 : 64);
       return f < 32 ? 32 * r + f : 1 << 20;
     };
-    int fi = first_in_run(ra, mn1), fa = first_in_run(rz, mx1);
+    int fi = (lmin == mn1) ? first_in_run(ra, mn1) : 1 << 20;
+    int fa = (lmax == mx1) ? first_in_run(rz, mx1) : 1 << 20;
+#pragma unroll
+    for (int o = 1; o < LPG; o <<= 1) {
+      fi = min(fi, __shfl_xor_sync(0xffffffffu, fi, o));
+      fa = min(fa, __shfl_xor_sync(0xffffffffu, fa, o));
+    }
     if (fi >= G) fi = 0;  // only with NaN input (already flagged)
     if (fa >= G) fa = 1;
     if (fi == fa) { fi = 0; fa = 1; }
     imin = fi; imax = fa;
     // reserved values are the elements themselves (codec.py:492-493)
     auto elem = [&](int e) -> uint32_t {
-      return *reinterpret_cast<const uint16_t*>(ist + IT::in_pos(lane, e >> 3) * 16 + (e & 7) * 2);
+      return *reinterpret_cast<const uint16_t*>(ist + IT::in_pos(gl, e >> 3) * 16 + (e & 7) * 2);
     };
     smin_bits = elem(imin);
     smax_bits = elem(imax);
@@ -348,25 +378,25 @@ __device__ __forceinline__ void encode_tile_bf16(const uint8_t* ist, uint8_t* os
   const bool fold_ok = !p.exact && fabsf(p.nz) <= FX::kFold;
   const float Lh = (float)L + 0.5f;
   if (cx.intlog) {
-    quant_runs<B, G, 2>(ist, ost, p, Lh, active);
+    quant_runs<B, G, 2, LPG>(ist, ost, p, Lh, active);
   } else if (__all_sync(0xffffffffu, fold_ok || p.exact || !active)) {
-    quant_runs<B, G, 0>(ist, ost, p, Lh, active);
+    quant_runs<B, G, 0, LPG>(ist, ost, p, Lh, active);
   } else {
-    quant_runs<B, G, 1>(ist, ost, p, Lh, active);
+    quant_runs<B, G, 1, LPG>(ist, ost, p, Lh, active);
   }
   if constexpr (SR) {  // reserved slots are quantized as 0.0 (codec.py:494-496)
     int sc;
     const uint32_t Xs = fixq_clamped<FB>(0.0f, p.off32, p.inv32, (float)L + 0.5f);
     if (p.exact || (Xs & FX::kTie) == 0u) sc = exact_code(0.0, p.off, p.div, L);
     else sc = (int)((Xs >> FB) & (uint32_t)L);
-    if (active) {
-      stage_patch<B, G>(ost, lane, imin, sc);
-      stage_patch<B, G>(ost, lane, imax, sc);
+    if (active) {  // the lane owning the element patches it
+      if (imin / (G / LPG) == li) stage_patch<B, G, GPT>(ost, gl, imin, sc);
+      if (imax / (G / LPG) == li) stage_patch<B, G, GPT>(ost, gl, imax, sc);
     }
   }
 
-  // ---- metadata record (R10), straight from the owning lane ---------------
-  if (active) {
+  // ---- metadata record (R10), straight from the group's first lane ---------
+  if (active && li == 0) {
     uint32_t rec[3];
     int rb;
     if (!cx.intlog) {
@@ -395,7 +425,7 @@ __device__ __forceinline__ void encode_tile_bf16(const uint8_t* ist, uint8_t* os
 #pragma unroll
   for (int u = 0; u < n_units(B); ++u) {
     const int W = unit_w(B, u), O = unit_off(B, u);
-    const uint8_t* base = ost + OutStage<B, G>::off(u);
+    const uint8_t* base = ost + OutStage<B, G, GPT>::off(u);
     uint8_t* dst = out + (cx.n * O) / 8 + tile_g0 * (G * W / 8);
     if (W == 1) copy_out<G, 1>(base, dst, ng);
     else if (W == 2) copy_out<G, 2>(base, dst, ng);

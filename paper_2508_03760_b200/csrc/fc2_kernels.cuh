@@ -197,25 +197,26 @@ __global__ void __launch_bounds__(kEncWarps * 32) k_encode_fast(const __grid_con
 // lane-per-group encoder (bf16 input, G in {32,64,128,256})
 // ---------------------------------------------------------------------------
 
-template <int G>
+template <int G, int LPG>
 __device__ __forceinline__ void issue_grp_tile(const EncBatch& b, int64_t t, uint8_t* stage) {
-  using IT = GTile<__nv_bfloat16, G>;
+  using IT = GTile<__nv_bfloat16, G, LPG>;
+  constexpr int GPT = 32 / LPG;  // groups per warp tile
   const int ji = find_job(b, t);
   const EncJob& jb = b.j[ji];
-  const int64_t e0 = (t - jb.t0) * 32 * G;
+  const int64_t e0 = (t - jb.t0) * GPT * G;
   const int lane = (int)lane_id();
   const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(jb.x);
-  if (e0 + 32 * G <= jb.n_valid) {  // whole tile present: plain 16-byte copies
+  if (e0 + GPT * G <= jb.n_valid) {  // whole tile present: plain 16-byte copies
     const uint8_t* src = reinterpret_cast<const uint8_t*>(x + e0);
 #pragma unroll
-    for (int j = 0; j < IT::CPG; ++j) {
+    for (int j = 0; j < IT::CPG / LPG; ++j) {
       const int tc = lane + 32 * j;
       cp_async16(stage + IT::in_pos(tc / IT::CPG, tc % IT::CPG) * 16, src + 16 * tc, 16);
     }
   } else {  // tail tile: zero-fill past n_valid (the padding of collectives.py:167-172)
     const int64_t rem = jb.n_valid - e0;  // may be <= 0
 #pragma unroll 4
-    for (int j = 0; j < IT::CPG; ++j) {
+    for (int j = 0; j < IT::CPG / LPG; ++j) {
       const int tc = lane + 32 * j;
       const int64_t v = rem - (int64_t)tc * 8;
       const int valid = v <= 0 ? 0 : (v >= 8 ? 8 : (int)v);
@@ -225,31 +226,33 @@ __device__ __forceinline__ void issue_grp_tile(const EncBatch& b, int64_t t, uin
   }
 }
 
-template <int B, bool SR, int G, int WARPS>
+template <int B, bool SR, int G, int WARPS, int LPG>
 __global__ void __launch_bounds__(WARPS * 32) k_encode_grp(const __grid_constant__ EncBatch b) {
-  using IT = GTile<__nv_bfloat16, G>;
-  constexpr int PER_WARP = 2 * IT::IN_BYTES + OutStage<B, G>::BYTES;
+  using IT = GTile<__nv_bfloat16, G, LPG>;
+  constexpr int GPT = 32 / LPG;                       // groups per warp tile
+  constexpr int IN_BYTES = IT::IN_BYTES / LPG;
+  constexpr int PER_WARP = 2 * IN_BYTES + OutStage<B, G, GPT>::BYTES;
   extern __shared__ __align__(16) uint8_t smem[];
   const int warp = (int)(threadIdx.x >> 5), lane = (int)lane_id();
   uint8_t* in0 = smem + warp * PER_WARP;
-  uint8_t* ost = in0 + 2 * IT::IN_BYTES;
+  uint8_t* ost = in0 + 2 * IN_BYTES;
   const int64_t nw = (int64_t)gridDim.x * WARPS;
   int64_t t = (int64_t)blockIdx.x * WARPS + warp;
-  if (t < b.total) issue_grp_tile<G>(b, t, in0);
+  if (t < b.total) issue_grp_tile<G, LPG>(b, t, in0);
   cp_async_commit();
   int stage = 0;
   for (; t < b.total; t += nw) {
     const int64_t tn = t + nw;
-    if (tn < b.total) issue_grp_tile<G>(b, tn, in0 + (stage ^ 1) * IT::IN_BYTES);
+    if (tn < b.total) issue_grp_tile<G, LPG>(b, tn, in0 + (stage ^ 1) * IN_BYTES);
     cp_async_commit();
     cp_async_wait<1>();
     __syncwarp();
     const int ji = find_job(b, t);
     const EncJob& jb = b.j[ji];
     const int64_t ngroups = jb.n / G;
-    const int64_t tg0 = (t - jb.t0) * 32;
-    const int64_t gabs = tg0 + lane;
-    const int ng = (int)min((int64_t)32, ngroups - tg0);
+    const int64_t tg0 = (t - jb.t0) * GPT;
+    const int64_t gabs = tg0 + lane / LPG;
+    const int ng = (int)min((int64_t)GPT, ngroups - tg0);
     EncCtx cx;
     cx.n = jb.n;
     cx.meta_off = jb.n * B / 8;
@@ -257,7 +260,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_encode_grp(const __grid_constant
     cx.theta = b.theta;
     cx.lut = b.lut;
     cx.err = b.err;
-    encode_tile_bf16<B, SR, G>(in0 + stage * IT::IN_BYTES, ost, gabs < ngroups, gabs, cx, jb.out, tg0, ng);
+    encode_tile_bf16<B, SR, G, LPG>(in0 + stage * IN_BYTES, ost, gabs < ngroups, gabs, cx, jb.out, tg0, ng);
     stage ^= 1;
   }
   cp_async_wait<0>();
@@ -265,10 +268,11 @@ __global__ void __launch_bounds__(WARPS * 32) k_encode_grp(const __grid_constant
 
 template <int B, bool SR, int G>
 struct EncGrp {
-  static constexpr int WARPS = G <= 128 ? 4 : 2;
-  static constexpr int SMEM = WARPS * (2 * GTile<__nv_bfloat16, G>::IN_BYTES + OutStage<B, G>::BYTES);
+  static constexpr int LPG = G >= 256 ? G / 128 : 1;  // lanes per group (128 elements per lane at g = 256)
+  static constexpr int WARPS = 4;
+  static constexpr int SMEM = WARPS * (2 * GTile<__nv_bfloat16, G>::IN_BYTES / LPG + OutStage<B, G, 32 / LPG>::BYTES);
   static int go(const EncBatch& b, cudaStream_t st) {
-    auto kern = k_encode_grp<B, SR, G, WARPS>;
+    auto kern = k_encode_grp<B, SR, G, WARPS, LPG>;
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
@@ -838,8 +842,9 @@ template <int B, bool SR, int G, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32) k_reduce_grp(const __grid_constant__ ReduceArgs a) {
   using IT = GTile<float, G>;
   constexpr int RUNS = G / 32;
-  constexpr int PER_WARP = IT::IN_BYTES + OutStage<B, G>::BYTES;
-  constexpr int BATCH = B <= 4 ? kRedMaxSrc : kRedMaxSrc / 2;  // sources whose codes are in flight together
+  constexpr int REC_BYTES = 32 * 3 * kRedMaxSrc * 4;  // per-lane metadata records of all sources
+  constexpr int PER_WARP = IT::IN_BYTES + OutStage<B, G>::BYTES + REC_BYTES;
+  constexpr int BATCH = 4;  // sources whose codes are in flight together
   extern __shared__ __align__(16) uint8_t rsm[];
   const int warp = (int)(threadIdx.x >> 5), lane = (int)lane_id();
   uint8_t* tile = rsm + warp * PER_WARP;
@@ -855,19 +860,24 @@ __global__ void __launch_bounds__(WARPS * 32) k_reduce_grp(const __grid_constant
     const bool active = g < ngroups;
     const int64_t gc = active ? g : 0;
     const int ng = (int)min((int64_t)32, ngroups - tg0);
-    // raw metadata records of every source for this group
-    uint32_t rec[kRedMaxSrc][3];
+    // raw metadata records of every source for this group (smem, so the
+    // source loop can stay rolled without local-memory arrays)
+    uint32_t* recs = reinterpret_cast<uint32_t*>(ost + OutStage<B, G>::BYTES) + lane * (3 * kRedMaxSrc);
 #pragma unroll
     for (int s = 0; s < kRedMaxSrc; ++s)
-      if (s < a.nsrc) load_record(a.src[s] + meta_off + gc * rb, rec[s], rb);
+      if (s < a.nsrc) {
+        uint32_t rr[3];
+        load_record(a.src[s] + meta_off + gc * rb, rr, rb);
+        recs[3 * s] = rr[0]; recs[3 * s + 1] = rr[1]; recs[3 * s + 2] = rr[2];
+      }
 #pragma unroll 1
     for (int r = 0; r < RUNS; ++r) {
       const int64_t er = gc * G + 32 * r;
       float acc[32];
 #pragma unroll
       for (int k = 0; k < 32; ++k) acc[k] = 0.0f;  // acc = zeros(float32) (collectives.py:293)
-#pragma unroll
-      for (int s0 = 0; s0 < kRedMaxSrc; s0 += BATCH) {
+#pragma unroll 1
+      for (int s0 = 0; s0 < a.nsrc; s0 += BATCH) {
         uint32_t cw[BATCH][B];
 #pragma unroll
         for (int i = 0; i < BATCH; ++i)
@@ -876,17 +886,18 @@ __global__ void __launch_bounds__(WARPS * 32) k_reduce_grp(const __grid_constant
         for (int i = 0; i < BATCH; ++i) {
           const int s = s0 + i;
           if (s >= a.nsrc) break;
+          const uint32_t rec0 = recs[3 * s], rec1 = recs[3 * s + 1], rec2 = recs[3 * s + 2];
           // metadata of source s (R10 layouts)
           float s32 = 0.f, z32 = 0.f, smin = 0.f, smax = 0.f;
           double s64 = 0.0, o64 = 0.0;
           int imin = -1, imax = -1;
           if (!a.intlog) {
-            s32 = bf16_val(rec[s][0] & 0xFFFFu);
-            z32 = bf16_val(rec[s][0] >> 16);
+            s32 = bf16_val(rec0 & 0xFFFFu);
+            z32 = bf16_val(rec0 >> 16);
             if constexpr (SR) {
-              smin = bf16_val(rec[s][1] & 0xFFFFu);
-              smax = bf16_val(rec[s][1] >> 16);
-              const float fi = bf16_val(rec[s][2] & 0xFFFFu), fa = bf16_val(rec[s][2] >> 16);
+              smin = bf16_val(rec1 & 0xFFFFu);
+              smax = bf16_val(rec1 >> 16);
+              const float fi = bf16_val(rec2 & 0xFFFFu), fa = bf16_val(rec2 >> 16);
               if ((fi > -1.0f) && (fi < (float)G) && (fa > -1.0f) && (fa < (float)G)) {
                 imin = (int)fi; imax = (int)fa;
               } else if (active && r == 0) {
@@ -894,13 +905,13 @@ __global__ void __launch_bounds__(WARPS * 32) k_reduce_grp(const __grid_constant
               }
             }
           } else {
-            const int si = (int)(int8_t)(rec[s][0] & 0xFFu), zi = (int)(int8_t)((rec[s][0] >> 8) & 0xFFu);
+            const int si = (int)(int8_t)(rec0 & 0xFFu), zi = (int)(int8_t)((rec0 >> 8) & 0xFFu);
             s64 = si == -128 ? 0.0 : a.lut[si + 128];
             o64 = __dmul_rn(-(double)zi, s64);
             if constexpr (SR) {
-              smin = bf16_val(rec[s][0] >> 16);
-              smax = bf16_val(rec[s][1] & 0xFFFFu);
-              const int ii = (int)((rec[s][1] >> 16) & 0xFFu), ia = (int)(rec[s][1] >> 24);
+              smin = bf16_val(rec0 >> 16);
+              smax = bf16_val(rec1 & 0xFFFFu);
+              const int ii = (int)((rec1 >> 16) & 0xFFu), ia = (int)(rec1 >> 24);
               if (ii < G && ia < G) { imin = ii; imax = ia; }
               else if (active && r == 0) atomicOr(a.err, FC2_ERR_SPIKE_INDEX);
             }
@@ -954,7 +965,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_reduce_grp(const __grid_constant
 template <int B, bool SR, int G>
 struct RedGrp {
   static constexpr int WARPS = G <= 128 ? 4 : 2;
-  static constexpr int SMEM = WARPS * (GTile<float, G>::IN_BYTES + OutStage<B, G>::BYTES);
+  static constexpr int SMEM = WARPS * (GTile<float, G>::IN_BYTES + OutStage<B, G>::BYTES + 32 * 3 * kRedMaxSrc * 4);
   static int go(const ReduceArgs& a0, cudaStream_t st) {
     ReduceArgs a = a0;
     a.total = (a.n / G + 31) / 32;
