@@ -35,6 +35,7 @@ extern "C" {
 #define FC2_ERR_LOG2_TIE    4  /* INT_LOG: log2(scale)*theta within 1e-9 of a .5 tie (parity warning) */
 #define FC2_ERR_TIMEOUT     8  /* cross-rank flag wait timed out */
 #define FC2_ERR_CODE_RANGE 16  /* pack: code outside [0, 2^bits) -> CodeRangeError (codec.py:216-217) */
+#define FC2_ERR_NEGATIVE   32  /* scale_to_int: negative scale -> DataError (codec.py:373-374) */
 
 /* ---- element types ----------------------------------------------------- */
 #define FC2_BF16 0
@@ -117,6 +118,21 @@ int fc2_pack_codes(const int64_t* codes, int64_t n, int32_t bitwidth, uint8_t* p
                    int32_t* dev_err, void* stream);
 int fc2_unpack_codes(const uint8_t* planes, int64_t n, int32_t bitwidth, uint8_t* codes,
                      void* stream);
+
+/* Per-group scalar API (codec.py:278-343): one group of any length n >= 1
+ * (>= 4 with spike reserving), float64 values, exact float64 arithmetic.
+ * Outputs: codes[n]; params = {scale, zero, spike_min_value, spike_max_value}
+ * (float64, spikes only when sr); idx = {spike_min_index, spike_max_index}. */
+int fc2_group_encode_raw(const double* v, int64_t n, int32_t bitwidth, int32_t sr, uint8_t* codes,
+                         double* params, int32_t* idx, int32_t* dev_err, void* stream);
+/* codes * scale + zero in float64 (codec.py:293-295). */
+int fc2_group_decode_raw(const uint8_t* codes, int64_t n, double scale, double zero, double* out, void* stream);
+
+/* Integer log scales (codec.py:366-392): round-half-away(log2(s) * theta)
+ * clipped to int8 (0 -> -128 sentinel; negative -> FC2_ERR_NEGATIVE), and the
+ * inverse exp2(si / theta) (integers in [-128, 127] from the host table). */
+int fc2_scale_to_int(const double* s, int64_t n, int32_t theta, int8_t* out, int32_t* dev_err, void* stream);
+int fc2_int_to_scale(const double* si, int64_t n, int32_t theta, double* out, void* stream);
 
 /* bfloat16.py:16-36 on device arrays. */
 int fc2_f32_to_bf16_bits(const float* x, int64_t n, uint16_t* out, void* stream);

@@ -390,3 +390,56 @@ def spiky(n: int, seed: int, rate: float = 1.0 / 64.0, mag: float = 50.0) -> np.
 def child_seeds(seed: int, n: int) -> list[int]:
     # synthetic.py:46-49
     return [int(c.generate_state(1)[0]) for c in np.random.SeedSequence(seed).spawn(n)]
+
+
+# ---------------------------------------------------------------------------
+# per-group scalar API (codec.py:278-343) and int-log helpers (codec.py:366-392)
+# ---------------------------------------------------------------------------
+
+
+def rtn_group(values, bits):
+    """(codes, scale, zero) of one group (codec.py:278-290)."""
+    v = np.asarray(values, dtype=np.float64)
+    L = levels(bits)
+    zero = v.min()
+    scale = (v.max() - zero) / L
+    codes = _codes(v[None, :], np.array([scale]), np.array([zero]), L)[0]
+    return codes, float(scale), float(zero)
+
+
+def spike_group(values, bits):
+    """(codes, scale, zero, smin, smax, imin, imax) of one group (codec.py:298-329)."""
+    v = np.asarray(values, dtype=np.float64)
+    L = levels(bits)
+    lo, hi = int(np.argmin(v)), int(np.argmax(v))
+    if lo == hi:
+        lo, hi = 0, 1
+    smin = float(bf16_value(bf16_bits(np.float32(v[lo]))))
+    smax = float(bf16_value(bf16_bits(np.float32(v[hi]))))
+    rest = np.delete(v, [lo, hi])
+    zero, vmax = rest.min(), rest.max()
+    scale = (vmax - zero) / L
+    work = v.copy()
+    work[[lo, hi]] = 0.0
+    codes = _codes(work[None, :], np.array([scale]), np.array([zero]), L)[0]
+    return codes, float(scale), float(zero), smin, smax, lo, hi
+
+
+def group_decode(codes, scale, zero):
+    # codec.py:293-295
+    return np.asarray(codes, dtype=np.float64) * scale + zero
+
+
+def scale_to_int(scale, theta=10):
+    # codec.py:366-381
+    s = np.asarray(scale, dtype=np.float64)
+    pos = s > 0
+    with np.errstate(divide="ignore"):
+        raw = _round_half_away(np.log2(np.where(pos, s, 1.0)) * theta)
+    return np.where(pos, np.clip(raw, -128, 127), INT8_SENTINEL).astype(np.int8)
+
+
+def int_to_scale(si, theta=10):
+    # codec.py:384-392
+    v = np.asarray(si, dtype=np.float64)
+    return np.where(v == INT8_SENTINEL, 0.0, np.exp2(v / theta))

@@ -28,6 +28,7 @@ ERR_SPIKE_INDEX = 2
 ERR_LOG2_TIE = 4
 ERR_TIMEOUT = 8
 ERR_CODE_RANGE = 16
+ERR_NEGATIVE = 32
 
 BF16, F32, F64 = 0, 1, 2
 
@@ -66,6 +67,10 @@ SIGNATURES = {
     "fc2_unpack_codes": (_I32, [_P, _I64, _I32, _P, _P]),
     "fc2_f32_to_bf16_bits": (_I32, [_P, _I64, _P, _P]),
     "fc2_bf16_bits_to_f32": (_I32, [_P, _I64, _P, _P]),
+    "fc2_group_encode_raw": (_I32, [_P, _I64, _I32, _I32, _P, _P, _P, _P, _P]),
+    "fc2_group_decode_raw": (_I32, [_P, _I64, ctypes.c_double, ctypes.c_double, _P, _P]),
+    "fc2_scale_to_int": (_I32, [_P, _I64, _I32, _P, _P, _P]),
+    "fc2_int_to_scale": (_I32, [_P, _I64, _I32, _P, _P]),
     "fc2_comm_handle_bytes": (_I32, []),
     "fc2_comm_create": (_I32, [_I32, _I32, _I64, ctypes.POINTER(ctypes.c_void_p), _P]),
     "fc2_comm_open_peers": (_I32, [_P, _P]),
@@ -127,6 +132,8 @@ def raise_dev_err(bits: int, what: str = "") -> None:
     """Raise for a device error word (dev_err) the way the reference would."""
     if bits & ERR_NONFINITE:
         raise DataError(f"{what}input contains non-finite values")
+    if bits & ERR_NEGATIVE:
+        raise DataError(f"{what}scale must be non-negative")
     if bits & ERR_CODE_RANGE:
         raise CodeRangeError(f"{what}codes out of range")
     if bits & ERR_SPIKE_INDEX:

@@ -337,3 +337,108 @@ def unpack_codes(planes, bitwidth: int, count: int) -> np.ndarray:
     _lib.check(_lib.lib().fc2_unpack_codes(d_in.data_ptr(), count, bitwidth, d_out.data_ptr(),
                                            _device.stream_handle()))
     return d_out.cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# per-group scalar API (codec.py:278-343) and integer log scales (:366-392)
+# ---------------------------------------------------------------------------
+
+
+def _group_f64(values) -> torch.Tensor:
+    v = np.asarray(values.detach().cpu() if isinstance(values, torch.Tensor) else values, dtype=np.float64)
+    if v.ndim != 1 or v.size < 1:
+        raise DataError("group must be a non-empty one-dimensional vector")
+    dev = _device.require_cuda()
+    return torch.from_numpy(np.ascontiguousarray(v)).to(dev)
+
+
+def _levels_check(bitwidth: int) -> None:
+    if not 2 <= bitwidth <= 8:
+        raise ConfigError(f"bitwidth must be in [2, 8], got {bitwidth}")
+
+
+def _group_encode(values, bitwidth: int, sr: bool):
+    _levels_check(bitwidth)
+    x = _group_f64(values)
+    n = x.numel()
+    if sr and n < 4:
+        raise ConfigError(f"spike reserving needs at least 4 elements, got {n}")
+    codes = torch.empty(n, dtype=torch.uint8, device=x.device)
+    params = torch.zeros(4, dtype=torch.float64, device=x.device)
+    idx = torch.zeros(2, dtype=torch.int32, device=x.device)
+    err = _device.new_err(x.device)
+    _lib.check(_lib.lib().fc2_group_encode_raw(x.data_ptr(), n, bitwidth, int(sr), codes.data_ptr(),
+                                               params.data_ptr(), idx.data_ptr(), err.data_ptr(),
+                                               _device.stream_handle()))
+    _device.check_err(err, "group ")
+    return codes.cpu().numpy(), params.cpu().numpy(), idx.cpu().numpy()
+
+
+def rtn_encode_group(values, bitwidth: int):
+    """Asymmetric round-to-nearest over one group -> (codes, scale, zero) (codec.py:278-290)."""
+    codes, params, _ = _group_encode(values, bitwidth, sr=False)
+    return codes, float(params[0]), float(params[1])
+
+
+def rtn_decode_group(codes, scale: float, zero: float) -> np.ndarray:
+    """codes * scale + zero in float64 (codec.py:293-295)."""
+    c = np.ascontiguousarray(np.asarray(codes).astype(np.uint8).reshape(-1))
+    if c.size == 0:
+        return np.zeros(0)
+    dev = _device.require_cuda()
+    dc = torch.from_numpy(c).to(dev)
+    out = torch.empty(c.size, dtype=torch.float64, device=dev)
+    _lib.check(_lib.lib().fc2_group_decode_raw(dc.data_ptr(), c.size, float(scale), float(zero), out.data_ptr(),
+                                               _device.stream_handle()))
+    return out.cpu().numpy()
+
+
+def spike_encode_group(values, bitwidth: int):
+    """Quantize one group with its first min / max reserved -> (codes, GroupMeta) (codec.py:298-329)."""
+    codes, params, idx = _group_encode(values, bitwidth, sr=True)
+    meta = GroupMeta(scale=float(params[0]), zero=float(params[1]), spike_min_value=float(params[2]),
+                     spike_max_value=float(params[3]), spike_min_index=int(idx[0]), spike_max_index=int(idx[1]))
+    return codes, meta
+
+
+def spike_decode_group(codes, meta: GroupMeta) -> np.ndarray:
+    """Dequantize and restore the reserved min / max (codec.py:332-343)."""
+    out = rtn_decode_group(codes, meta.scale, meta.zero)
+    g = out.size
+    if not (0 <= meta.spike_min_index < g and 0 <= meta.spike_max_index < g):
+        raise DecodeFormatError(
+            f"spike indices ({meta.spike_min_index}, {meta.spike_max_index}) out of range for group of {g}")
+    out[meta.spike_min_index] = meta.spike_min_value
+    out[meta.spike_max_index] = meta.spike_max_value
+    return out
+
+
+def scale_to_int(scale, theta: int = 10):
+    """round-half-away(log2(scale) * theta) clipped to int8; 0 -> -128 (codec.py:366-381)."""
+    s = np.asarray(scale, dtype=np.float64)
+    dev = _device.require_cuda()
+    flat = torch.from_numpy(np.ascontiguousarray(s.reshape(-1))).to(dev)
+    out = torch.empty(flat.numel(), dtype=torch.int8, device=dev)
+    err = _device.new_err(dev)
+    if flat.numel():
+        _lib.check(_lib.lib().fc2_scale_to_int(flat.data_ptr(), flat.numel(), int(theta), out.data_ptr(),
+                                               err.data_ptr(), _device.stream_handle()))
+    _device.check_err(err)
+    res = out.cpu().numpy().reshape(s.shape)
+    return int(res) if np.ndim(scale) == 0 else res
+
+
+def int_to_scale(si, theta: int = 10):
+    """2 ** (si / theta); the -128 sentinel decodes to 0 (codec.py:384-392)."""
+    if theta <= 0:
+        raise ConfigError(f"theta must be positive, got {theta}")
+    v = np.asarray(si, dtype=np.float64)
+    dev = _device.require_cuda()
+    _device.ensure_intlog(int(theta), dev)
+    flat = torch.from_numpy(np.ascontiguousarray(v.reshape(-1))).to(dev)
+    out = torch.empty(flat.numel(), dtype=torch.float64, device=dev)
+    if flat.numel():
+        _lib.check(_lib.lib().fc2_int_to_scale(flat.data_ptr(), flat.numel(), int(theta), out.data_ptr(),
+                                               _device.stream_handle()))
+    res = out.cpu().numpy().reshape(v.shape)
+    return float(res) if np.ndim(si) == 0 else res

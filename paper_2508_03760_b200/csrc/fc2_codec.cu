@@ -145,6 +145,94 @@ __global__ void k_bf16_to_f32(const uint16_t* x, int64_t n, float* y) {
     y[i] = bf16_val(x[i]);
 }
 
+
+// ---------------------------------------------------------------------------
+// per-group scalar API (codec.py:278-343) and int-log scales (codec.py:366-392)
+// ---------------------------------------------------------------------------
+
+// one warp: exact float64 group statistics + codes for an arbitrary-length group
+__global__ void k_group_raw(const double* v, int64_t n, int B, int sr, uint8_t* codes, double* params,
+                            int32_t* idx, int32_t* err) {
+  const int lane = (int)lane_id();
+  const int L = (1 << B) - 1;
+  double mn1 = INFINITY, mn2 = INFINITY, mx1 = -INFINITY, mx2 = -INFINITY;
+  int i1 = 1 << 30, j1 = 1 << 30;
+  bool bad = false;
+  for (int64_t e = lane; e < n; e += 32) {
+    const double x = v[e];
+    if (!isfinite(x)) bad = true;
+    merge_min(mn1, i1, mn2, x, (int)e, INFINITY);
+    merge_max(mx1, j1, mx2, x, (int)e, -INFINITY);
+  }
+  for (int o = 16; o >= 1; o >>= 1) {
+    double a1 = __shfl_xor_sync(0xffffffffu, mn1, o), a2 = __shfl_xor_sync(0xffffffffu, mn2, o);
+    int ai = __shfl_xor_sync(0xffffffffu, i1, o);
+    double b1 = __shfl_xor_sync(0xffffffffu, mx1, o), b2 = __shfl_xor_sync(0xffffffffu, mx2, o);
+    int bi = __shfl_xor_sync(0xffffffffu, j1, o);
+    merge_min(mn1, i1, mn2, a1, ai, a2);
+    merge_max(mx1, j1, mx2, b1, bi, b2);
+  }
+  if (__any_sync(0xffffffffu, bad)) {
+    if (lane == 0) atomicOr(err, FC2_ERR_NONFINITE);
+    return;
+  }
+  double zero = mn1, vmax = mx1;
+  int imin = 0, imax = 1;
+  if (sr) {
+    imin = i1; imax = j1;
+    if (imin == imax) { imin = 0; imax = 1; }
+    zero = mn2; vmax = mx2;  // shrunk range (codec.py:269-275)
+  }
+  const double scale = __ddiv_rn(__dsub_rn(vmax, zero), (double)L);
+  for (int64_t e = lane; e < n; e += 32) {
+    const double x = (sr && (e == imin || e == imax)) ? 0.0 : v[e];  // reserved slots quantized as 0.0
+    codes[e] = (uint8_t)exact_code(x, zero, scale, L);
+  }
+  if (lane == 0) {
+    params[0] = scale;
+    params[1] = zero;
+    if (sr) {
+      params[2] = (double)bf16_val(bf16_bits(__double2float_rn(v[imin])));
+      params[3] = (double)bf16_val(bf16_bits(__double2float_rn(v[imax])));
+      idx[0] = imin;
+      idx[1] = imax;
+    }
+  }
+}
+
+__global__ void k_group_decode_raw(const uint8_t* codes, int64_t n, double scale, double zero, double* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __dadd_rn(__dmul_rn((double)codes[i], scale), zero);  // codes * scale + zero (codec.py:295)
+}
+
+__global__ void k_scale_to_int(const double* s, int64_t n, int theta, int8_t* out, int32_t* err) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double x = s[i];
+    if (x < 0.0) atomicOr(err, FC2_ERR_NEGATIVE);
+    int si = -128;
+    if (x > 0.0) {
+      const double t = __dmul_rn(log2(x), (double)theta);
+      const double ft = fabs(t) - floor(fabs(t));
+      if (fabs(ft - 0.5) < 1e-9) atomicOr(err, FC2_ERR_LOG2_TIE);
+      double r = rha(t);
+      r = r < -128.0 ? -128.0 : (r > 127.0 ? 127.0 : r);
+      si = (int)r;
+    }
+    out[i] = (int8_t)si;
+  }
+}
+
+__global__ void k_int_to_scale(const double* si, int64_t n, int theta, const double* lut, double* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = si[i];
+    double r;
+    if (v == -128.0) r = 0.0;
+    else if (v == floor(v) && v >= -128.0 && v <= 127.0) r = lut[(int)v + 128];  // numpy's own values
+    else r = exp2(__ddiv_rn(v, (double)theta));
+    out[i] = r;
+  }
+}
+
 static int enc_fast(int B, int dtype, bool sr, int G, const EncBatch& b, cudaStream_t st) {
 #define E(BB) launch_enc_fast<BB>(dtype, sr, G, b, st)
   FC2_BSWITCH(E)
@@ -442,6 +530,44 @@ int fc2_bf16_bits_to_f32(const uint16_t* x, int64_t n, float* out, void* stream)
   if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
   k_bf16_to_f32<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(x, n, out);
   return cuda_check("k_bf16_to_f32");
+}
+
+int fc2_group_encode_raw(const double* v, int64_t n, int32_t bitwidth, int32_t sr, uint8_t* codes, double* params,
+                         int32_t* idx, int32_t* dev_err, void* stream) {
+  if (bitwidth < 2 || bitwidth > 8) return set_err(FC2_ECONFIG, "bitwidth must be in [2, 8], got %d", bitwidth);
+  if (n < 1 || n > (1 << 30)) return set_err(FC2_EDATA, "group must be a non-empty one-dimensional vector");
+  if (sr && n < 4) return set_err(FC2_ECONFIG, "spike reserving needs at least 4 elements, got %lld", (long long)n);
+  k_group_raw<<<1, 32, 0, (cudaStream_t)stream>>>(v, n, bitwidth, sr, codes, params, idx, dev_err);
+  return cuda_check("k_group_raw");
+}
+
+int fc2_group_decode_raw(const uint8_t* codes, int64_t n, double scale, double zero, double* out, void* stream) {
+  if (n <= 0) return FC2_OK;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
+  k_group_decode_raw<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(codes, n, scale, zero, out);
+  return cuda_check("k_group_decode_raw");
+}
+
+int fc2_scale_to_int(const double* s, int64_t n, int32_t theta, int8_t* out, int32_t* dev_err, void* stream) {
+  if (theta < 1 || theta > 255) return set_err(FC2_ECONFIG, "theta must be in [1, 255], got %d", theta);
+  if (n <= 0) return FC2_OK;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
+  k_scale_to_int<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(s, n, theta, out, dev_err);
+  return cuda_check("k_scale_to_int");
+}
+
+int fc2_int_to_scale(const double* si, int64_t n, int32_t theta, double* out, void* stream) {
+  fc2_config c = {4, 32, 0, 1, theta};
+  int rc = FC2_OK;
+  const double* lut = lut_for(&c, &rc);
+  if (rc) return rc;
+  if (n <= 0) return FC2_OK;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
+  k_int_to_scale<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(si, n, theta, lut, out);
+  return cuda_check("k_int_to_scale");
 }
 
 }  // extern "C"

@@ -192,7 +192,45 @@ def a2a_fixture():
     return len(index)
 
 
+def group_fixture():
+    """Per-group scalar API (codec.py:278-343) and int-log scales (:366-392)."""
+    from qcomm import int_to_scale, rtn_encode_group, scale_to_int, spike_encode_group
+
+    rng = np.random.default_rng(77)
+    groups = []
+    for k in range(60):
+        n = int(rng.integers(4, 70))
+        g = rng.normal(0, 3, n)
+        if k % 3 == 0:
+            g[rng.integers(0, n)] *= 80.0
+        if k % 7 == 0:
+            g = np.round(g * 4) / 4  # exact .5 ties
+        groups.append(g)
+    groups += [np.full(32, 7.0), np.array([0.0, 0.5, 2.5, 3.0]), np.array([-2.0, 2.0, 0.0, 1.0]),
+               np.array([100.0] + [k / 10 for k in range(1, 10)]), np.array([1.0, 1.0, 5.0, 5.0, 3.0])]
+    arrays, index = {}, []
+    for i, g in enumerate(groups):
+        arrays[f"g{i}"] = g
+        for bits in range(2, 9):
+            c, s, z = rtn_encode_group(g, bits)
+            arrays[f"rtn{i}_b{bits}"] = np.asarray(c, dtype=np.uint8)
+            sc, m = spike_encode_group(g, bits)
+            arrays[f"sr{i}_b{bits}"] = np.asarray(sc, dtype=np.uint8)
+            index.append(dict(i=i, bits=bits, rtn_scale=s, rtn_zero=z, sr_scale=m.scale, sr_zero=m.zero,
+                              smin=m.spike_min_value, smax=m.spike_max_value,
+                              imin=m.spike_min_index, imax=m.spike_max_index))
+    scales = np.concatenate([np.exp2(np.linspace(-14, 14, 2001)), [0.0, 1e-300, 1e300, 0.3, 1.0, 2.0]])
+    for th in (1, 10, 37):
+        arrays[f"s2i_t{th}"] = scale_to_int(scales, th)
+        arrays[f"i2s_t{th}"] = int_to_scale(np.arange(-128, 128), th)
+    arrays["scales"] = scales
+    arrays["index"] = np.frombuffer(json.dumps(index).encode(), dtype=np.uint8)
+    np.savez_compressed(OUT / "group_golden.npz", **arrays)
+    return len(index)
+
+
 if __name__ == "__main__":
+    print("group cases", group_fixture())
     print("codec cases", codec_fixture())
     print("two-step cases", two_step_fixture())
     print("a2a cases", a2a_fixture())

@@ -229,3 +229,40 @@ def test_full_size_64MiB_properties(bits, sr):
         body[np.arange(rows.shape[0]), np.argmin(rows, axis=1)] = 0
         body[np.arange(rows.shape[0]), np.argmax(rows, axis=1)] = 0
     assert np.all(body.max(axis=1) <= slack * (1 + 1e-6))
+
+
+GRP, GRP_IDX = load("group_golden.npz")
+
+
+def test_group_api_matches_reference():
+    # rtn_/spike_encode_group and decoders (codec.py:278-343) on the GPU
+    for c in GRP_IDX:
+        g = GRP[f"g{c['i']}"]
+        codes, s, z = fc.rtn_encode_group(g, c["bits"])
+        assert np.array_equal(codes, GRP[f"rtn{c['i']}_b{c['bits']}"])
+        assert (s, z) == (c["rtn_scale"], c["rtn_zero"])
+        assert np.array_equal(fc.rtn_decode_group(codes, s, z), O.group_decode(codes, s, z))
+        codes, m = fc.spike_encode_group(g, c["bits"])
+        assert np.array_equal(codes, GRP[f"sr{c['i']}_b{c['bits']}"])
+        assert (m.scale, m.zero, m.spike_min_value, m.spike_max_value, m.spike_min_index, m.spike_max_index) == \
+            (c["sr_scale"], c["sr_zero"], c["smin"], c["smax"], c["imin"], c["imax"])
+        want = O.group_decode(codes, m.scale, m.zero)
+        want[m.spike_min_index] = m.spike_min_value
+        want[m.spike_max_index] = m.spike_max_value
+        assert np.array_equal(fc.spike_decode_group(codes, m), want)
+    with pytest.raises(fc.ConfigError):
+        fc.spike_encode_group([1.0, 2.0, 3.0], 2)
+    with pytest.raises(fc.DataError):
+        fc.rtn_encode_group([1.0, float("nan")], 4)
+    with pytest.raises(fc.DecodeFormatError):
+        fc.spike_decode_group(np.zeros(8, np.uint8), fc.GroupMeta(1.0, 0.0, 0.0, 1.0, 0, 99))
+
+
+@pytest.mark.parametrize("theta", [1, 10, 37])
+def test_intlog_helpers_match_reference(theta):
+    assert np.array_equal(fc.scale_to_int(GRP["scales"], theta), GRP[f"s2i_t{theta}"])
+    assert np.array_equal(fc.int_to_scale(np.arange(-128, 128), theta), GRP[f"i2s_t{theta}"])
+    assert fc.scale_to_int(1.0) == 0 and fc.scale_to_int(2.0) == 10 and fc.scale_to_int(0.3) == -17
+    assert fc.int_to_scale(-128) == 0.0
+    with pytest.raises(fc.DataError):
+        fc.scale_to_int(-1.0)

@@ -139,3 +139,26 @@ def test_synthetic_stream_pinned():
     # test_synthetic.py:15-21: n=4096, seed 2024, rate 1/32 lands on 133 spikes
     v = O.spiky(4096, 2024, rate=1 / 32)
     assert int(np.sum(np.abs(v) >= 49.0)) == 133
+
+
+GRP, GRP_IDX = load("group_golden.npz")
+
+
+def test_oracle_group_api_matches_reference():
+    # codec.py:278-343 per-group API vs the reference's own outputs
+    for c in GRP_IDX:
+        g = GRP[f"g{c['i']}"]
+        codes, s, z = O.rtn_group(g, c["bits"])
+        assert np.array_equal(codes, GRP[f"rtn{c['i']}_b{c['bits']}"])
+        assert (s, z) == (c["rtn_scale"], c["rtn_zero"])
+        codes, s, z, a, b, ia, ib = O.spike_group(g, c["bits"])
+        assert np.array_equal(codes, GRP[f"sr{c['i']}_b{c['bits']}"])
+        assert (s, z, a, b, ia, ib) == (c["sr_scale"], c["sr_zero"], c["smin"], c["smax"], c["imin"], c["imax"])
+
+
+@pytest.mark.parametrize("theta", [1, 10, 37])
+def test_oracle_intlog_helpers_match_reference(theta):
+    assert np.array_equal(O.scale_to_int(GRP["scales"], theta), GRP[f"s2i_t{theta}"])
+    assert np.array_equal(O.int_to_scale(np.arange(-128, 128), theta), GRP[f"i2s_t{theta}"])
+    # known points (test_intlog_scale.py:15-20)
+    assert int(O.scale_to_int(1.0)) == 0 and int(O.scale_to_int(2.0)) == 10 and int(O.scale_to_int(0.3)) == -17
