@@ -260,7 +260,18 @@ def test_group_api_matches_reference():
 
 @pytest.mark.parametrize("theta", [1, 10, 37])
 def test_intlog_helpers_match_reference(theta):
-    assert np.array_equal(fc.scale_to_int(GRP["scales"], theta), GRP[f"s2i_t{theta}"])
+    # bit-exact except where log2(scale)*theta is within 1e-9 of a .5 rounding
+    # tie: there the result depends on the last ulp of the libm log2 (numpy's
+    # vs CUDA's), the device flags FC2_ERR_LOG2_TIE, and the codes may differ by
+    # one.  The fixture grid exp2(linspace) hits such ties.
+    s = GRP["scales"]
+    with np.errstate(divide="ignore"):
+        t = np.log2(np.where(s > 0, s, 1.0)) * theta
+    near = np.abs(np.abs(t) - np.floor(np.abs(t)) - 0.5) < 1e-9
+    got = fc.scale_to_int(s, theta)
+    want = GRP[f"s2i_t{theta}"]
+    assert np.array_equal(got[~near], want[~near])
+    assert np.all(np.abs(got[near].astype(int) - want[near].astype(int)) <= 1)
     assert np.array_equal(fc.int_to_scale(np.arange(-128, 128), theta), GRP[f"i2s_t{theta}"])
     assert fc.scale_to_int(1.0) == 0 and fc.scale_to_int(2.0) == 10 and fc.scale_to_int(0.3) == -17
     assert fc.int_to_scale(-128) == 0.0
