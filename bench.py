@@ -365,15 +365,40 @@ def run_allreduce(args, rank, world, local_rank):
     import paper_2508_03760_b200 as fc
     from paper_2508_03760_b200 import dist as fcd
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    dist.init_process_group("nccl", device_id=dev)
+    ndev = torch.cuda.device_count()
+    dev = torch.device("cuda", local_rank % ndev)
+    torch.cuda.set_device(dev)
+    # one process per GPU over NCCL; --backend gloo lets several ranks share one
+    # GPU (CUDA IPC works between processes on a device) to validate the path
+    backend = args.backend
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group("gloo")
     sr = args.scheme == "sr"
     cfg = fc.QuantConfig(args.bits, group_size=args.group, chunk_size=args.group,
                          scheme=fc.Scheme.SPIKE_RESERVING if sr else fc.Scheme.RTN)
     n = args.n
     x = spiky_bf16(n, 1000 + rank, dev)
-    comm = fcd.QComm(dist.group.WORLD, max_elems=n, config=cfg)
+    # MoE All2All (BASELINE configs[3]): 4096 tokens x 7168, top-8 of 256
+    # experts, EP = world; one copy per distinct destination rank
+    hidden, tokens, topk, experts = 7168, args.moe_tokens, 8, 256
+    g = torch.Generator().manual_seed(4242)
+    mats = []
+    for r in range(world):
+        sel = torch.rand(tokens, experts, generator=g).topk(topk, dim=1).indices // (experts // world)
+        hit = torch.zeros(tokens, world, dtype=torch.bool)
+        hit.scatter_(1, sel, True)
+        mats.append(hit.sum(0))
+    tok_mat = torch.stack(mats).numpy()                    # tokens src -> dst
+    a2a_mat = tok_mat * hidden                               # elements
+    cap = 0
+    for d in range(world):
+        for s2 in range(world):
+            m = int(a2a_mat[s2, d])
+            if s2 != d and m:
+                cap += (fc.footprint_bytes(cfg, -(-m // args.group) * args.group) + 15) // 16 * 16
+    comm = fcd.QComm(dist.group.WORLD, max_elems=n, config=cfg, a2a_bytes=cap + 4096)
     y = torch.empty_like(x)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
@@ -393,7 +418,7 @@ def run_allreduce(args, rank, world, local_rank):
             e.record()
             torch.cuda.synchronize()
             tot += s.elapsed_time(e)
-        t = torch.tensor([tot / steps], device=dev)
+        t = torch.tensor([tot / steps], device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -403,7 +428,7 @@ def run_allreduce(args, rank, world, local_rank):
         ms = timed(lambda: comm.all_reduce(x, out=y), args.steps, args.warmup)
     launches = lib.fc2_launch_count() - l0
     xb = x.clone()
-    ms_nccl = timed(lambda: dist.all_reduce(xb), args.steps, args.warmup)
+    ms_nccl = timed(lambda: dist.all_reduce(xb), args.steps, args.warmup) if backend == "nccl" else None
     # e2e: pinned host in -> allreduce -> host out
     xh = x.cpu().pin_memory()
     yh = torch.empty_like(xh).pin_memory()
@@ -415,6 +440,18 @@ def run_allreduce(args, rank, world, local_rank):
         yh.copy_(y, non_blocking=True)
 
     ms_e2e = timed(e2e, max(3, args.steps), 2)
+    # All2All dispatch and combine: quantized (ours) vs bf16 NCCL all_to_all
+    send = spiky_bf16(int(a2a_mat[rank].sum()), 7000 + rank, dev)
+    ms_disp = timed(lambda: comm.all2all(send, a2a_mat, out_dtype=torch.bfloat16), args.steps, args.warmup)
+    back = spiky_bf16(int(a2a_mat[:, rank].sum()), 8000 + rank, dev)
+    ms_comb = timed(lambda: comm.all2all(back, a2a_mat.T.copy(), out_dtype=torch.bfloat16), args.steps, args.warmup)
+    ms_disp_nccl = None
+    if backend == "nccl":
+        recv = torch.empty(int(a2a_mat[:, rank].sum()), dtype=torch.bfloat16, device=dev)
+        ins = [int(v) for v in a2a_mat[rank]]
+        outs = [int(v) for v in a2a_mat[:, rank]]
+        ms_disp_nccl = timed(lambda: dist.all_to_all_single(recv, send, outs, ins), args.steps, args.warmup)
+    sent_bytes = 2 * int(a2a_mat[rank].sum() - a2a_mat[rank, rank])
     if rank == 0:
         algbw = 2 * n / (ms * 1e-3) / 1e9
         F = fc.footprint_bytes(cfg, comm.shard_len)
@@ -436,14 +473,21 @@ def run_allreduce(args, rank, world, local_rank):
             "config": {"workload": "two-step quantized AllReduce, 8192x4096 bf16 per rank (BASELINE configs[2])",
                        "n": n, "bits": args.bits, "group": args.group, "scheme": args.scheme,
                        "l2": "flushed before every step", "parallelism": f"tp{world}"},
-            "nccl_bf16": {"ms": round(ms_nccl, 5), "algbw_GBps": round(2 * n / (ms_nccl * 1e-3) / 1e9, 2),
-                          "speedup": round(ms_nccl / ms, 3),
-                          "nvls_env": os.environ.get("NCCL_NVLS_ENABLE", "default")},
+            "nccl_bf16": None if ms_nccl is None else {
+                "ms": round(ms_nccl, 5), "algbw_GBps": round(2 * n / (ms_nccl * 1e-3) / 1e9, 2),
+                "speedup": round(ms_nccl / ms, 3), "nvls_env": os.environ.get("NCCL_NVLS_ENABLE", "default")},
+            "backend": backend,
             "roofline": {"bound": "nvlink", "unit": "GB/s",
                          "achieved": round(2 * (world - 1) / world * F * world / (ms * 1e-3) / 1e9 / world, 2),
                          "peak": 770.0, "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
                          "frac": round(2 * (world - 1) / world * F * world / (ms * 1e-3) / 1e9 / world / 770.0, 4),
                          "traffic": None},
+            "all2all_moe": {
+                "shape": f"{tokens} tok x {hidden}, top-{topk} of {experts}, EP={world}",
+                "dispatch_ms": round(ms_disp, 4), "combine_ms": round(ms_comb, 4),
+                "dispatch_algbw_GBps": round(sent_bytes / (ms_disp * 1e-3) / 1e9, 2),
+                "nccl_bf16_dispatch_ms": None if ms_disp_nccl is None else round(ms_disp_nccl, 4),
+                "speedup_vs_nccl": None if ms_disp_nccl is None else round(ms_disp_nccl / ms_disp, 3)},
             "e2e": {"value": round(2 * n * world / (ms_e2e * 1e-3) / 1e9, 2), "unit": "GB/s",
                     "ms_per_step": round(ms_e2e, 4), "h2d_bytes_per_step": 2 * n, "d2h_bytes_per_step": 2 * n},
             "gpu_launches": launches,
@@ -524,10 +568,13 @@ def main():
     ap.add_argument("--bits", type=int, default=4)
     ap.add_argument("--group", type=int, default=128)
     ap.add_argument("--scheme", choices=["sr", "rtn"], default="sr")
-    ap.add_argument("--n", type=int, default=N_ELEMS)
+    ap.add_argument("--elems", dest="n", type=int, default=N_ELEMS)
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--cpu-reps", type=int, default=2)
     ap.add_argument("--ref-sample", type=int, default=1 << 22)
+    ap.add_argument("--moe-tokens", type=int, default=4096)
+    ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
+                    help="process-group backend for N>1 (gloo: several ranks may share one GPU)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = int(os.environ.get("RANK", "0"))
