@@ -962,6 +962,164 @@ __global__ void __launch_bounds__(WARPS * 32) k_reduce_grp(const __grid_constant
   }
 }
 
+
+template <int B, bool SR, int G>
+__global__ void __launch_bounds__(G) k_reduce_cta(const __grid_constant__ ReduceArgs a) {
+  constexpr int LPG = G / 32;   // lanes per group in the encode phase (= warps per CTA)
+  constexpr int GPW = 32 / LPG; // groups per warp in the encode phase
+  constexpr int BATCH = 4;      // sources whose codes are in flight together
+  extern __shared__ __align__(16) uint8_t csm[];
+  uint8_t* tile = csm;
+  uint8_t* ost = csm + RTile<G>::BYTES;
+  const int w = (int)(threadIdx.x >> 5), lane = (int)lane_id();
+  const int64_t ngroups = a.n / G;
+  const int rb = rec_bytes(SR, a.intlog != 0);
+  const int64_t meta_off = a.n * B / 8;
+  EncCtx cx;
+  cx.n = a.n; cx.meta_off = meta_off; cx.intlog = a.intlog; cx.theta = a.theta; cx.lut = a.lut; cx.err = a.err;
+  for (int64_t t = blockIdx.x; t < a.total; t += gridDim.x) {
+    const int64_t tg0 = t * 32;
+    const int ng = (int)min((int64_t)32, ngroups - tg0);
+    // ---- accumulation: warp w = run w, lane = group
+    {
+      const int64_t g = tg0 + lane;
+      const bool act = g < ngroups;
+      const int64_t gc = act ? g : tg0;
+      const int64_t er = gc * G + 32 * w;
+      float acc[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) acc[k] = 0.0f;  // acc = zeros(float32) (collectives.py:293)
+#pragma unroll 1
+      for (int s0 = 0; s0 < a.nsrc; s0 += BATCH) {
+        uint32_t cw[BATCH][B];
+        uint32_t rec[BATCH][3];
+#pragma unroll
+        for (int i = 0; i < BATCH; ++i)
+          if (s0 + i < a.nsrc) {
+            load_run_words<B>(a.src[s0 + i], a.n, er, cw[i]);
+            load_record(a.src[s0 + i] + meta_off + gc * rb, rec[i], rb);
+          }
+#pragma unroll
+        for (int i = 0; i < BATCH; ++i) {
+          if (s0 + i >= a.nsrc) break;
+          float s32 = 0.f, z32 = 0.f, smin = 0.f, smax = 0.f;
+          double s64 = 0.0, o64 = 0.0;
+          int imin = -1, imax = -1;
+          if (!a.intlog) {
+            s32 = bf16_val(rec[i][0] & 0xFFFFu);
+            z32 = bf16_val(rec[i][0] >> 16);
+            if constexpr (SR) {
+              smin = bf16_val(rec[i][1] & 0xFFFFu);
+              smax = bf16_val(rec[i][1] >> 16);
+              const float fi = bf16_val(rec[i][2] & 0xFFFFu), fa = bf16_val(rec[i][2] >> 16);
+              if ((fi > -1.0f) && (fi < (float)G) && (fa > -1.0f) && (fa < (float)G)) {
+                imin = (int)fi; imax = (int)fa;
+              } else if (act && w == 0) {
+                atomicOr(a.err, FC2_ERR_SPIKE_INDEX);
+              }
+            }
+          } else {
+            const int si = (int)(int8_t)(rec[i][0] & 0xFFu), zi = (int)(int8_t)((rec[i][0] >> 8) & 0xFFu);
+            s64 = si == -128 ? 0.0 : a.lut[si + 128];
+            o64 = __dmul_rn(-(double)zi, s64);
+            if constexpr (SR) {
+              smin = bf16_val(rec[i][0] >> 16);
+              smax = bf16_val(rec[i][1] & 0xFFFFu);
+              const int ii = (int)((rec[i][1] >> 16) & 0xFFu), ia = (int)(rec[i][1] >> 24);
+              if (ii < G && ia < G) { imin = ii; imax = ia; }
+              else if (act && w == 0) atomicOr(a.err, FC2_ERR_SPIKE_INDEX);
+            }
+          }
+          uint32_t cf[32];
+          run_code_floats<B>(cw[i], cf);
+          float d[32];
+          if (!a.intlog) {
+#pragma unroll
+            for (int k = 0; k < 32; k += 2) {
+              float c0, c1;
+              add2(c0, c1, __uint_as_float(cf[k]), __uint_as_float(cf[k + 1]), -8388608.0f, -8388608.0f);
+              fma2(d[k], d[k + 1], c0, c1, s32, s32, z32, z32);
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < 32; ++k)
+              d[k] = __double2float_rn(__dadd_rn(__dmul_rn((double)(cf[k] & 0xFFu), s64), o64));
+          }
+          if constexpr (SR) {  // reserved values (imin then imax) through the lane's tile region
+            const int ka = imin - 32 * w, kz = imax - 32 * w;
+            const bool ha = ka >= 0 && ka < 32, hz = kz >= 0 && kz < 32;
+            if (__any_sync(0xffffffffu, ha || hz)) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                *reinterpret_cast<float4*>(tile + RTile<G>::pos(lane, 8 * w + j) * 16) =
+                    make_float4(d[4 * j], d[4 * j + 1], d[4 * j + 2], d[4 * j + 3]);
+              if (ha) *reinterpret_cast<float*>(tile + RTile<G>::pos(lane, 8 * w + (ka >> 2)) * 16 + (ka & 3) * 4) = smin;
+              if (hz) *reinterpret_cast<float*>(tile + RTile<G>::pos(lane, 8 * w + (kz >> 2)) * 16 + (kz & 3) * 4) = smax;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float4 q = *reinterpret_cast<const float4*>(tile + RTile<G>::pos(lane, 8 * w + j) * 16);
+                d[4 * j] = q.x; d[4 * j + 1] = q.y; d[4 * j + 2] = q.z; d[4 * j + 3] = q.w;
+              }
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < 32; k += 2) add2(acc[k], acc[k + 1], acc[k], acc[k + 1], d[k], d[k + 1]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        *reinterpret_cast<float4*>(tile + RTile<G>::pos(lane, 8 * w + j) * 16) =
+            make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+    }
+    __syncthreads();
+    // ---- encode: LPG lanes per group, one run per lane
+    {
+      const int gl = w * GPW + lane / LPG, li = lane % LPG;
+      const int64_t g_abs = tg0 + gl;
+      encode_run_f32<B, SR, G>(tile, ost, gl, li, g_abs < ngroups, g_abs, cx, a.dst, a.ndst);
+    }
+    __syncthreads();  // whole tile staged (runs of a group come from several warps... same warp here)
+    // ---- copy-out: warp w writes groups [w*GPW, w*GPW + GPW) to every destination
+    {
+      const int first = w * GPW;
+      const int cnt = max(0, min(GPW, ng - first));
+      for (int dd = 0; dd < a.ndst; ++dd) {
+#pragma unroll
+        for (int u = 0; u < n_units(B); ++u) {
+          const int W = unit_w(B, u), O = unit_off(B, u);
+          const uint8_t* base = ost + OutStage<B, G>::off(u);
+          uint8_t* dst = a.dst[dd] + (a.n * O) / 8 + (tg0 + first) * (G * W / 8);
+          if (W == 1) copy_out_groups<G, 1>(base, dst, first, cnt);
+          else if (W == 2) copy_out_groups<G, 2>(base, dst, first, cnt);
+          else if (W == 4) copy_out_groups<G, 4>(base, dst, first, cnt);
+          else copy_out_groups<G, 8>(base, dst, first, cnt);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int B, bool SR, int G>
+struct RedCta {
+  static constexpr int SMEM = RTile<G>::BYTES + OutStage<B, G>::BYTES;
+  static int go(const ReduceArgs& a0, cudaStream_t st) {
+    ReduceArgs a = a0;
+    a.total = (a.n / G + 31) / 32;
+    auto kern = k_reduce_cta<B, SR, G>;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+      attr = true;
+    }
+    int64_t blocks = a.total;
+    if (blocks < 1) blocks = 1;
+    if (blocks > 65535LL * 16) blocks = 65535LL * 16;
+    kern<<<(unsigned)blocks, G, SMEM, st>>>(a);
+    return cuda_check("k_reduce_cta");
+  }
+};
+
 template <int B, bool SR, int G>
 struct RedGrp {
   static constexpr int WARPS = G <= 128 ? 4 : 2;
@@ -1028,10 +1186,10 @@ struct Launchers {
       if (reinterpret_cast<uintptr_t>(a.src[s]) & 15u) grp = false;
     if (grp) {
       switch (G) {
-        case 32: return RedGrp<B, SR, 32>::go(a, st);
-        case 64: return RedGrp<B, SR, 64>::go(a, st);
-        case 128: return RedGrp<B, SR, 128>::go(a, st);
-        case 256: return RedGrp<B, SR, 256>::go(a, st);
+        case 32: return RedCta<B, SR, 32>::go(a, st);
+        case 64: return RedCta<B, SR, 64>::go(a, st);
+        case 128: return RedCta<B, SR, 128>::go(a, st);
+        case 256: return RedCta<B, SR, 256>::go(a, st);
       }
     }
     switch (G) {
