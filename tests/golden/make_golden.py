@@ -229,7 +229,42 @@ def group_fixture():
     return len(index)
 
 
+def file_fixture():
+    """FCTN -> chunk file -> FCTN through the reference CLI (cli.py:79-112)."""
+    import tempfile
+
+    from qcomm.cli import main as ref_main
+
+    rng = np.random.default_rng(99)
+    n = 3 * 4096 + 1024  # last chunk is short
+    vals = (rng.normal(0, 2, n) * rng.uniform(0.01, 50, n)).astype(np.float32)
+    vals[rng.integers(0, n, 40)] *= 60.0
+    cases = [
+        ("b5_sr_g32_bf16", ["--bitwidth", "5", "--group-size", "32", "--scheme", "sr"]),
+        ("b3_rtn_g128_bf16", ["--bitwidth", "3", "--group-size", "128", "--scheme", "rtn"]),
+        ("b4_sr_g128_intlog", ["--bitwidth", "4", "--group-size", "128", "--scheme", "sr",
+                               "--scale-encoding", "intlog"]),
+        ("b8_rtn_g64_c1024", ["--bitwidth", "8", "--group-size", "64", "--chunk-size", "1024"]),
+    ]
+    arrays, index = {"tensor": vals}, []
+    with tempfile.TemporaryDirectory() as td:
+        tin = os.path.join(td, "in.fctn")
+        qcomm.fileio.write_tensor(tin, vals)
+        arrays["tensor_file"] = np.frombuffer(Path(tin).read_bytes(), dtype=np.uint8)
+        for key, flags in cases:
+            cf, tout = os.path.join(td, key + ".fcv2"), os.path.join(td, key + ".fctn")
+            assert ref_main(["quantize", "--in", tin, "--out", cf] + flags) == 0
+            assert ref_main(["dequantize", "--in", cf, "--out", tout]) == 0
+            arrays[f"chunks_{key}"] = np.frombuffer(Path(cf).read_bytes(), dtype=np.uint8)
+            arrays[f"deq_{key}"] = np.frombuffer(Path(tout).read_bytes(), dtype=np.uint8)
+            index.append(dict(key=key, flags=flags))
+    arrays["index"] = np.frombuffer(json.dumps(index).encode(), dtype=np.uint8)
+    np.savez_compressed(OUT / "file_golden.npz", **arrays)
+    return len(index)
+
+
 if __name__ == "__main__":
+    print("file cases", file_fixture())
     print("group cases", group_fixture())
     print("codec cases", codec_fixture())
     print("two-step cases", two_step_fixture())
