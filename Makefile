@@ -1,7 +1,7 @@
 # Build the B200 (sm_100a) shared library behind the C ABI in include/fc2.h.
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr $(EXTRA)
 PKG := paper_2508_03760_b200
 SRC := $(PKG)/csrc
 OBJ := $(PKG)/_build

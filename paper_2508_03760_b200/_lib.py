@@ -14,7 +14,8 @@ import threading
 from .errors import CodeRangeError, ConfigError, DataError, DecodeFormatError, NotApplicableError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfc2.so")
+# FC2_LIB: alternate build of the same library (kernel-variant experiments)
+LIB_PATH = os.environ.get("FC2_LIB") or os.path.join(_HERE, "libfc2.so")
 
 FC2_OK = 0
 FC2_ECONFIG = -1

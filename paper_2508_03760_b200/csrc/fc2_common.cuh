@@ -142,9 +142,23 @@ struct Fix<15> {
   static constexpr uint32_t kTie = 0x7FF0u;
   static constexpr float kFold = 512.0f;
 };
+// 16-bit fraction (B <= 7): y in [128, 256), code in bits [16, 24) -- a whole
+// byte, so plane words are gathered with byte permutes; fraction = low half.
+// kFold bounds |nz| for the single-FFMA form y = fma(v, inv, nz + kCM):
+// |error| <= 2^-24 (127.5 + 128) + 2^-16 (nz + kCM rounding) + 2^-17 (fma)
+// ~ 2.5 ulp of 2^-16, inside the 8-ulp tie window.
+template <>
+struct Fix<16> {
+  static constexpr int kBits = 16;
+  static constexpr float kC = 0.5f + 8.0f / 65536.0f;
+  static constexpr float kM = 128.0f;
+  static constexpr float kCM = 128.5f + 8.0f / 65536.0f;
+  static constexpr uint32_t kTie = 0xFFF0u;
+  static constexpr float kFold = 128.0f;
+};
 template <int B>
 struct FixFor {
-  static constexpr int FB = 15;
+  static constexpr int FB = B <= 7 ? 16 : 15;
 };
 
 template <int FB>
@@ -157,11 +171,20 @@ __device__ __forceinline__ uint32_t fixq_clamped(float v, float off32, float inv
 
 // tie mask bits for a pair of fixed-point words: bit `pp` for X0 and bit
 // `16 + pp` for X1 when the fraction is within 8 ulps of a rounding tie
+// (FB = 16: the masked fraction can be 0x8000 == -0.0 as f16, so it is
+// XOR-ed onto 1.0 first: equal to 1.0 exactly when the masked bits are zero)
 template <int FB>
 __device__ __forceinline__ uint32_t pair_tie_bits(uint32_t X0, uint32_t X1, int pp) {
-  uint32_t fr = __byte_perm(X0, X1, 0x5410) & (Fix<FB>::kTie | (Fix<FB>::kTie << 16));
-  __half2 h = *reinterpret_cast<const __half2*>(&fr);
-  return __heq2_mask(h, __float2half2_rn(0.0f)) & (0x00010001u << pp);
+  constexpr uint32_t M = Fix<FB>::kTie | (Fix<FB>::kTie << 16);
+  if constexpr (FB == 16) {
+    uint32_t fr = (__byte_perm(X0, X1, 0x5410) & M) ^ 0x3C003C00u;
+    __half2 h = *reinterpret_cast<const __half2*>(&fr);
+    return __heq2_mask(h, __float2half2_rn(1.0f)) & (0x00010001u << pp);
+  } else {
+    uint32_t fr = __byte_perm(X0, X1, 0x5410) & M;
+    __half2 h = *reinterpret_cast<const __half2*>(&fr);
+    return __heq2_mask(h, __float2half2_rn(0.0f)) & (0x00010001u << pp);
+  }
 }
 
 // packed float32x2 arithmetic (sm_100: FFMA2 / FADD2)

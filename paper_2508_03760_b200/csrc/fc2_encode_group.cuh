@@ -177,11 +177,48 @@ __device__ __forceinline__ void top_final(const TopState& s, float& mn1, float& 
   }
 }
 
+// Pack the 32 codes of a run into plane words (LaneWords layout: unit-major,
+// word t of a W-bit unit holds codes [32t/W, 32(t+1)/W) LSB-first).  FB = 16
+// puts each code in byte 2 of its fixed-point word, so four codes are
+// gathered into one word with three byte permutes; slice s of a word holds
+// codes k0 + s, k0 + s + S, ... (S = 8 / W) and is merged with one shift-or.
+// MASK: codes may be out of range (unclamped spike slots, patched later).
+template <int B, bool MASK>
+__device__ __forceinline__ void pack_run_fb16(const uint32_t (&X)[32], uint32_t (&w)[B]) {
+#pragma unroll
+  for (int u = 0; u < n_units(B); ++u) {
+    const int W = unit_w(B, u), O = unit_off(B, u);
+    const int S = 8 / W;
+    const uint32_t mrep = ((1u << W) - 1u) * 0x01010101u;
+#pragma unroll
+    for (int t = 0; t < W; ++t) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int sl = 0; sl < S; ++sl) {
+        const int k0 = t * (32 / W) + sl;
+        const uint32_t lo = __byte_perm(X[k0], X[k0 + S], 0x0062);
+        const uint32_t hi = __byte_perm(X[k0 + 2 * S], X[k0 + 3 * S], 0x0062);
+        const uint32_t A = __byte_perm(lo, hi, 0x5410);  // codes as bytes
+        uint32_t v;
+        if (W == B && !MASK) {
+          v = A << (W * sl);
+        } else {
+          const int sh = W * sl - O;
+          v = sh >= 0 ? ((A & (mrep << O)) << sh) : ((A >> (-sh)) & (mrep << (W * sl)));
+        }
+        word |= v;
+      }
+      w[LaneWords<B>::base(u) + t] = word;
+    }
+  }
+}
+
 // pass 3 for all runs of the lane's group with the code form fixed at compile
 // time (MODE 0: folded fma, 1: explicit v - off, 2: INT_LOG clamped).
-// Writes packed words into the output stage, returns per-run tie masks in
-// split layout (bit i < 16: element 2i; bit 16 + i: element 2i + 1).
-template <int B, int G, int MODE, int LPG>
+// Writes packed words into the output stage; near-tie elements (split-layout
+// tie masks: bit i < 16 element 2i, bit 16 + i element 2i + 1) are recomputed
+// exactly and patched in the stage.
+template <int B, bool SR, int G, int MODE, int LPG>
 __device__ __forceinline__ void quant_runs(const uint8_t* ist, uint8_t* ost, const GroupParams& p, float Lh,
                                            bool active) {
   using IT = GTile<__nv_bfloat16, G, LPG>;
@@ -191,12 +228,15 @@ __device__ __forceinline__ void quant_runs(const uint8_t* ist, uint8_t* ost, con
   constexpr int FB = FixFor<B>::FB;
   using FX = Fix<FB>;
   constexpr int L = (1 << B) - 1;
+  // FB = 16 folded form: one FFMA, y = fma(v, inv, nz + kCM) (bound: Fix<16>)
+  const float c16 = __fadd_rn(p.nz, FX::kCM);
 #pragma unroll 2
   for (int rr = 0; rr < RUNS; ++rr) {
     const int r = r0 + rr;  // run index inside the group
     LaneWords<B> lw;
     lw.clear();
     uint32_t tmj[2] = {0u, 0u};  // two accumulators: shorter dependency chains
+    uint32_t XR[32];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       uint32_t& tm = tmj[j & 1];
@@ -208,9 +248,13 @@ __device__ __forceinline__ void quant_runs(const uint8_t* ist, uint8_t* ost, con
         const float a = __uint_as_float(ww[pp] << 16), b = __uint_as_float(ww[pp] & 0xFFFF0000u);
         float y0, y1;
         if constexpr (MODE == 0) {
-          float t0, t1;
-          fma2(t0, t1, a, b, p.inv32, p.inv32, p.nz, p.nz);
-          add2(y0, y1, t0, t1, FX::kCM, FX::kCM);
+          if constexpr (FB == 16) {
+            fma2(y0, y1, a, b, p.inv32, p.inv32, c16, c16);
+          } else {
+            float t0, t1;
+            fma2(t0, t1, a, b, p.inv32, p.inv32, p.nz, p.nz);
+            add2(y0, y1, t0, t1, FX::kCM, FX::kCM);
+          }
         } else if constexpr (MODE == 1) {
           float d0, d1, t0, t1;
           add2(d0, d1, a, b, -p.off32, -p.off32);
@@ -224,9 +268,15 @@ __device__ __forceinline__ void quant_runs(const uint8_t* ist, uint8_t* ost, con
         X[2 * pp + 1] = __float_as_uint(y1);
         tm |= pair_tie_bits<FB>(X[2 * pp], X[2 * pp + 1], 4 * j + pp);
       }
+      if constexpr (FB == 16) {
 #pragma unroll
-      for (int e = 0; e < 8; ++e) lw.template put_fixb<FB>(8 * j + e, X[e], 0);
+        for (int e = 0; e < 8; ++e) XR[8 * j + e] = X[e];
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) lw.template put_fixb<FB>(8 * j + e, X[e], 0);
+      }
     }
+    if constexpr (FB == 16) pack_run_fb16<B, SR && MODE != 2>(XR, lw.w);
 #pragma unroll
     for (int u = 0; u < n_units(B); ++u) {
       const int W = unit_w(B, u);
@@ -270,94 +320,117 @@ __device__ __forceinline__ void encode_tile_bf16(const uint8_t* ist, uint8_t* os
   constexpr int FB = FixFor<B>::FB;
   using FX = Fix<FB>;
 
-  // ---- pass 1: statistics; ra / rz = run where the running min / max last
-  // strictly improved == run holding the first occurrence of the extreme.
-  // Two independent accumulator sets (even / odd chunks) halve the
-  // dependency chains; they are merged per run for the running extremes.
-  TopState ts, tt;
-  int ra = r0, rz = r0;
-  {
-    const uint4 q0 = chunk(4 * r0), q1 = chunk(4 * r0 + 1);
-    top_init(ts, q0.x);
-    top_add<SR>(ts, q0.y); top_add<SR>(ts, q0.z); top_add<SR>(ts, q0.w);
-    top_init(tt, q1.x);
-    top_add<SR>(tt, q1.y); top_add<SR>(tt, q1.z); top_add<SR>(tt, q1.w);
-    const uint4 q2 = chunk(4 * r0 + 2), q3 = chunk(4 * r0 + 3);
-    top_add<SR>(ts, q2.x); top_add<SR>(ts, q2.y); top_add<SR>(ts, q2.z); top_add<SR>(ts, q2.w);
-    top_add<SR>(tt, q3.x); top_add<SR>(tt, q3.y); top_add<SR>(tt, q3.z); top_add<SR>(tt, q3.w);
-  }
-  float rmin = 0.f, rmax = 0.f;
-  if constexpr (SR) {
-    rmin = fmin_nan(fmin_nan(__low2float(ts.a1), __high2float(ts.a1)), fmin_nan(__low2float(tt.a1), __high2float(tt.a1)));
-    rmax = fmax_nan(fmax_nan(__low2float(ts.b1), __high2float(ts.b1)), fmax_nan(__low2float(tt.b1), __high2float(tt.b1)));
-  }
-#pragma unroll 1
-  for (int r = r0 + 1; r < r0 + RUNS; ++r) {
+  // ---- pass 1: packed bf16x2 min / max of every run of this lane ----------
+  __nv_bfloat162 rmn[RUNS], rmx[RUNS];
 #pragma unroll
-    for (int j = 0; j < 4; j += 2) {
-      const uint4 q = chunk(4 * r + j), p2 = chunk(4 * r + j + 1);
-      top_add<SR>(ts, q.x); top_add<SR>(tt, p2.x); top_add<SR>(ts, q.y); top_add<SR>(tt, p2.y);
-      top_add<SR>(ts, q.z); top_add<SR>(tt, p2.z); top_add<SR>(ts, q.w); top_add<SR>(tt, p2.w);
-    }
-    if constexpr (SR) {
-      const float nmin = fmin_nan(fmin_nan(__low2float(ts.a1), __high2float(ts.a1)),
-                                  fmin_nan(__low2float(tt.a1), __high2float(tt.a1)));
-      const float nmax = fmax_nan(fmax_nan(__low2float(ts.b1), __high2float(ts.b1)),
-                                  fmax_nan(__low2float(tt.b1), __high2float(tt.b1)));
-      if (nmin < rmin) ra = r;
-      if (nmax > rmax) rz = r;
-      rmin = nmin;
-      rmax = nmax;
-    }
+  for (int rr = 0; rr < RUNS; ++rr) {
+    const int r = r0 + rr;
+    const uint4 q0 = chunk(4 * r), q1 = chunk(4 * r + 1), q2 = chunk(4 * r + 2), q3 = chunk(4 * r + 3);
+    auto h = [](uint32_t w) { return *reinterpret_cast<const __nv_bfloat162*>(&w); };
+    const __nv_bfloat162 a0 = __hmin2_nan(__hmin2_nan(h(q0.x), h(q0.y)), __hmin2_nan(h(q0.z), h(q0.w)));
+    const __nv_bfloat162 a1 = __hmin2_nan(__hmin2_nan(h(q1.x), h(q1.y)), __hmin2_nan(h(q1.z), h(q1.w)));
+    const __nv_bfloat162 a2 = __hmin2_nan(__hmin2_nan(h(q2.x), h(q2.y)), __hmin2_nan(h(q2.z), h(q2.w)));
+    const __nv_bfloat162 a3 = __hmin2_nan(__hmin2_nan(h(q3.x), h(q3.y)), __hmin2_nan(h(q3.z), h(q3.w)));
+    rmn[rr] = __hmin2_nan(__hmin2_nan(a0, a1), __hmin2_nan(a2, a3));
+    const __nv_bfloat162 b0 = __hmax2_nan(__hmax2_nan(h(q0.x), h(q0.y)), __hmax2_nan(h(q0.z), h(q0.w)));
+    const __nv_bfloat162 b1 = __hmax2_nan(__hmax2_nan(h(q1.x), h(q1.y)), __hmax2_nan(h(q1.z), h(q1.w)));
+    const __nv_bfloat162 b2 = __hmax2_nan(__hmax2_nan(h(q2.x), h(q2.y)), __hmax2_nan(h(q2.z), h(q2.w)));
+    const __nv_bfloat162 b3 = __hmax2_nan(__hmax2_nan(h(q3.x), h(q3.y)), __hmax2_nan(h(q3.z), h(q3.w)));
+    rmx[rr] = __hmax2_nan(__hmax2_nan(b0, b1), __hmax2_nan(b2, b3));
   }
-  top_merge<SR>(ts, tt);
-  float mn1, mn2, mx1, mx2;
-  top_final<SR>(ts, mn1, mn2, mx1, mx2);
-  const float lmin = mn1, lmax = mx1;  // this lane's own extremes
+  __nv_bfloat162 tmn = rmn[0], tmx = rmx[0];
+#pragma unroll
+  for (int rr = 1; rr < RUNS; ++rr) {
+    tmn = __hmin2_nan(tmn, rmn[rr]);
+    tmx = __hmax2_nan(tmx, rmx[rr]);
+  }
+  float mn1 = fmin_nan(__low2float(tmn), __high2float(tmn));
+  float mx1 = fmax_nan(__low2float(tmx), __high2float(tmx));
 #pragma unroll
   for (int o = 1; o < LPG; o <<= 1) {  // merge the LPG parts of the group
-    const float a1 = __shfl_xor_sync(0xffffffffu, mn1, o), b1 = __shfl_xor_sync(0xffffffffu, mx1, o);
-    if constexpr (SR) {
-      const float a2 = __shfl_xor_sync(0xffffffffu, mn2, o), b2 = __shfl_xor_sync(0xffffffffu, mx2, o);
-      mn2 = fmin_nan(fmax_nan(mn1, a1), fmin_nan(mn2, a2));
-      mx2 = fmax_nan(fmin_nan(mx1, b1), fmax_nan(mx2, b2));
-    }
-    mn1 = fmin_nan(mn1, a1);
-    mx1 = fmax_nan(mx1, b1);
+    mn1 = fmin_nan(mn1, __shfl_xor_sync(0xffffffffu, mn1, o));
+    mx1 = fmax_nan(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
   }
-  if (!SR) { mn2 = mn1; mx2 = mx1; }
+  float mn2 = mn1, mx2 = mx1;
   const bool finite = isfinite(mn1) && isfinite(mx1);
   if (active && !finite && li == 0) atomicOr(cx.err, FC2_ERR_NONFINITE);
 
-  // ---- spikes: first argmin / argmax (codec.py:259-266) ---------------------
-  // The running minimum first equals the group minimum in the run holding its
-  // first occurrence; only that run is searched (by the lane whose part holds
-  // the group extreme), then the lowest index over the group's lanes wins.
+  // ---- spikes (codec.py:259-275): first argmin / argmax, and the extremes of
+  // the rest.  Only the first run holding the extreme is searched; it also
+  // yields that run's extreme with the extreme's occurrences removed.  With
+  // one occurrence in the group the shrunk extreme is min(other runs, that);
+  // with several it is the extreme itself.
   int imin = 0, imax = 1;
   uint32_t smin_bits = 0, smax_bits = 0;
   if constexpr (SR) {
-    auto first_in_run = [&](int r, float m) -> int {
+    // search run `r` for value m: first index, occurrences, extreme of the rest
+    auto search = [&](int r, float m, bool is_min, int& first, int& occ, float& rest) {
       const __nv_bfloat162 mm = __float2bfloat162_rn(m);
+      const uint32_t sent = is_min ? 0x7F807F80u : 0xFF80FF80u;  // +inf / -inf
       uint32_t em = 0;
+      __nv_bfloat162 acc = *reinterpret_cast<const __nv_bfloat162*>(&sent);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const uint4 q = chunk(4 * r + j);
         const uint32_t ww[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-        for (int pp = 0; pp < 4; ++pp)
-          em |= __heq2_mask(*reinterpret_cast<const __nv_bfloat162*>(&ww[pp]), mm) & (0x00010001u << (4 * j + pp));
+        for (int pp = 0; pp < 4; ++pp) {
+          const uint32_t eq = __heq2_mask(*reinterpret_cast<const __nv_bfloat162*>(&ww[pp]), mm);
+          em |= eq & (0x00010001u << (4 * j + pp));
+          const uint32_t xr = (ww[pp] & ~eq) | (sent & eq);
+          const __nv_bfloat162 x = *reinterpret_cast<const __nv_bfloat162*>(&xr);
+          acc = is_min ? __hmin2_nan(acc, x) : __hmax2_nan(acc, x);
+        }
       }
       const uint32_t lo = em & 0xFFFFu, hi = em >> 16;
       const int f = min(lo ? 2 * (__ffs(lo) - 1) : 64, hi ? 2 * (__ffs(hi) - 1) + 1 : 64);
-      return f < 32 ? 32 * r + f : 1 << 20;
+      first = f < 32 ? 32 * r + f : 1 << 20;
+      occ = __popc(em);
+      rest = is_min ? fmin_nan(__low2float(acc), __high2float(acc)) : fmax_nan(__low2float(acc), __high2float(acc));
     };
-    int fi = (lmin == mn1) ? first_in_run(ra, mn1) : 1 << 20;
-    int fa = (lmax == mx1) ? first_in_run(rz, mx1) : 1 << 20;
+    const __nv_bfloat162 mm = __float2bfloat162_rn(mn1), MM = __float2bfloat162_rn(mx1);
+    int ra = -1, rz = -1, omin = 0, omax = 0;
+#pragma unroll
+    for (int rr = RUNS - 1; rr >= 0; --rr) {  // first run holding each extreme
+      if (__heq2_mask(rmn[rr], mm)) { if (ra >= 0) omin += 1; ra = rr; }
+      if (__heq2_mask(rmx[rr], MM)) { if (rz >= 0) omax += 1; rz = rr; }
+    }
+    // runs of this lane other than ra / rz
+    float omn = __int_as_float(0x7f800000), omx = __int_as_float(0xff800000);
+#pragma unroll
+    for (int rr = 0; rr < RUNS; ++rr) {
+      const uint32_t pinf = 0x7F807F80u, ninf = 0xFF80FF80u;
+      const __nv_bfloat162 a = rr == ra ? *reinterpret_cast<const __nv_bfloat162*>(&pinf) : rmn[rr];
+      const __nv_bfloat162 z = rr == rz ? *reinterpret_cast<const __nv_bfloat162*>(&ninf) : rmx[rr];
+      omn = fmin_nan(omn, fmin_nan(__low2float(a), __high2float(a)));
+      omx = fmax_nan(omx, fmax_nan(__low2float(z), __high2float(z)));
+    }
+    int fi = 1 << 20, fa = 1 << 20;
+    if (ra >= 0) {
+      int occ;
+      float rest;
+      search(r0 + ra, mn1, true, fi, occ, rest);
+      omin += occ;
+      omn = fmin_nan(omn, rest);
+    }
+    if (rz >= 0) {
+      int occ;
+      float rest;
+      search(r0 + rz, mx1, false, fa, occ, rest);
+      omax += occ;
+      omx = fmax_nan(omx, rest);
+    }
 #pragma unroll
     for (int o = 1; o < LPG; o <<= 1) {
       fi = min(fi, __shfl_xor_sync(0xffffffffu, fi, o));
       fa = min(fa, __shfl_xor_sync(0xffffffffu, fa, o));
+      omin += __shfl_xor_sync(0xffffffffu, omin, o);
+      omax += __shfl_xor_sync(0xffffffffu, omax, o);
+      omn = fmin_nan(omn, __shfl_xor_sync(0xffffffffu, omn, o));
+      omx = fmax_nan(omx, __shfl_xor_sync(0xffffffffu, omx, o));
     }
+    mn2 = omin >= 2 ? mn1 : omn;
+    mx2 = omax >= 2 ? mx1 : omx;
     if (fi >= G) fi = 0;  // only with NaN input (already flagged)
     if (fa >= G) fa = 1;
     if (fi == fa) { fi = 0; fa = 1; }
@@ -378,11 +451,11 @@ __device__ __forceinline__ void encode_tile_bf16(const uint8_t* ist, uint8_t* os
   const bool fold_ok = !p.exact && fabsf(p.nz) <= FX::kFold;
   const float Lh = (float)L + 0.5f;
   if (cx.intlog) {
-    quant_runs<B, G, 2, LPG>(ist, ost, p, Lh, active);
+    quant_runs<B, SR, G, 2, LPG>(ist, ost, p, Lh, active);
   } else if (__all_sync(0xffffffffu, fold_ok || p.exact || !active)) {
-    quant_runs<B, G, 0, LPG>(ist, ost, p, Lh, active);
+    quant_runs<B, SR, G, 0, LPG>(ist, ost, p, Lh, active);
   } else {
-    quant_runs<B, G, 1, LPG>(ist, ost, p, Lh, active);
+    quant_runs<B, SR, G, 1, LPG>(ist, ost, p, Lh, active);
   }
   if constexpr (SR) {  // reserved slots are quantized as 0.0 (codec.py:494-496)
     int sc;

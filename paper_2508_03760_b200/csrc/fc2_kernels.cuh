@@ -226,26 +226,35 @@ __device__ __forceinline__ void issue_grp_tile(const EncBatch& b, int64_t t, uin
   }
 }
 
-template <int B, bool SR, int G, int WARPS, int LPG>
+template <int B, bool SR, int G, int WARPS, int LPG, int STAGES>
 __global__ void __launch_bounds__(WARPS * 32) k_encode_grp(const __grid_constant__ EncBatch b) {
   using IT = GTile<__nv_bfloat16, G, LPG>;
   constexpr int GPT = 32 / LPG;                       // groups per warp tile
   constexpr int IN_BYTES = IT::IN_BYTES / LPG;
-  constexpr int PER_WARP = 2 * IN_BYTES + OutStage<B, G, GPT>::BYTES;
+  constexpr int PER_WARP = STAGES * IN_BYTES + OutStage<B, G, GPT>::BYTES;
   extern __shared__ __align__(16) uint8_t smem[];
   const int warp = (int)(threadIdx.x >> 5), lane = (int)lane_id();
   uint8_t* in0 = smem + warp * PER_WARP;
-  uint8_t* ost = in0 + 2 * IN_BYTES;
+  uint8_t* ost = in0 + STAGES * IN_BYTES;
   const int64_t nw = (int64_t)gridDim.x * WARPS;
   int64_t t = (int64_t)blockIdx.x * WARPS + warp;
-  if (t < b.total) issue_grp_tile<G, LPG>(b, t, in0);
-  cp_async_commit();
+  if constexpr (STAGES == 2) {
+    if (t < b.total) issue_grp_tile<G, LPG>(b, t, in0);
+    cp_async_commit();
+  }
   int stage = 0;
   for (; t < b.total; t += nw) {
-    const int64_t tn = t + nw;
-    if (tn < b.total) issue_grp_tile<G, LPG>(b, tn, in0 + (stage ^ 1) * IN_BYTES);
-    cp_async_commit();
-    cp_async_wait<1>();
+    if constexpr (STAGES == 2) {
+      const int64_t tn = t + nw;
+      if (tn < b.total) issue_grp_tile<G, LPG>(b, tn, in0 + (stage ^ 1) * IN_BYTES);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      __syncwarp();  // previous tile fully consumed
+      issue_grp_tile<G, LPG>(b, t, in0);
+      cp_async_commit();
+      cp_async_wait<0>();
+    }
     __syncwarp();
     const int ji = find_job(b, t);
     const EncJob& jb = b.j[ji];
@@ -261,18 +270,27 @@ __global__ void __launch_bounds__(WARPS * 32) k_encode_grp(const __grid_constant
     cx.lut = b.lut;
     cx.err = b.err;
     encode_tile_bf16<B, SR, G, LPG>(in0 + stage * IN_BYTES, ost, gabs < ngroups, gabs, cx, jb.out, tg0, ng);
-    stage ^= 1;
+    if constexpr (STAGES == 2) stage ^= 1;
   }
   cp_async_wait<0>();
 }
 
+#ifndef FC2_ENC_STAGES
+#define FC2_ENC_STAGES 1
+#endif
+#ifndef FC2_ENC_WARPS
+#define FC2_ENC_WARPS 4
+#endif
+
 template <int B, bool SR, int G>
 struct EncGrp {
   static constexpr int LPG = G >= 256 ? G / 128 : 1;  // lanes per group (128 elements per lane at g = 256)
-  static constexpr int WARPS = 4;
-  static constexpr int SMEM = WARPS * (2 * GTile<__nv_bfloat16, G>::IN_BYTES / LPG + OutStage<B, G, 32 / LPG>::BYTES);
+  static constexpr int WARPS = FC2_ENC_WARPS;
+  static constexpr int STAGES = FC2_ENC_STAGES;
+  static constexpr int SMEM =
+      WARPS * (STAGES * GTile<__nv_bfloat16, G>::IN_BYTES / LPG + OutStage<B, G, 32 / LPG>::BYTES);
   static int go(const EncBatch& b, cudaStream_t st) {
-    auto kern = k_encode_grp<B, SR, G, WARPS, LPG>;
+    auto kern = k_encode_grp<B, SR, G, WARPS, LPG, STAGES>;
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
