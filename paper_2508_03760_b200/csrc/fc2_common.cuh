@@ -177,7 +177,9 @@ template <int FB>
 __device__ __forceinline__ uint32_t pair_tie_bits(uint32_t X0, uint32_t X1, int pp) {
   constexpr uint32_t M = Fix<FB>::kTie | (Fix<FB>::kTie << 16);
   if constexpr (FB == 16) {
-    uint32_t fr = (__byte_perm(X0, X1, 0x5410) & M) ^ 0x3C003C00u;
+    uint32_t one;  // 1.0 as f16x2, in a register so (x & M) ^ one is one LOP3
+    asm("mov.b32 %0, 0x3C003C00;" : "=r"(one));
+    uint32_t fr = (__byte_perm(X0, X1, 0x5410) & M) ^ one;
     __half2 h = *reinterpret_cast<const __half2*>(&fr);
     return __heq2_mask(h, __float2half2_rn(1.0f)) & (0x00010001u << pp);
   } else {

@@ -226,8 +226,11 @@ __device__ __forceinline__ void issue_grp_tile(const EncBatch& b, int64_t t, uin
   }
 }
 
+#ifndef FC2_ENC_MINB
+#define FC2_ENC_MINB 5  // 5 CTAs of 4 warps per SM: <= 102 registers (smem allows 5)
+#endif
 template <int B, bool SR, int G, int WARPS, int LPG, int STAGES>
-__global__ void __launch_bounds__(WARPS * 32) k_encode_grp(const __grid_constant__ EncBatch b) {
+__global__ void __launch_bounds__(WARPS * 32, FC2_ENC_MINB) k_encode_grp(const __grid_constant__ EncBatch b) {
   using IT = GTile<__nv_bfloat16, G, LPG>;
   constexpr int GPT = 32 / LPG;                       // groups per warp tile
   constexpr int IN_BYTES = IT::IN_BYTES / LPG;
@@ -281,6 +284,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_encode_grp(const __grid_constant
 #ifndef FC2_ENC_WARPS
 #define FC2_ENC_WARPS 4
 #endif
+#ifndef FC2_ENC_CTAS_PER_SM
+#define FC2_ENC_CTAS_PER_SM 64
+#endif
 
 template <int B, bool SR, int G>
 struct EncGrp {
@@ -297,7 +303,7 @@ struct EncGrp {
       attr = true;
     }
     int64_t blocks = (b.total + WARPS - 1) / WARPS;
-    int64_t cap = (int64_t)num_sms() * 64;
+    int64_t cap = (int64_t)num_sms() * FC2_ENC_CTAS_PER_SM;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     kern<<<(unsigned)blocks, WARPS * 32, SMEM, st>>>(b);
