@@ -365,7 +365,7 @@ int fc2_encode_batch(const fc2_config* cfg, int32_t x_dtype, int32_t njobs, cons
     j.n = n[i];
     j.t0 = b->total;
     // fast tiles: bf16 -> 32 groups per warp tile (lane per group); f32 -> 1024 elements
-    const int64_t lpg = G >= 256 ? G / 128 : 1;  // must match EncGrp::LPG
+    const int64_t lpg = enc_lpg(G);  // EncGrp::LPG
     const int64_t tile = x_dtype == FC2_BF16 ? 32 / lpg * (int64_t)G : 1024;
     b->total += use_fast ? (n[i] + tile - 1) / tile : n[i] / G;
     (void)esz;

@@ -177,6 +177,10 @@ template <int FB>
 __device__ __forceinline__ uint32_t pair_tie_bits(uint32_t X0, uint32_t X1, int pp) {
   constexpr uint32_t M = Fix<FB>::kTie | (Fix<FB>::kTie << 16);
   if constexpr (FB == 16) {
+    // (x & M) ^ 1.0: equal to 1.0 exactly when the masked fraction is zero
+    // (the raw masked fraction can be 0x8000 == -0.0, which a zero test would
+    // also accept; an |.| < tiny test would flag exact-integer q, which bf16
+    // data hits often)
     uint32_t one;  // 1.0 as f16x2, in a register so (x & M) ^ one is one LOP3
     asm("mov.b32 %0, 0x3C003C00;" : "=r"(one));
     uint32_t fr = (__byte_perm(X0, X1, 0x5410) & M) ^ one;
@@ -271,6 +275,13 @@ __device__ __forceinline__ GroupParams group_params(double zero, double vmax, in
 // ---------------------------------------------------------------------------
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+
+// lanes per group of the lane-per-group encoder: each lane owns at most
+// FC2_ENC_EPL consecutive elements of its group (host and device agree)
+#ifndef FC2_ENC_EPL
+#define FC2_ENC_EPL 128
+#endif
+__host__ __device__ constexpr int enc_lpg(int G) { return G > FC2_ENC_EPL ? G / FC2_ENC_EPL : 1; }
 
 // store nbytes (<= 12) from words[]; widest stores the alignment allows
 __device__ __forceinline__ void store_record(uint8_t* p, const uint32_t* w, int nbytes) {

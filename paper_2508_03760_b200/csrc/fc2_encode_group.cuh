@@ -111,11 +111,18 @@ __device__ __forceinline__ void stage_words(uint8_t* base, int g, int run, const
 }
 
 // copy the tile's unit segment (ng groups) from the stage to global, coalesced
-template <int G, int W>
+template <int G, int W, int GPT = 32>
 __device__ __forceinline__ void copy_out(const uint8_t* base, uint8_t* dst, int ng) {
   const int lane = (int)lane_id();
   const int bytes = ng * OTile<G, W>::GB;
-  if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0 && (bytes & 15) == 0) {
+  constexpr int FULL = GPT * OTile<G, W>::GB;  // bytes of a full tile segment
+  if (ng == GPT && FULL % 512 == 0 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
+#pragma unroll
+    for (int i = 0; i < FULL / 512; ++i) {
+      const int t = lane + 32 * i;
+      *reinterpret_cast<uint4*>(dst + 16 * t) = *reinterpret_cast<const uint4*>(base + OTile<G, W>::lin_pos(t));
+    }
+  } else if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0 && (bytes & 15) == 0) {
     for (int t = lane; t < bytes / 16; t += 32)
       *reinterpret_cast<uint4*>(dst + 16 * t) = *reinterpret_cast<const uint4*>(base + OTile<G, W>::lin_pos(t));
   } else {
@@ -218,9 +225,15 @@ __device__ __forceinline__ void pack_run_fb16(const uint32_t (&X)[32], uint32_t 
 // Writes packed words into the output stage; near-tie elements (split-layout
 // tie masks: bit i < 16 element 2i, bit 16 + i element 2i + 1) are recomputed
 // exactly and patched in the stage.
+#ifndef FC2_TIE_DEFER
+#define FC2_TIE_DEFER 0
+#endif
+#ifndef FC2_SPIKE_STANDIN
+#define FC2_SPIKE_STANDIN 1
+#endif
 template <int B, bool SR, int G, int MODE, int LPG>
-__device__ __forceinline__ void quant_runs(const uint8_t* ist, uint8_t* ost, const GroupParams& p, float Lh,
-                                           bool active) {
+__device__ __forceinline__ void quant_runs(const uint8_t* ist, uint8_t* ost, uint32_t* tms, const GroupParams& p,
+                                           float Lh, bool active) {
   using IT = GTile<__nv_bfloat16, G, LPG>;
   constexpr int GPT = 32 / LPG;
   constexpr int RUNS = G / 32 / LPG;  // runs of this lane
@@ -276,7 +289,9 @@ __device__ __forceinline__ void quant_runs(const uint8_t* ist, uint8_t* ost, con
         for (int e = 0; e < 8; ++e) lw.template put_fixb<FB>(8 * j + e, X[e], 0);
       }
     }
-    if constexpr (FB == 16) pack_run_fb16<B, SR && MODE != 2>(XR, lw.w);
+    // spike slots hold an in-range stand-in (encode_tile_bf16), so every code
+    // fits its width and no masking is needed when the unit is the whole code
+    if constexpr (FB == 16) pack_run_fb16<B, SR && MODE != 2 && !FC2_SPIKE_STANDIN>(XR, lw.w);
 #pragma unroll
     for (int u = 0; u < n_units(B); ++u) {
       const int W = unit_w(B, u);
@@ -287,13 +302,52 @@ __device__ __forceinline__ void quant_runs(const uint8_t* ist, uint8_t* ost, con
       else if (W == 4) stage_words<G, 4>(base, gl, r, w);
       else stage_words<G, 8>(base, gl, r, w);
     }
-    // exact float64 recompute of near-tie elements (rare), patched in smem;
-    // split layout: bit i < 16 -> element 2i, bit 16 + i -> element 2i + 1
+    // near-tie masks of this run, resolved after all runs (one divergent
+    // pass per tile instead of one per run)
+#if FC2_TIE_DEFER
+    tms[32 * rr + (int)lane_id()] = tmj[0] | tmj[1];
+#else
     uint32_t tm = (p.exact ? 0xffffffffu : (tmj[0] | tmj[1])) & (active ? 0xffffffffu : 0u);
     while (tm) {
       const int k = __ffs(tm) - 1;
       tm &= tm - 1;
       const int e = 32 * r + (k < 16 ? 2 * k : 2 * (k - 16) + 1);
+      const float v = __uint_as_float(
+          (uint32_t)*reinterpret_cast<const uint16_t*>(ist + IT::in_pos(gl, e >> 3) * 16 + (e & 7) * 2) << 16);
+      stage_patch<B, G, GPT>(ost, gl, e, exact_code((double)v, p.off, p.div, (1 << B) - 1));
+    }
+#endif
+  }
+}
+
+// exact float64 recompute of the near-tie elements of all runs of this lane
+// (rare), patched in the output stage; split layout of a run mask: bit i < 16
+// -> element 2i, bit 16 + i -> element 2i + 1
+template <int B, int G, int LPG>
+__device__ __forceinline__ void resolve_ties(const uint8_t* ist, uint8_t* ost, const uint32_t* tms,
+                                             const GroupParams& p, bool active) {
+  using IT = GTile<__nv_bfloat16, G, LPG>;
+  constexpr int GPT = 32 / LPG;
+  constexpr int RUNS = G / 32 / LPG;
+  constexpr int L = (1 << B) - 1;
+  const int gl = (int)lane_id() / LPG, r0 = ((int)lane_id() % LPG) * RUNS;
+  uint32_t tm[RUNS];
+  uint32_t any = 0;
+#pragma unroll
+  for (int rr = 0; rr < RUNS; ++rr) {
+    tm[rr] = p.exact ? 0xffffffffu : tms[32 * rr + (int)lane_id()];
+    any |= tm[rr];
+  }
+  if (!active || !any) return;
+#pragma unroll 1
+  for (int rr = 0; rr < RUNS; ++rr) {
+    uint32_t t = tm[0];
+#pragma unroll
+    for (int q = 1; q < RUNS; ++q) t = rr == q ? tm[q] : t;
+    while (t) {
+      const int k = __ffs(t) - 1;
+      t &= t - 1;
+      const int e = 32 * (r0 + rr) + (k < 16 ? 2 * k : 2 * (k - 16) + 1);
       const float v = __uint_as_float(
           (uint32_t)*reinterpret_cast<const uint16_t*>(ist + IT::in_pos(gl, e >> 3) * 16 + (e & 7) * 2) << 16);
       stage_patch<B, G, GPT>(ost, gl, e, exact_code((double)v, p.off, p.div, L));
@@ -306,8 +360,9 @@ __device__ __forceinline__ void quant_runs(const uint8_t* ist, uint8_t* ost, con
 // ---------------------------------------------------------------------------
 
 template <int B, bool SR, int G, int LPG>
-__device__ __forceinline__ void encode_tile_bf16(const uint8_t* ist, uint8_t* ost, bool active, int64_t g_abs,
-                                                 const EncCtx& cx, uint8_t* out, int64_t tile_g0, int ng) {
+__device__ __forceinline__ void encode_tile_bf16(uint8_t* ist, uint8_t* ost, uint32_t* tms, bool active,
+                                                 int64_t g_abs, const EncCtx& cx, uint8_t* out, int64_t tile_g0,
+                                                 int ng) {
   using IT = GTile<__nv_bfloat16, G, LPG>;
   constexpr int GPT = 32 / LPG;
   constexpr int L = (1 << B) - 1;
@@ -450,14 +505,32 @@ __device__ __forceinline__ void encode_tile_bf16(const uint8_t* ist, uint8_t* os
   // 0: folded fma form, 1: explicit (v - off) form, 2: INT_LOG (clamped)
   const bool fold_ok = !p.exact && fabsf(p.nz) <= FX::kFold;
   const float Lh = (float)L + 0.5f;
-  if (cx.intlog) {
-    quant_runs<B, SR, G, 2, LPG>(ist, ost, p, Lh, active);
-  } else if (__all_sync(0xffffffffu, fold_ok || p.exact || !active)) {
-    quant_runs<B, SR, G, 0, LPG>(ist, ost, p, Lh, active);
-  } else {
-    quant_runs<B, SR, G, 1, LPG>(ist, ost, p, Lh, active);
+  if constexpr (SR && FC2_SPIKE_STANDIN) {
+    // Reserved slots are quantized as 0.0 (codec.py:494-496).  0.0 may lie
+    // outside [zero, vmax] and then clips to code 0 (below) or L (above);
+    // the in-range bf16 stand-in with the same code is written over both
+    // slots, so pass 3 yields their codes directly and no code word ever
+    // needs masking.  (Reserved values were read out above.)
+    // (INT_LOG codes are clamped in pass 3 and 0.0 stays as is.)
+    const uint32_t sv = cx.intlog ? 0u
+                                  : (zf > 0.f ? __float_as_uint(zf) >> 16 : (vf < 0.f ? __float_as_uint(vf) >> 16 : 0u));
+    if (active) {
+      if (imin / (G / LPG) == li)
+        *reinterpret_cast<uint16_t*>(ist + IT::in_pos(gl, imin >> 3) * 16 + (imin & 7) * 2) = (uint16_t)sv;
+      if (imax / (G / LPG) == li)
+        *reinterpret_cast<uint16_t*>(ist + IT::in_pos(gl, imax >> 3) * 16 + (imax & 7) * 2) = (uint16_t)sv;
+    }
+    if constexpr (LPG > 1) __syncwarp();
   }
-  if constexpr (SR) {  // reserved slots are quantized as 0.0 (codec.py:494-496)
+  if (cx.intlog) {
+    quant_runs<B, SR, G, 2, LPG>(ist, ost, tms, p, Lh, active);
+  } else if (__all_sync(0xffffffffu, fold_ok || p.exact || !active)) {
+    quant_runs<B, SR, G, 0, LPG>(ist, ost, tms, p, Lh, active);
+  } else {
+    quant_runs<B, SR, G, 1, LPG>(ist, ost, tms, p, Lh, active);
+  }
+  if (FC2_TIE_DEFER) resolve_ties<B, G, LPG>(ist, ost, tms, p, active);
+  if constexpr (SR && !FC2_SPIKE_STANDIN) {  // reserved slots are quantized as 0.0 (codec.py:494-496)
     int sc;
     const uint32_t Xs = fixq_clamped<FB>(0.0f, p.off32, p.inv32, (float)L + 0.5f);
     if (p.exact || (Xs & FX::kTie) == 0u) sc = exact_code(0.0, p.off, p.div, L);
@@ -500,10 +573,10 @@ __device__ __forceinline__ void encode_tile_bf16(const uint8_t* ist, uint8_t* os
     const int W = unit_w(B, u), O = unit_off(B, u);
     const uint8_t* base = ost + OutStage<B, G, GPT>::off(u);
     uint8_t* dst = out + (cx.n * O) / 8 + tile_g0 * (G * W / 8);
-    if (W == 1) copy_out<G, 1>(base, dst, ng);
-    else if (W == 2) copy_out<G, 2>(base, dst, ng);
-    else if (W == 4) copy_out<G, 4>(base, dst, ng);
-    else copy_out<G, 8>(base, dst, ng);
+    if (W == 1) copy_out<G, 1, GPT>(base, dst, ng);
+    else if (W == 2) copy_out<G, 2, GPT>(base, dst, ng);
+    else if (W == 4) copy_out<G, 4, GPT>(base, dst, ng);
+    else copy_out<G, 8, GPT>(base, dst, ng);
   }
   __syncwarp();
 }

@@ -60,6 +60,7 @@ struct ReduceArgs {
 
 template <class Batch>
 __device__ __forceinline__ int find_job(const Batch& b, int64_t t) {
+  if (b.nj == 1) return 0;  // the common single-chunk launch: no search
   int lo = 0, hi = b.nj - 1;
   while (lo < hi) {
     int mid = (lo + hi + 1) >> 1;
@@ -234,11 +235,13 @@ __global__ void __launch_bounds__(WARPS * 32, FC2_ENC_MINB) k_encode_grp(const _
   using IT = GTile<__nv_bfloat16, G, LPG>;
   constexpr int GPT = 32 / LPG;                       // groups per warp tile
   constexpr int IN_BYTES = IT::IN_BYTES / LPG;
-  constexpr int PER_WARP = STAGES * IN_BYTES + OutStage<B, G, GPT>::BYTES;
+  constexpr int TIE_BYTES = G / LPG * 4;               // one 32-bit tie mask per run per lane
+  constexpr int PER_WARP = STAGES * IN_BYTES + OutStage<B, G, GPT>::BYTES + TIE_BYTES;
   extern __shared__ __align__(16) uint8_t smem[];
   const int warp = (int)(threadIdx.x >> 5), lane = (int)lane_id();
   uint8_t* in0 = smem + warp * PER_WARP;
   uint8_t* ost = in0 + STAGES * IN_BYTES;
+  uint32_t* tms = reinterpret_cast<uint32_t*>(ost + OutStage<B, G, GPT>::BYTES);
   const int64_t nw = (int64_t)gridDim.x * WARPS;
   int64_t t = (int64_t)blockIdx.x * WARPS + warp;
   if constexpr (STAGES == 2) {
@@ -272,7 +275,7 @@ __global__ void __launch_bounds__(WARPS * 32, FC2_ENC_MINB) k_encode_grp(const _
     cx.theta = b.theta;
     cx.lut = b.lut;
     cx.err = b.err;
-    encode_tile_bf16<B, SR, G, LPG>(in0 + stage * IN_BYTES, ost, gabs < ngroups, gabs, cx, jb.out, tg0, ng);
+    encode_tile_bf16<B, SR, G, LPG>(in0 + stage * IN_BYTES, ost, tms, gabs < ngroups, gabs, cx, jb.out, tg0, ng);
     if constexpr (STAGES == 2) stage ^= 1;
   }
   cp_async_wait<0>();
@@ -290,11 +293,11 @@ __global__ void __launch_bounds__(WARPS * 32, FC2_ENC_MINB) k_encode_grp(const _
 
 template <int B, bool SR, int G>
 struct EncGrp {
-  static constexpr int LPG = G >= 256 ? G / 128 : 1;  // lanes per group (128 elements per lane at g = 256)
+  static constexpr int LPG = enc_lpg(G);  // lanes per group
   static constexpr int WARPS = FC2_ENC_WARPS;
   static constexpr int STAGES = FC2_ENC_STAGES;
   static constexpr int SMEM =
-      WARPS * (STAGES * GTile<__nv_bfloat16, G>::IN_BYTES / LPG + OutStage<B, G, 32 / LPG>::BYTES);
+      WARPS * (STAGES * GTile<__nv_bfloat16, G>::IN_BYTES / LPG + OutStage<B, G, 32 / LPG>::BYTES + G / LPG * 4);
   static int go(const EncBatch& b, cudaStream_t st) {
     auto kern = k_encode_grp<B, SR, G, WARPS, LPG, STAGES>;
     static bool attr = false;
@@ -509,7 +512,12 @@ __global__ void __launch_bounds__(kDecWarps * 32) k_decode_fast(const __grid_con
     const uint8_t* st = in0 + stage * DecIn<B>::BYTES;
     // metadata record of this lane's first group (in flight with the codes)
     uint32_t rec[3] = {0, 0, 0};
-    int64_t grp = e0 / G;
+    // group of the lane's first element; gin = offset inside it (no 64-bit division)
+    int64_t grp;
+    if ((G & (G - 1)) == 0) grp = e0 >> (__ffs(G) - 1);
+    else if (e0 < 0x7fffffff) grp = (int64_t)((uint32_t)e0 / (uint32_t)G);
+    else grp = e0 / G;
+    int gin = (int)(e0 - grp * G);
     const bool live = e0 < jb.n;
     if (live) load_record(jb.pay + jb.n * B / 8 + grp * rb, rec, rb);
     issue(t + nw, in0 + (stage ^ 1) * DecIn<B>::BYTES);
@@ -570,10 +578,11 @@ __global__ void __launch_bounds__(kDecWarps * 32) k_decode_fast(const __grid_con
       for (int r = 0; r < 4; ++r) {
         const int64_t er = e0 + 32 * r;
         if (er >= jb.n) break;
-        const int64_t g_r = er / G;
-        if (g_r != grp) {  // next group (G < 128): finish the previous one first
+        if (r > 0) gin += 32;
+        if (gin >= G) {  // next group (G < 128): finish the previous one first
           if (b.sr) patch_spikes(grp * G);
-          grp = g_r;
+          gin -= G;
+          grp += 1;
           load_record(jb.pay + jb.n * B / 8 + grp * rb, rec, rb);
           decode_meta();
         }
@@ -668,9 +677,14 @@ __global__ void __launch_bounds__(kDecWarps * 32) k_decode_fast(const __grid_con
     constexpr int EPC = 16 / ESZ;
     constexpr int NCH = kDecTile / EPC;
     if (valid >= kDecTile && (reinterpret_cast<uintptr_t>(y) & 15u) == 0) {
-#pragma unroll 4
-      for (int c = lane; c < NCH; c += 32)
-        *reinterpret_cast<uint4*>(y + c * EPC) = *reinterpret_cast<const uint4*>(ost + 16 * (c ^ ((c >> 3) & 7)));
+      // chunk c = lane + 32 i sits at slot c ^ ((c >> 3) & 7) = 32 i + (lane ^ s),
+      // s = ((lane >> 3) + 4 i) & 7 alternating with i: two base pointers
+      const uint8_t* s0 = ost + 16 * (lane ^ ((lane >> 3) & 7));
+      const uint8_t* s1 = ost + 16 * (lane ^ (((lane >> 3) + 4) & 7));
+      uint4* yd = reinterpret_cast<uint4*>(y) + lane;
+#pragma unroll
+      for (int i = 0; i < NCH / 32; ++i)
+        yd[32 * i] = *reinterpret_cast<const uint4*>((i & 1 ? s1 : s0) + 512 * i);
     } else {
       for (int i = lane; i < valid && i < kDecTile; i += 32) {
         const int c = i / EPC;
