@@ -226,7 +226,7 @@ __device__ __forceinline__ void pack_run_fb16(const uint32_t (&X)[32], uint32_t 
 // tie masks: bit i < 16 element 2i, bit 16 + i element 2i + 1) are recomputed
 // exactly and patched in the stage.
 #ifndef FC2_TIE_DEFER
-#define FC2_TIE_DEFER 0
+#define FC2_TIE_DEFER 1  // 1: warp-cooperative tie resolution after pass 3; 0: per run, per lane
 #endif
 #ifndef FC2_SPIKE_STANDIN
 #define FC2_SPIKE_STANDIN 1
@@ -320,39 +320,109 @@ __device__ __forceinline__ void quant_runs(const uint8_t* ist, uint8_t* ost, uin
   }
 }
 
-// exact float64 recompute of the near-tie elements of all runs of this lane
-// (rare), patched in the output stage; split layout of a run mask: bit i < 16
-// -> element 2i, bit 16 + i -> element 2i + 1
+// patch element e of group g with code c in the output stage by XOR-ing the
+// difference into its 32-bit word: several lanes may patch elements that share
+// a word concurrently (cooperative tie resolution), and each only flips its
+// own bits, which no other lane touches
+template <int B, int G, int GPT = 32>
+__device__ __forceinline__ void stage_patch_xor(uint8_t* ost, int g, int e, int c) {
+#pragma unroll
+  for (int u = 0; u < n_units(B); ++u) {
+    const int W = unit_w(B, u), O = unit_off(B, u);
+    const int bit = e * W;
+    int bp;
+    if (W == 1) bp = OutStage<B, G, GPT>::off(u) + OTile<G, 1>::byte_pos(g, bit >> 3);
+    else if (W == 2) bp = OutStage<B, G, GPT>::off(u) + OTile<G, 2>::byte_pos(g, bit >> 3);
+    else if (W == 4) bp = OutStage<B, G, GPT>::off(u) + OTile<G, 4>::byte_pos(g, bit >> 3);
+    else bp = OutStage<B, G, GPT>::off(u) + OTile<G, 8>::byte_pos(g, bit >> 3);
+    uint32_t* wp = reinterpret_cast<uint32_t*>(ost + (bp & ~3));
+    const int sh = (bp & 3) * 8 + (bit & 7);
+    const uint32_t m = (1u << W) - 1u;
+    const uint32_t cur = (*wp >> sh) & m, want = ((uint32_t)c >> O) & m;
+    if (cur != want) atomicXor(wp, (cur ^ want) << sh);
+  }
+}
+
+// Exact float64 recompute of the near-tie elements of the tile, done by the
+// whole warp: every lane's tie masks (one per run, left in smem by pass 3:
+// bit i < 16 -> element 2i, bit 16 + i -> element 2i + 1) are compacted into
+// one list (lane << 16 | element), and the 32 lanes resolve 32 entries per
+// round, each fetching its group's offset/divisor from the owning lane by
+// shuffle.  Ties are ~0.1-0.3% of elements, so one round usually covers the
+// tile instead of one divergent pass per run.  Groups that need float64 for
+// every element (p.exact) loop on their own.
 template <int B, int G, int LPG>
-__device__ __forceinline__ void resolve_ties(const uint8_t* ist, uint8_t* ost, const uint32_t* tms,
-                                             const GroupParams& p, bool active) {
+__device__ __forceinline__ void resolve_ties_coop(const uint8_t* ist, uint8_t* ost, uint32_t* tms,
+                                                  const GroupParams& p, bool active) {
   using IT = GTile<__nv_bfloat16, G, LPG>;
   constexpr int GPT = 32 / LPG;
   constexpr int RUNS = G / 32 / LPG;
   constexpr int L = (1 << B) - 1;
-  const int gl = (int)lane_id() / LPG, r0 = ((int)lane_id() % LPG) * RUNS;
-  uint32_t tm[RUNS];
-  uint32_t any = 0;
+  constexpr int CAP = RUNS * 32;  // list entries that fit in the mask area
+  const int lane = (int)lane_id();
+  const int gl = lane / LPG, r0 = (lane % LPG) * RUNS;
+  auto value = [&](int g, int e) -> double {
+    return (double)__uint_as_float(
+        (uint32_t)*reinterpret_cast<const uint16_t*>(ist + IT::in_pos(g, e >> 3) * 16 + (e & 7) * 2) << 16);
+  };
+  __syncwarp();
+  uint32_t m[RUNS];
+  int cnt = 0;
+  const bool listed = active && !p.exact;
 #pragma unroll
   for (int rr = 0; rr < RUNS; ++rr) {
-    tm[rr] = p.exact ? 0xffffffffu : tms[32 * rr + (int)lane_id()];
-    any |= tm[rr];
+    m[rr] = listed ? tms[32 * rr + lane] : 0u;
+    cnt += __popc(m[rr]);
   }
-  if (!active || !any) return;
-#pragma unroll 1
-  for (int rr = 0; rr < RUNS; ++rr) {
-    uint32_t t = tm[0];
+  int incl = cnt;
 #pragma unroll
-    for (int q = 1; q < RUNS; ++q) t = rr == q ? tm[q] : t;
-    while (t) {
-      const int k = __ffs(t) - 1;
-      t &= t - 1;
-      const int e = 32 * (r0 + rr) + (k < 16 ? 2 * k : 2 * (k - 16) + 1);
-      const float v = __uint_as_float(
-          (uint32_t)*reinterpret_cast<const uint16_t*>(ist + IT::in_pos(gl, e >> 3) * 16 + (e & 7) * 2) << 16);
-      stage_patch<B, G, GPT>(ost, gl, e, exact_code((double)v, p.off, p.div, L));
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  if (total > 0) {  // warp-uniform
+    if (total <= CAP) {
+      __syncwarp();  // every lane has read its masks before the list overwrites them
+      int pos = incl - cnt;
+#pragma unroll
+      for (int rr = 0; rr < RUNS; ++rr) {
+        uint32_t t = m[rr];
+        while (t) {
+          const int k = __ffs(t) - 1;
+          t &= t - 1;
+          tms[pos++] = ((uint32_t)lane << 16) | (uint32_t)(32 * (r0 + rr) + (k < 16 ? 2 * k : 2 * (k - 16) + 1));
+        }
+      }
+      __syncwarp();
+      for (int base = 0; base < total; base += 32) {  // warp-uniform rounds
+        const int i = base + lane;
+        const uint32_t ent = i < total ? tms[i] : 0u;
+        const int src = (int)(ent >> 16), e = (int)(ent & 0xFFFFu);
+        const double off = __shfl_sync(0xffffffffu, p.off, src), div = __shfl_sync(0xffffffffu, p.div, src);
+        if (i < total) stage_patch_xor<B, G, GPT>(ost, src / LPG, e, exact_code(value(src / LPG, e), off, div, L));
+      }
+    } else {  // many ties in one tile (rare): each lane resolves its own
+#pragma unroll 1
+      for (int rr = 0; rr < RUNS; ++rr) {
+        uint32_t t = m[0];
+#pragma unroll
+        for (int q = 1; q < RUNS; ++q) t = rr == q ? m[q] : t;
+        while (t) {
+          const int k = __ffs(t) - 1;
+          t &= t - 1;
+          const int e = 32 * (r0 + rr) + (k < 16 ? 2 * k : 2 * (k - 16) + 1);
+          stage_patch_xor<B, G, GPT>(ost, gl, e, exact_code(value(gl, e), p.off, p.div, L));
+        }
+      }
     }
   }
+  if (active && p.exact) {  // every element of the group in float64
+#pragma unroll 1
+    for (int e = r0 * 32; e < (r0 + RUNS) * 32; ++e)
+      stage_patch_xor<B, G, GPT>(ost, gl, e, exact_code(value(gl, e), p.off, p.div, L));
+  }
+  __syncwarp();
 }
 
 // ---------------------------------------------------------------------------
@@ -529,7 +599,7 @@ __device__ __forceinline__ void encode_tile_bf16(uint8_t* ist, uint8_t* ost, uin
   } else {
     quant_runs<B, SR, G, 1, LPG>(ist, ost, tms, p, Lh, active);
   }
-  if (FC2_TIE_DEFER) resolve_ties<B, G, LPG>(ist, ost, tms, p, active);
+  if (FC2_TIE_DEFER) resolve_ties_coop<B, G, LPG>(ist, ost, tms, p, active);
   if constexpr (SR && !FC2_SPIKE_STANDIN) {  // reserved slots are quantized as 0.0 (codec.py:494-496)
     int sc;
     const uint32_t Xs = fixq_clamped<FB>(0.0f, p.off32, p.inv32, (float)L + 0.5f);
