@@ -118,6 +118,16 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 
 
+def flush_l2(buf):
+    """Evict L2 between timed steps: write a buffer twice the size of the
+    126 MB L2, then read it back so the lines left behind are clean (a
+    write-only flush leaves ~126 MB of dirty lines whose write-back would be
+    billed to the next timed kernel).  FC2_FLUSH_READ=0: write only."""
+    buf.zero_()
+    if os.environ.get("FC2_FLUSH_READ", "1") != "0":
+        buf.view(-1, 4096).amax(dim=1)
+
+
 def spiky_bf16(n, seed, device):
     import torch
 
@@ -138,14 +148,14 @@ def time_roundtrip(fc, x, cfg, steps, warmup, flush):
     err = torch.zeros(1, dtype=torch.int32, device=x.device)
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
     for _ in range(warmup):
-        flush.zero_()
+        flush_l2(flush)
         fc.encode_payload(x, cfg, n, out=pay, err=err, check=False)
         fc.decode_payload(pay, cfg, n, out=y, err=err, check=False)
     torch.cuda.synchronize()
     lib = fc._lib.lib()
     l0 = lib.fc2_launch_count()
     for i in range(steps):
-        flush.zero_()  # evict L2 between steps (outside the timed region)
+        flush_l2(flush)  # evict L2 between steps (outside the timed region)
         ev[i][0].record()
         fc.encode_payload(x, cfg, n, out=pay, err=err, check=False)
         ev[i][1].record()
@@ -194,7 +204,7 @@ def two_step_stage_times(fc, x, cfg, flush, steps, N=8):
             fn()
         ts = []
         for _ in range(steps):
-            flush.zero_()
+            flush_l2(flush)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             fn()
@@ -206,27 +216,35 @@ def two_step_stage_times(fc, x, cfg, flush, steps, N=8):
     return out
 
 
-def time_e2e(fc, x_host, cfg, steps, warmup):
-    """Host-buffer round trip through the public API: pinned bf16 in -> H2D ->
-    encode -> payload D2H (the wire bytes) -> decode -> bf16 D2H."""
+def time_e2e(fc, x_host, cfg, steps, warmup, serial=False):
+    """Host-buffer round trip through the public API: pinned bf16 chunk in ->
+    packed payload bytes and decoded bf16 values back in pinned host memory.
+    Default: one roundtrip_host call (fc2_roundtrip_host: the chunk is sliced
+    and H2D / kernels / D2H of different slices overlap on internal streams).
+    serial=True: the unpipelined sequence H2D -> encode -> D2H payload ->
+    decode -> D2H values on one stream, for comparison."""
     import torch
 
     n = x_host.numel()
     F = fc.footprint_bytes(cfg, n)
     dev = torch.device("cuda")
-    xd = torch.empty(n, dtype=torch.bfloat16, device=dev)
-    pay = torch.empty(F, dtype=torch.uint8, device=dev)
-    yd = torch.empty(n, dtype=torch.bfloat16, device=dev)
     pay_h = torch.empty(F, dtype=torch.uint8).pin_memory()
     y_h = torch.empty(n, dtype=torch.bfloat16).pin_memory()
-    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    if serial:
+        xd = torch.empty(n, dtype=torch.bfloat16, device=dev)
+        pay = torch.empty(F, dtype=torch.uint8, device=dev)
+        yd = torch.empty(n, dtype=torch.bfloat16, device=dev)
+        err = torch.zeros(1, dtype=torch.int32, device=dev)
 
-    def step():
-        xd.copy_(x_host, non_blocking=True)
-        fc.encode_payload(xd, cfg, n, out=pay, err=err, check=False)
-        pay_h.copy_(pay, non_blocking=True)
-        fc.decode_payload(pay, cfg, n, out=yd, err=err, check=False)
-        y_h.copy_(yd, non_blocking=True)
+        def step():
+            xd.copy_(x_host, non_blocking=True)
+            fc.encode_payload(xd, cfg, n, out=pay, err=err, check=False)
+            pay_h.copy_(pay, non_blocking=True)
+            fc.decode_payload(pay, cfg, n, out=yd, err=err, check=False)
+            y_h.copy_(yd, non_blocking=True)
+    else:
+        def step():
+            fc.roundtrip_host(x_host, cfg, payload=pay_h, out=y_h, check=False)
 
     for _ in range(warmup):
         step()
@@ -238,6 +256,10 @@ def time_e2e(fc, x_host, cfg, steps, warmup):
     e.record()
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / steps
+    if not serial:  # the bytes that came back are the device path's bytes
+        want = fc.encode_payload(x_host.cuda(), cfg, n).cpu()
+        if not torch.equal(pay_h, want):
+            raise RuntimeError("roundtrip_host payload differs from the device path")
     return ms, 2 * n, F + 2 * n
 
 
@@ -288,7 +310,7 @@ def run_codec(args):
     }
     dom = "encode" if t_enc >= t_dec else "decode"
     roof = {
-        "kernel": "k_encode_fast" if dom == "encode" else "k_decode_fast",
+        "kernel": "k_encode_grp" if dom == "encode" else "k_decode_fast",
         "bound": "hbm",
         "achieved": kernels[dom]["GBps"],
         "peak": peak,
@@ -318,6 +340,7 @@ def run_codec(args):
     # end to end through host buffers
     x_host = x.cpu().pin_memory()
     e2e_ms, h2d, d2h = time_e2e(fc, x_host, cfg, max(3, args.steps), 2)
+    e2e_serial_ms, _, _ = time_e2e(fc, x_host, cfg, max(3, args.steps // 2), 1, serial=True)
     cpu_val, cpu_dt = cpu_baseline_codec(n, args.cpu_reps, args.bits, args.group, sr)
     line = {
         "metric": METRIC,
@@ -335,12 +358,16 @@ def run_codec(args):
         "data": "synthetic: N(0,1) with 1/64 of entries at +-50 (reference default_spiky_spec), bf16",
         "config": {"workload": "codec round trip, 64 MiB bf16 tensor (BASELINE configs[1])",
                    "n": n, "bits": args.bits, "group": args.group, "scheme": args.scheme,
-                   "payload_bytes": F, "l2": "flushed (256 MiB write) before every step"},
+                   "payload_bytes": F, "l2": "flushed before every step (256 MiB write, then read back)"},
         "kernels": kernels,
         "roofline": roof,
         "e2e": {"value": round(2 * n / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
                 "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "path": "encode_payload/decode_payload (C ABI) with pinned host buffers"},
+                "path": "roundtrip_host -> fc2_roundtrip_host (C ABI): pinned host chunk in, payload bytes + "
+                        "decoded bf16 back in pinned host memory; 4 Mi-element slices, PCIe both ways "
+                        "overlapped with the kernels",
+                "serial_value": round(2 * n / (e2e_serial_ms * 1e-3) / 1e9, 2),
+                "serial_path": "H2D -> encode_payload -> D2H payload -> decode_payload -> D2H values, one stream"},
         "cpu_baseline": None if cpu_val is None else {
             "value": round(cpu_val, 4), "unit": "GB/s", "cores": 1, "kind": "port",
             "sample": f"full workload ({n} elements) x {args.cpu_reps}, oracle/fc2_oracle.py "
@@ -404,12 +431,12 @@ def run_allreduce(args, rank, world, local_rank):
 
     def timed(fn, steps, warmup):
         for _ in range(warmup):
-            flush.zero_()
+            flush_l2(flush)
             fn()
         torch.cuda.synchronize()
         tot = 0.0
         for _ in range(steps):
-            flush.zero_()
+            flush_l2(flush)
             dist.barrier()
             torch.cuda.synchronize()
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -472,7 +499,7 @@ def run_allreduce(args, rank, world, local_rank):
             "data": "synthetic spiky bf16 per rank",
             "config": {"workload": "two-step quantized AllReduce, 8192x4096 bf16 per rank (BASELINE configs[2])",
                        "n": n, "bits": args.bits, "group": args.group, "scheme": args.scheme,
-                       "l2": "flushed before every step", "parallelism": f"tp{world}"},
+                       "l2": "flushed before every step (256 MiB write, then read back)", "parallelism": f"tp{world}"},
             "nccl_bf16": None if ms_nccl is None else {
                 "ms": round(ms_nccl, 5), "algbw_GBps": round(2 * n / (ms_nccl * 1e-3) / 1e9, 2),
                 "speedup": round(ms_nccl / ms, 3), "nvls_env": os.environ.get("NCCL_NVLS_ENABLE", "default")},

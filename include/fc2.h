@@ -111,6 +111,29 @@ int fc2_gather_decode(const fc2_config* cfg, int32_t nshards, const void* const*
                       int64_t shard_len, void* y, int32_t y_dtype, int64_t n_out,
                       int32_t* dev_err, void* stream);
 
+/* Host-resident chunks (the reference's encode_chunk / decode_chunk take and
+ * return host arrays and bytes: codec.py:477-519, 522-563).  The chunk of n
+ * elements lives in host memory (pin it for overlap); the caller supplies the
+ * device staging buffers (x_dev: n elements, payload_dev: fc2_footprint(n)
+ * bytes, y_dev: n elements) so nothing is allocated per call.  The chunk is
+ * processed in slices of `slice` elements (rounded up to a multiple of 32768
+ * and of group_size; <= 0: 4 Mi) on internal streams so host<->device copies
+ * in both directions overlap the kernels; stream-ordered with respect to
+ * `stream`.  payload_host holds the exact payload bytes (planes, then
+ * metadata; R9-R11).  Round trip = encode then decode of the same chunk, the
+ * QDQ of collectives.py:179-182 (_encode_once); payload_host may be NULL
+ * there when only the decoded values are wanted. */
+int fc2_encode_host(const fc2_config* cfg, const void* x_host, int32_t x_dtype, int64_t n,
+                    void* x_dev, void* payload_dev, void* payload_host, int64_t slice,
+                    int32_t* dev_err, void* stream);
+int fc2_decode_host(const fc2_config* cfg, const void* payload_host, int64_t n, void* payload_dev,
+                    void* y_dev, int32_t y_dtype, void* y_host, int64_t slice, int32_t* dev_err,
+                    void* stream);
+int fc2_roundtrip_host(const fc2_config* cfg, const void* x_host, int32_t x_dtype, int64_t n,
+                       void* x_dev, void* payload_dev, void* y_dev, int32_t y_dtype,
+                       void* payload_host, void* y_host, int64_t slice, int32_t* dev_err,
+                       void* stream);
+
 /* pack_codes / unpack_codes (codec.py:204-238): codes are int64 (range
  * checked on device, FC2_ERR_CODE_RANGE), n % 8 == 0; planes is one
  * contiguous buffer (plane 0, plane 1, ...). */

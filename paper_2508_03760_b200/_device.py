@@ -74,3 +74,18 @@ def ensure_intlog(theta: int, device) -> None:
         _lib.check(_lib.lib().fc2_set_intlog_table(int(theta), buf.ctypes.data_as(
             __import__("ctypes").POINTER(__import__("ctypes").c_double))))
     _INTLOG_LOADED.add(key)
+
+
+_WORKSPACES: dict[tuple[int, str], torch.Tensor] = {}
+
+
+def workspace(name: str, nbytes: int, device) -> torch.Tensor:
+    """A cached uint8 device buffer of at least ``nbytes`` (staging for the
+    host-resident pipeline; grown, never shrunk)."""
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    key = (idx, name)
+    buf = _WORKSPACES.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=torch.device("cuda", idx))
+        _WORKSPACES[key] = buf
+    return buf

@@ -62,6 +62,9 @@ SIGNATURES = {
     "fc2_encode_batch": (_I32, [_PCFG, _I32, _I32, _PP, _PI64, _PI64, _PP, _P, _P]),
     "fc2_decode": (_I32, [_PCFG, _P, _I64, _P, _I32, _I64, _P, _P]),
     "fc2_decode_batch": (_I32, [_PCFG, _I32, _I32, _PP, _PI64, _PP, _PI64, _P, _P]),
+    "fc2_encode_host": (_I32, [_PCFG, _P, _I32, _I64, _P, _P, _P, _I64, _P, _P]),
+    "fc2_decode_host": (_I32, [_PCFG, _P, _I64, _P, _P, _I32, _P, _I64, _P, _P]),
+    "fc2_roundtrip_host": (_I32, [_PCFG, _P, _I32, _I64, _P, _P, _P, _I32, _P, _P, _I64, _P, _P]),
     "fc2_reduce_requant": (_I32, [_PCFG, _I32, _PP, _I64, _I32, _PP, _P, _P]),
     "fc2_gather_decode": (_I32, [_PCFG, _I32, _PP, _I64, _P, _I32, _I64, _P, _P]),
     "fc2_pack_codes": (_I32, [_P, _I64, _I32, _P, _P, _P]),

@@ -45,7 +45,7 @@ __all__ = [
     "QuantConfig", "Scheme", "ScaleEncoding", "GroupMeta", "QuantizedChunk",
     "bit_split", "default_group_size", "footprint_bytes", "footprint_breakdown",
     "meta_record_nbytes", "encode_chunk", "decode_chunk", "pack_codes", "unpack_codes",
-    "parse_chunk", "encode_payload", "decode_payload",
+    "parse_chunk", "encode_payload", "decode_payload", "encode_host", "decode_host", "roundtrip_host",
 ]
 
 
@@ -224,6 +224,110 @@ def decode_payload(payload: torch.Tensor, config: QuantConfig, n: int,
     if check and own_err:
         _device.check_err(err)
     return out
+
+
+# ---------------------------------------------------------------------------
+# host-resident entry points: CPU tensors in/out, PCIe overlapped with the
+# kernels (fc2_encode_host / fc2_decode_host / fc2_roundtrip_host)
+# ---------------------------------------------------------------------------
+
+
+def _host_tensor(t, what):
+    if not isinstance(t, torch.Tensor) or t.is_cuda or not t.is_contiguous():
+        raise TypeError(f"{what} must be a contiguous CPU tensor (pinned for overlap)")
+    return t
+
+
+def encode_host(x: torch.Tensor, config: QuantConfig, payload: torch.Tensor | None = None,
+                slice_elems: int = 1 << 22, check: bool = True) -> torch.Tensor:
+    """encode_chunk of a host-resident chunk (codec.py:477-519): CPU bf16 /
+    float32 / float64 tensor of n elements (n % group_size == 0) -> uint8 CPU
+    payload (planes, then metadata).  Stream-ordered; with ``check`` the call
+    synchronizes and raises the reference's errors."""
+    dev = _device.require_cuda()
+    if config.int_log:
+        _device.ensure_intlog(config.theta, dev)
+    x = _host_tensor(x, "x").reshape(-1)
+    n = x.numel()
+    F = footprint_bytes(config, n)
+    if payload is None:
+        payload = torch.empty(F, dtype=torch.uint8, pin_memory=True)
+    _host_tensor(payload, "payload")
+    xd = _device.workspace("host_x", n * x.element_size(), dev)
+    pd = _device.workspace("host_pay", F, dev)
+    err = _device.workspace("host_err", 4, dev)[:4].view(torch.int32)
+    err.zero_()
+    cfg = config.c_struct()
+    _lib.check(_lib.lib().fc2_encode_host(ctypes.byref(cfg), x.data_ptr(), _device.dtype_code(x), n,
+                                          xd.data_ptr(), pd.data_ptr(), payload.data_ptr(), int(slice_elems),
+                                          err.data_ptr(), _device.stream_handle()))
+    if check:
+        torch.cuda.current_stream().synchronize()
+        _device.check_err(err)
+    return payload
+
+
+def decode_host(payload: torch.Tensor, config: QuantConfig, n: int, out: torch.Tensor | None = None,
+                out_dtype: torch.dtype = torch.float32, slice_elems: int = 1 << 22,
+                check: bool = True) -> torch.Tensor:
+    """decode_chunk of a host-resident payload (codec.py:522-563) into a CPU
+    tensor of ``out_dtype`` (bf16 / float32 / float64)."""
+    dev = _device.require_cuda()
+    if config.int_log:
+        _device.ensure_intlog(config.theta, dev)
+    payload = _host_tensor(payload, "payload")
+    F = footprint_bytes(config, n)
+    if payload.numel() < F:
+        raise DecodeFormatError(f"payload has {payload.numel()} bytes, chunk needs {F}")
+    if out is None:
+        out = torch.empty(n, dtype=out_dtype, pin_memory=True)
+    _host_tensor(out, "out")
+    pd = _device.workspace("host_pay", F, dev)
+    yd = _device.workspace("host_y", n * out.element_size(), dev)
+    err = _device.workspace("host_err", 4, dev)[:4].view(torch.int32)
+    err.zero_()
+    cfg = config.c_struct()
+    _lib.check(_lib.lib().fc2_decode_host(ctypes.byref(cfg), payload.data_ptr(), n, pd.data_ptr(), yd.data_ptr(),
+                                          _device.dtype_code(out), out.data_ptr(), int(slice_elems),
+                                          err.data_ptr(), _device.stream_handle()))
+    if check:
+        torch.cuda.current_stream().synchronize()
+        _device.check_err(err)
+    return out
+
+
+def roundtrip_host(x: torch.Tensor, config: QuantConfig, payload: torch.Tensor | None = None,
+                   out: torch.Tensor | None = None, out_dtype: torch.dtype | None = None,
+                   slice_elems: int = 1 << 22, check: bool = True):
+    """Encode then decode a host-resident chunk in one pipelined pass (the
+    QDQ of collectives.py:179-182): returns (payload, decoded) CPU tensors;
+    pass ``payload=False`` to skip copying the packed bytes back."""
+    dev = _device.require_cuda()
+    if config.int_log:
+        _device.ensure_intlog(config.theta, dev)
+    x = _host_tensor(x, "x").reshape(-1)
+    n = x.numel()
+    F = footprint_bytes(config, n)
+    if payload is None:
+        payload = torch.empty(F, dtype=torch.uint8, pin_memory=True)
+    if out is None:
+        out = torch.empty(n, dtype=out_dtype or x.dtype, pin_memory=True)
+    _host_tensor(out, "out")
+    xd = _device.workspace("host_x", n * x.element_size(), dev)
+    pd = _device.workspace("host_pay", F, dev)
+    yd = _device.workspace("host_y", n * out.element_size(), dev)
+    err = _device.workspace("host_err", 4, dev)[:4].view(torch.int32)
+    err.zero_()
+    cfg = config.c_struct()
+    ph = 0 if payload is False else _host_tensor(payload, "payload").data_ptr()
+    _lib.check(_lib.lib().fc2_roundtrip_host(ctypes.byref(cfg), x.data_ptr(), _device.dtype_code(x), n,
+                                             xd.data_ptr(), pd.data_ptr(), yd.data_ptr(), _device.dtype_code(out),
+                                             ph, out.data_ptr(), int(slice_elems), err.data_ptr(),
+                                             _device.stream_handle()))
+    if check:
+        torch.cuda.current_stream().synchronize()
+        _device.check_err(err)
+    return (None if payload is False else payload), out
 
 
 # ---------------------------------------------------------------------------

@@ -332,12 +332,29 @@ int fc2_set_intlog_table(int32_t theta, const double* table256) {
   return FC2_OK;
 }
 
-int fc2_encode_batch(const fc2_config* cfg, int32_t x_dtype, int32_t njobs, const void* const* xs,
-                     const int64_t* n_valid, const int64_t* n, void* const* payloads, int32_t* dev_err,
-                     void* stream) {
+}  // extern "C"
+
+namespace fc2 {
+// Encode tile granularity of a job (elements): the unit a sub-range launch
+// must start on.  Fast bf16: one warp tile of 32 / LPG groups; fast f32: 1024;
+// generic: one group.
+static int64_t enc_unit(const fc2_config* cfg, int32_t x_dtype, const void* x, int64_t n_valid) {
+  const int G = cfg->group_size;
+  const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15u) == 0 || n_valid == 0;
+  if (!(fast_group(G) && x_dtype != FC2_F64 && aligned)) return G;
+  return x_dtype == FC2_BF16 ? 32 / enc_lpg(G) * (int64_t)G : 1024;
+}
+
+// e_begin / e_end (nullable): encode only elements [e_begin, e_end) of each
+// chunk (e_begin a multiple of enc_unit); the job's tile numbering is shifted
+// with a negative t0 so the kernels see absolute tile indices.
+static int encode_batch_impl(const fc2_config* cfg, int32_t x_dtype, int32_t njobs, const void* const* xs,
+                             const int64_t* n_valid, const int64_t* n, void* const* payloads, int32_t* dev_err,
+                             void* stream, const int64_t* e_begin, const int64_t* e_end) {
   int rc = check_cfg(cfg);
   if (rc) return rc;
   if (njobs < 0 || njobs > FC2_MAX_JOBS) return set_err(FC2_ECONFIG, "njobs %d out of range", njobs);
+  if ((e_begin || e_end) && njobs != 1) return set_err(FC2_ECONFIG, "sub-range encode takes one job");
   if (x_dtype < 0 || x_dtype > 2) return set_err(FC2_ECONFIG, "bad dtype %d", x_dtype);
   const double* lut = lut_for(cfg, &rc);
   if (rc) return rc;
@@ -363,11 +380,16 @@ int fc2_encode_batch(const fc2_config* cfg, int32_t x_dtype, int32_t njobs, cons
     j.out = (uint8_t*)payloads[i];
     j.n_valid = n_valid[i];
     j.n = n[i];
-    j.t0 = b->total;
-    // fast tiles: bf16 -> 32 groups per warp tile (lane per group); f32 -> 1024 elements
-    const int64_t lpg = enc_lpg(G);  // EncGrp::LPG
-    const int64_t tile = x_dtype == FC2_BF16 ? 32 / lpg * (int64_t)G : 1024;
-    b->total += use_fast ? (n[i] + tile - 1) / tile : n[i] / G;
+    // fast tiles: bf16 -> 32 / LPG groups per warp tile; f32 -> 1024 elements; generic: groups
+    const int64_t tile = enc_unit(cfg, x_dtype, xs[i], n_valid[i]);
+    const int64_t eb = e_begin ? e_begin[i] : 0, ee = e_end ? e_end[i] : n[i];
+    if (eb % tile || eb < 0 || ee > n[i] || ee < eb)
+      return set_err(FC2_ECONFIG, "encode range [%lld, %lld) not on a %lld-element boundary", (long long)eb,
+                     (long long)ee, (long long)tile);
+    const int64_t first = eb / tile, last = (ee + tile - 1) / tile;
+    if (last <= first) { b->nj--; continue; }
+    j.t0 = b->total - first;
+    b->total += last - first;
     (void)esz;
   }
   if (fast.nj) {
@@ -387,6 +409,16 @@ int fc2_encode_batch(const fc2_config* cfg, int32_t x_dtype, int32_t njobs, cons
   return FC2_OK;
 }
 
+}  // namespace fc2
+
+extern "C" {
+
+int fc2_encode_batch(const fc2_config* cfg, int32_t x_dtype, int32_t njobs, const void* const* xs,
+                     const int64_t* n_valid, const int64_t* n, void* const* payloads, int32_t* dev_err,
+                     void* stream) {
+  return encode_batch_impl(cfg, x_dtype, njobs, xs, n_valid, n, payloads, dev_err, stream, nullptr, nullptr);
+}
+
 int fc2_encode(const fc2_config* cfg, const void* x, int32_t x_dtype, int64_t n_valid, int64_t n, void* payload,
                int32_t* dev_err, void* stream) {
   return fc2_encode_batch(cfg, x_dtype, 1, &x, &n_valid, &n, &payload, dev_err, stream);
@@ -394,7 +426,8 @@ int fc2_encode(const fc2_config* cfg, const void* x, int32_t x_dtype, int64_t n_
 
 static int decode_batch_impl(const fc2_config* cfg, int32_t y_dtype, int32_t njobs, const void* const* payloads,
                              const int64_t* n, void* const* ys, const int64_t* n_out, int32_t* dev_err,
-                             void* stream, int round_bf16);
+                             void* stream, int round_bf16, const int64_t* e_begin = nullptr,
+                             const int64_t* e_end = nullptr);
 
 int fc2_decode_batch(const fc2_config* cfg, int32_t y_dtype, int32_t njobs, const void* const* payloads,
                      const int64_t* n, void* const* ys, const int64_t* n_out, int32_t* dev_err, void* stream) {
@@ -403,10 +436,11 @@ int fc2_decode_batch(const fc2_config* cfg, int32_t y_dtype, int32_t njobs, cons
 
 static int decode_batch_impl(const fc2_config* cfg, int32_t y_dtype, int32_t njobs, const void* const* payloads,
                              const int64_t* n, void* const* ys, const int64_t* n_out, int32_t* dev_err,
-                             void* stream, int round_bf16) {
+                             void* stream, int round_bf16, const int64_t* e_begin, const int64_t* e_end) {
   int rc = check_cfg(cfg);
   if (rc) return rc;
   if (njobs < 0 || njobs > FC2_MAX_JOBS) return set_err(FC2_ECONFIG, "njobs %d out of range", njobs);
+  if ((e_begin || e_end) && njobs != 1) return set_err(FC2_ECONFIG, "sub-range decode takes one job");
   if (y_dtype < 0 || y_dtype > 2) return set_err(FC2_ECONFIG, "bad dtype %d", y_dtype);
   const double* lut = lut_for(cfg, &rc);
   if (rc) return rc;
@@ -429,8 +463,16 @@ static int decode_batch_impl(const fc2_config* cfg, int32_t y_dtype, int32_t njo
     j.y = ys[i];
     j.n = n[i];
     j.n_out = n_out[i];
-    j.t0 = b.total;
-    b.total += fastG ? (n[i] + 4095) / 4096 : n_out[i];
+    // sub-range [e_begin, e_end): fast tiles are 4096 elements, generic units one element
+    const int64_t unit = fastG ? 4096 : 1;
+    const int64_t eb = e_begin ? e_begin[i] : 0;
+    const int64_t ee = e_end ? (e_end[i] < n_out[i] ? e_end[i] : n_out[i]) : n_out[i];
+    if (eb % unit || eb < 0) return set_err(FC2_ECONFIG, "decode range start %lld not on a %lld-element boundary",
+                                             (long long)eb, (long long)unit);
+    const int64_t first = eb / unit, last = (ee + unit - 1) / unit;
+    if (last <= first) { b.nj--; continue; }
+    j.t0 = b.total - first;
+    b.total += last - first;
   }
   if (!b.nj) return FC2_OK;
   if (fastG) {
@@ -451,6 +493,175 @@ return dec_fast(B, y_dtype, blocks, b, st);
 int fc2_decode(const fc2_config* cfg, const void* payload, int64_t n, void* y, int32_t y_dtype, int64_t n_out,
                int32_t* dev_err, void* stream) {
   return fc2_decode_batch(cfg, y_dtype, 1, &payload, &n, &y, &n_out, dev_err, stream);
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// host-buffer pipeline: encode_chunk / decode_chunk / their round trip with
+// the chunk in host memory.  The chunk is cut into slices on tile boundaries;
+// slice k runs on internal stream k % kPipeStreams as
+//   H2D(x slice) -> encode(slice) -> D2H(plane + meta segments of the slice)
+//   [-> decode(slice) -> D2H(y slice)]            (round trip)
+//   H2D(payload segments) -> decode(slice) -> D2H(y slice)   (decode only)
+// so PCIe traffic in both directions overlaps the kernels and each other.
+// Stream-ordered with respect to the caller's stream (event fork / join).
+// ---------------------------------------------------------------------------
+
+namespace fc2 {
+
+constexpr int kPipeStreams = 4;  // s[0]: uploads; s[1..3]: kernels + downloads, round robin
+constexpr int kPipeEvents = 8;
+struct HostPipe {
+  cudaStream_t s[kPipeStreams];
+  cudaEvent_t fork, join[kPipeStreams], up[kPipeEvents];
+};
+
+static HostPipe* host_pipe(int* rc) {
+  static HostPipe pipes[64];
+  static bool made[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) { *rc = set_err(FC2_ECUDA, "device %d out of range", dev); return nullptr; }
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!made[dev]) {
+    HostPipe& p = pipes[dev];
+    for (int i = 0; i < kPipeStreams; ++i) {
+      if (cudaStreamCreateWithFlags(&p.s[i], cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&p.join[i], cudaEventDisableTiming) != cudaSuccess) {
+        *rc = set_err(FC2_ECUDA, "host pipeline stream/event creation failed");
+        return nullptr;
+      }
+    }
+    bool ok = cudaEventCreateWithFlags(&p.fork, cudaEventDisableTiming) == cudaSuccess;
+    for (int i = 0; i < kPipeEvents; ++i)
+      ok = ok && cudaEventCreateWithFlags(&p.up[i], cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) {
+      *rc = set_err(FC2_ECUDA, "host pipeline event creation failed");
+      return nullptr;
+    }
+    made[dev] = true;
+  }
+  *rc = FC2_OK;
+  return &pipes[dev];
+}
+
+static int esize(int32_t dt) { return dt == FC2_BF16 ? 2 : (dt == FC2_F32 ? 4 : (dt == FC2_F64 ? 8 : 0)); }
+
+// copy the payload bytes of elements [e0, e1) (one segment per plane + the
+// metadata segment) between host and device
+static int copy_payload_slice(const fc2_config* cfg, int64_t n, int64_t e0, int64_t e1, void* dev, void* host,
+                              cudaMemcpyKind kind, cudaStream_t st) {
+  const int B = cfg->bitwidth, G = cfg->group_size;
+  for (int u = 0; u < n_units(B); ++u) {
+    const int W = unit_w(B, u);
+    const int64_t off = n * unit_off(B, u) / 8 + e0 * W / 8, len = (e1 - e0) * W / 8;
+    uint8_t* d = (uint8_t*)dev + off;
+    uint8_t* h = (uint8_t*)host + off;
+    if (cudaMemcpyAsync(kind == cudaMemcpyHostToDevice ? (void*)d : (void*)h,
+                        kind == cudaMemcpyHostToDevice ? (const void*)h : (const void*)d, len, kind, st) != cudaSuccess)
+      return set_err(FC2_ECUDA, "payload plane copy failed");
+  }
+  const int64_t rb = rec_nb(cfg), off = n * B / 8 + e0 / G * rb, len = (e1 - e0) / G * rb;
+  uint8_t* d = (uint8_t*)dev + off;
+  uint8_t* h = (uint8_t*)host + off;
+  if (cudaMemcpyAsync(kind == cudaMemcpyHostToDevice ? (void*)d : (void*)h,
+                      kind == cudaMemcpyHostToDevice ? (const void*)h : (const void*)d, len, kind, st) != cudaSuccess)
+    return set_err(FC2_ECUDA, "payload meta copy failed");
+  return FC2_OK;
+}
+
+// mode bit 1: x_host -> encode; 2: payload -> payload_host; 4: payload_host -> device;
+// 8: decode -> y_host
+static int host_pipeline(int mode, const fc2_config* cfg, const void* x_host, int32_t x_dtype, int64_t n,
+                         void* x_dev, void* pay_dev, void* y_dev, int32_t y_dtype, void* pay_host, void* y_host,
+                         int64_t slice, int32_t* dev_err, void* stream) {
+  int rc = check_cfg(cfg);
+  if (rc) return rc;
+  const int G = cfg->group_size;
+  if (n < 0 || n % G) return set_err(FC2_ECONFIG, "chunk %lld not a multiple of group_size %d", (long long)n, G);
+  if (n == 0) return FC2_OK;
+  if ((mode & 1) && (!x_host || !x_dev || !esize(x_dtype))) return set_err(FC2_ECONFIG, "encode needs x buffers");
+  if ((mode & 8) && (!y_host || !y_dev || !esize(y_dtype))) return set_err(FC2_ECONFIG, "decode needs y buffers");
+  if ((mode & 6) && !pay_host) return set_err(FC2_ECONFIG, "payload host buffer missing");
+  if (!pay_dev) return set_err(FC2_ECONFIG, "payload device buffer missing");
+  // slice: a multiple of every tile unit (encode <= 8192 elements or one
+  // group; decode 4096) and of the group size
+  int64_t unit = 32768;
+  while (unit % G) unit += 32768;
+  if (slice <= 0) slice = (int64_t)1 << 22;
+  slice = (slice + unit - 1) / unit * unit;
+  HostPipe* hp = host_pipe(&rc);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaEventRecord(hp->fork, st) != cudaSuccess) return set_err(FC2_ECUDA, "fork event failed");
+  for (int i = 0; i < kPipeStreams; ++i) cudaStreamWaitEvent(hp->s[i], hp->fork, 0);
+  const int xs = esize(x_dtype), ys = esize(y_dtype);
+  // uploads stream back to back on s[0] (never queued behind a download);
+  // slice k's kernels and downloads run on s[1 + k % 3] after its upload event
+  cudaStream_t up = hp->s[0];
+  int64_t k = 0;
+  for (int64_t e0 = 0; e0 < n; e0 += slice, ++k) {
+    const int64_t e1 = e0 + slice < n ? e0 + slice : n;
+    cudaStream_t s = hp->s[1 + k % (kPipeStreams - 1)];
+    if (mode & 5) {
+      if (mode & 1) {
+        if (cudaMemcpyAsync((uint8_t*)x_dev + e0 * xs, (const uint8_t*)x_host + e0 * xs, (e1 - e0) * xs,
+                            cudaMemcpyHostToDevice, up) != cudaSuccess)
+          return set_err(FC2_ECUDA, "x slice copy failed");
+      } else {
+        rc = copy_payload_slice(cfg, n, e0, e1, pay_dev, pay_host, cudaMemcpyHostToDevice, up);
+        if (rc) return rc;
+      }
+      cudaEvent_t ev = hp->up[k % kPipeEvents];
+      if (cudaEventRecord(ev, up) != cudaSuccess || cudaStreamWaitEvent(s, ev, 0) != cudaSuccess)
+        return set_err(FC2_ECUDA, "upload event failed");
+    }
+    if (mode & 1) {
+      rc = encode_batch_impl(cfg, x_dtype, 1, &x_dev, &n, &n, &pay_dev, dev_err, s, &e0, &e1);
+      if (rc) return rc;
+    }
+    if (mode & 2) {
+      rc = copy_payload_slice(cfg, n, e0, e1, pay_dev, pay_host, cudaMemcpyDeviceToHost, s);
+      if (rc) return rc;
+    }
+    if (mode & 8) {
+      const void* pd = pay_dev;
+      rc = decode_batch_impl(cfg, y_dtype, 1, &pd, &n, &y_dev, &n, dev_err, s, 0, &e0, &e1);
+      if (rc) return rc;
+      if (cudaMemcpyAsync((uint8_t*)y_host + e0 * ys, (const uint8_t*)y_dev + e0 * ys, (e1 - e0) * ys,
+                          cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        return set_err(FC2_ECUDA, "y slice copy failed");
+    }
+  }
+  for (int i = 0; i < kPipeStreams; ++i) {
+    cudaEventRecord(hp->join[i], hp->s[i]);
+    cudaStreamWaitEvent(st, hp->join[i], 0);
+  }
+  return cuda_check("host pipeline");
+}
+
+}  // namespace fc2
+
+extern "C" {
+
+int fc2_encode_host(const fc2_config* cfg, const void* x_host, int32_t x_dtype, int64_t n, void* x_dev,
+                    void* payload_dev, void* payload_host, int64_t slice, int32_t* dev_err, void* stream) {
+  return host_pipeline(1 | 2, cfg, x_host, x_dtype, n, x_dev, payload_dev, nullptr, 0, payload_host, nullptr, slice,
+                       dev_err, stream);
+}
+
+int fc2_decode_host(const fc2_config* cfg, const void* payload_host, int64_t n, void* payload_dev, void* y_dev,
+                    int32_t y_dtype, void* y_host, int64_t slice, int32_t* dev_err, void* stream) {
+  return host_pipeline(4 | 8, cfg, nullptr, 0, n, nullptr, payload_dev, y_dev, y_dtype,
+                       const_cast<void*>(payload_host), y_host, slice, dev_err, stream);
+}
+
+int fc2_roundtrip_host(const fc2_config* cfg, const void* x_host, int32_t x_dtype, int64_t n, void* x_dev,
+                       void* payload_dev, void* y_dev, int32_t y_dtype, void* payload_host, void* y_host,
+                       int64_t slice, int32_t* dev_err, void* stream) {
+  return host_pipeline(1 | (payload_host ? 2 : 0) | 8, cfg, x_host, x_dtype, n, x_dev, payload_dev, y_dev, y_dtype,
+                       payload_host, y_host, slice, dev_err, stream);
 }
 
 int fc2_gather_decode(const fc2_config* cfg, int32_t nshards, const void* const* shard_payloads, int64_t shard_len,

@@ -277,3 +277,47 @@ def test_intlog_helpers_match_reference(theta):
     assert fc.int_to_scale(-128) == 0.0
     with pytest.raises(fc.DataError):
         fc.scale_to_int(-1.0)
+
+
+@pytest.mark.parametrize("bits,sr,g,n,slice_elems", [
+    (4, True, 128, 1 << 20, 1 << 16),       # 16 slices over 4 streams
+    (3, False, 128, 3 * 32768 + 4096, 32768),  # ragged last slice, bit-split planes
+    (5, True, 64, 1 << 18, 1 << 22),        # one slice
+    (8, True, 256, 5 * 32768, 32768),
+    (6, False, 96, 96 * 1024, 32768),       # generic group size: slice rounded to lcm
+])
+def test_host_pipeline_matches_device_path(bits, sr, g, n, slice_elems):
+    """encode_host / decode_host / roundtrip_host (fc2_*_host: sliced, PCIe
+    overlapped) produce the same payload bytes and values as the device path
+    and as the oracle."""
+    cfg = cfg_of(bits, g, sr, False, n)
+    x = torch.from_numpy(O.bf16_snap(O.spiky(n, bits)).astype(np.float32)).to(torch.bfloat16)
+    xp = x.pin_memory()
+    want = fc.encode_payload(x.cuda(), cfg, n).cpu()
+    pay = fc.encode_host(xp, cfg, slice_elems=slice_elems)
+    assert torch.equal(pay, want)
+    y = fc.decode_host(pay, cfg, n, out_dtype=torch.float32, slice_elems=slice_elems)
+    ywant = fc.decode_payload(want.cuda(), cfg, n, out_dtype=torch.float32).cpu()
+    assert torch.equal(y, ywant)
+    pay2, y2 = fc.roundtrip_host(xp, cfg, out_dtype=torch.bfloat16, slice_elems=slice_elems)
+    assert torch.equal(pay2, want)
+    assert torch.equal(y2, ywant.to(torch.bfloat16))
+    # oracle on a prefix (groups are independent)
+    m = 8192 if n >= 8192 else n
+    m -= m % g
+    planes, meta = O.encode(x[:m].float().numpy(), bits, g, sr)
+    units = O.UNITS[bits]
+    off = 0
+    for w, p in zip(units, planes):
+        assert pay[off:off + m * w // 8].numpy().tobytes() == p
+        off += n * w // 8
+
+
+def test_host_pipeline_errors():
+    cfg = cfg_of(4, 128, True, False, 4096)
+    x = torch.zeros(4096, dtype=torch.float32)
+    x[7] = float("nan")
+    with pytest.raises(fc.DataError):
+        fc.encode_host(x.pin_memory(), cfg)
+    with pytest.raises(TypeError):
+        fc.encode_host(x.cuda(), cfg)
