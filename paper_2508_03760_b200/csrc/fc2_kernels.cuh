@@ -207,12 +207,26 @@ __device__ __forceinline__ void issue_grp_tile(const EncBatch& b, int64_t t, uin
   const int64_t e0 = (t - jb.t0) * GPT * G;
   const int lane = (int)lane_id();
   const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(jb.x);
+  constexpr int NJ = IT::CPG / LPG;  // 16-byte chunks per lane
   if (e0 + GPT * G <= jb.n_valid) {  // whole tile present: plain 16-byte copies
     const uint8_t* src = reinterpret_cast<const uint8_t*>(x + e0);
+    if constexpr (IT::CPG <= 32 && 32 % IT::CPG == 0 && NJ > 8) {
+      // chunk lane + 32 j: group g0 + K j, column c; the swizzle only sees
+      // (group & 7), so slots repeat every 8 j with a 256-chunk stride
+      constexpr int K = 32 / IT::CPG;
+      const int g0 = lane / IT::CPG, c = lane % IT::CPG;
+      int sb[8];
 #pragma unroll
-    for (int j = 0; j < IT::CPG / LPG; ++j) {
-      const int tc = lane + 32 * j;
-      cp_async16(stage + IT::in_pos(tc / IT::CPG, tc % IT::CPG) * 16, src + 16 * tc, 16);
+      for (int j = 0; j < 8; ++j) sb[j] = IT::in_pos(g0 + K * j, c) * 16;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+        cp_async16(stage + sb[j % 8] + (j / 8) * (8 * K * IT::CPG * 16), src + 16 * (lane + 32 * j), 16);
+    } else {
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const int tc = lane + 32 * j;
+        cp_async16(stage + IT::in_pos(tc / IT::CPG, tc % IT::CPG) * 16, src + 16 * tc, 16);
+      }
     }
   } else {  // tail tile: zero-fill past n_valid (the padding of collectives.py:167-172)
     const int64_t rem = jb.n_valid - e0;  // may be <= 0
