@@ -37,3 +37,9 @@ for _ in range(a.reps):
     fc.decode_payload(pay, cfg, n, out=y, err=err, check=False)
 torch.cuda.synchronize()
 print("err", int(err.item()))
+
+# two-step AllReduce per-rank kernels (8 shards of this tensor as 8 sources)
+from bench import two_step_stage_times  # noqa: E402
+
+two_step_stage_times(fc, x, cfg, flush, 1)
+torch.cuda.synchronize()
