@@ -475,7 +475,7 @@ struct DecIn {
 template <typename OT, int B>
 __global__ void __launch_bounds__(kDecWarps * 32) k_decode_fast(const __grid_constant__ DecBatch b) {
   constexpr int ESZ = (int)sizeof(OT);
-  constexpr int OUT_BYTES = kDecTile * ESZ;
+  constexpr int OUT_BYTES = kDecTile / 2 * ESZ;  // half a tile: runs (0,1) then (2,3) of every lane
   constexpr int PER_WARP = 2 * DecIn<B>::BYTES + OUT_BYTES;
   extern __shared__ __align__(16) uint8_t dsm[];
   const int warp = (int)(threadIdx.x >> 5), lane = (int)lane_id();
@@ -538,10 +538,10 @@ __global__ void __launch_bounds__(kDecWarps * 32) k_decode_fast(const __grid_con
     cp_async_commit();
     cp_async_wait<1>();
     __syncwarp();
-    if (live) {
-      constexpr int CPR = 32 * (int)sizeof(OT) / 16;  // output chunks per run
-      constexpr int CPLn = 4 * CPR;                    // output chunks per lane
-      GroupMeta m;
+    constexpr int CPR = 32 * (int)sizeof(OT) / 16;  // output chunks per run
+    constexpr int CPH = 2 * CPR;                     // output chunks per lane per half
+    GroupMeta m;
+    {
       auto decode_meta = [&]() {
         m.imin = m.imax = -1;
         m.smin = m.smax = 0.f;
@@ -573,32 +573,50 @@ __global__ void __launch_bounds__(kDecWarps * 32) k_decode_fast(const __grid_con
           }
         }
       };
-      // reserved values of the group that starts at element gs (if inside this lane's span)
-      auto patch_spikes = [&](int64_t gs) {
-        auto put = [&](int idx, float val) {
-          if (sizeof(OT) == 4 && b.round_bf16) val = bf16_val(bf16_bits(val));
-          const int64_t k = gs + idx - e0;  // lane-relative element
-          if (k >= 0 && k < kDecElems && gs + idx < jb.n) {
-            const int c = CPLn * lane + (int)k / (16 / (int)sizeof(OT));
-            *reinterpret_cast<OT*>(ost + 16 * (c ^ ((c >> 3) & 7)) + ((int)k % (16 / (int)sizeof(OT))) * (int)sizeof(OT)) =
-                cvt_out<OT>(val);
-          }
+      // Reserved values of the current group: lane-relative positions (0..127,
+      // else outside this lane's span) and their stage byte offsets, computed
+      // once per group; patch_spikes(h) writes those in half h (the half now in
+      // the stage), imin first, then imax (codec.py:559-561).
+      int kmin = -1, kmax = -1, omin = 0, omax = 0;
+      OT vmin{}, vmax{};
+      auto spike_pos = [&]() {
+        auto pos = [&](int idx, int& kk, int& off) {
+          const int64_t k = grp * G + idx - e0;
+          kk = (idx >= 0 && k >= 0 && k < kDecElems && grp * G + idx < jb.n) ? (int)k : -1;
+          const int kh = kk & (kDecElems / 2 - 1);
+          const int c = CPH * lane + kh / (16 / (int)sizeof(OT));
+          off = 16 * (c ^ ((c >> 3) & 7)) + (kh % (16 / (int)sizeof(OT))) * (int)sizeof(OT);
         };
-        if (m.imin >= 0) put(m.imin, m.smin);
-        if (m.imax >= 0) put(m.imax, m.smax);
+        pos(m.imin, kmin, omin);
+        pos(m.imax, kmax, omax);
+        float a = m.smin, z = m.smax;
+        if (sizeof(OT) == 4 && b.round_bf16) { a = bf16_val(bf16_bits(a)); z = bf16_val(bf16_bits(z)); }
+        vmin = cvt_out<OT>(a);
+        vmax = cvt_out<OT>(z);
       };
-      decode_meta();
+      auto patch_spikes = [&](int h) {
+        if (kmin >= 0 && (kmin >> 6) == h) *reinterpret_cast<OT*>(ost + omin) = vmin;
+        if (kmax >= 0 && (kmax >> 6) == h) *reinterpret_cast<OT*>(ost + omax) = vmax;
+      };
+      if (live) {
+        decode_meta();
+        if (b.sr) spike_pos();
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+      if (live) {
 #pragma unroll 1
-      for (int r = 0; r < 4; ++r) {
+      for (int r = 2 * h; r < 2 * h + 2; ++r) {
         const int64_t er = e0 + 32 * r;
         if (er >= jb.n) break;
         if (r > 0) gin += 32;
         if (gin >= G) {  // next group (G < 128): finish the previous one first
-          if (b.sr) patch_spikes(grp * G);
+          if (b.sr) patch_spikes(h);
           gin -= G;
           grp += 1;
           load_record(jb.pay + jb.n * B / 8 + grp * rb, rec, rb);
           decode_meta();
+          if (b.sr) spike_pos();
         }
         // ---- codes of this 32-element run from the stage
         RunRegs<B> rr;
@@ -662,8 +680,10 @@ __global__ void __launch_bounds__(kDecWarps * 32) k_decode_fast(const __grid_con
             for (int k = 0; k < 32; ++k) v[k] = bf16_val(bf16_bits(v[k]));
           }
         }
-        // ---- stage: this run's CPR chunks of the lane segment
-        const int cbase = CPLn * lane + CPR * r;
+        // ---- stage: this run's CPR chunks of the lane's half segment
+        // (CPH is a multiple of 8, so (c >> 3) & 7 only sees the lane and the
+        // chunk's 8-block: slot = c ^ sw)
+        const int cbase = CPH * lane + CPR * (r & 1);
 #pragma unroll
         for (int j = 0; j < CPR; ++j) {
           uint4 q;
@@ -682,27 +702,35 @@ __global__ void __launch_bounds__(kDecWarps * 32) k_decode_fast(const __grid_con
           *reinterpret_cast<uint4*>(ost + 16 * (c ^ ((c >> 3) & 7))) = q;
         }
       }
-      if (b.sr) patch_spikes(grp * G);
-    }
-    __syncwarp();
-    // ---- coalesced copy-out, bounded by n_out
-    OT* y = reinterpret_cast<OT*>(jb.y) + ebase;
-    const int64_t valid = jb.n_out - ebase;
-    constexpr int EPC = 16 / ESZ;
-    constexpr int NCH = kDecTile / EPC;
-    if (valid >= kDecTile && (reinterpret_cast<uintptr_t>(y) & 15u) == 0) {
-      // chunk c = lane + 32 i sits at slot c ^ ((c >> 3) & 7) = 32 i + (lane ^ s),
-      // s = ((lane >> 3) + 4 i) & 7 alternating with i: two base pointers
-      const uint8_t* s0 = ost + 16 * (lane ^ ((lane >> 3) & 7));
-      const uint8_t* s1 = ost + 16 * (lane ^ (((lane >> 3) + 4) & 7));
-      uint4* yd = reinterpret_cast<uint4*>(y) + lane;
+      if (b.sr) patch_spikes(h);
+      }
+      __syncwarp();
+      // ---- coalesced copy-out of half h, bounded by n_out: stage chunk q
+      // (lane q / CPH, chunk q % CPH of its half) -> elements
+      // 128 (q / CPH) + 64 h + EPC (q % CPH) of the tile; 32 consecutive q
+      // cover whole 128-byte segments
+      OT* y = reinterpret_cast<OT*>(jb.y) + ebase;
+      const int64_t valid = jb.n_out - ebase;
+      constexpr int EPC = 16 / ESZ;
+      constexpr int NCH = kDecTile / 2 / EPC;
+      if (valid >= kDecTile && (reinterpret_cast<uintptr_t>(y) & 15u) == 0) {
+        // q = lane + 32 i: lane q / CPH = lane / CPH + (32 / CPH) i, chunk q % CPH = lane % CPH;
+        // slot q ^ ((q >> 3) & 7) = 32 i + (lane ^ s_i), s_i = ((lane >> 3) + 4 i) & 7
+        OT* yl = y + kDecElems * (lane / CPH) + 64 * h + EPC * (lane % CPH);
+        const uint8_t* s0 = ost + 16 * (lane ^ ((lane >> 3) & 7));
+        const uint8_t* s1 = ost + 16 * (lane ^ (((lane >> 3) + 4) & 7));
 #pragma unroll
-      for (int i = 0; i < NCH / 32; ++i)
-        yd[32 * i] = *reinterpret_cast<const uint4*>((i & 1 ? s1 : s0) + 512 * i);
-    } else {
-      for (int i = lane; i < valid && i < kDecTile; i += 32) {
-        const int c = i / EPC;
-        y[i] = *reinterpret_cast<const OT*>(ost + 16 * (c ^ ((c >> 3) & 7)) + (i % EPC) * ESZ);
+        for (int i = 0; i < NCH / 32; ++i)
+          *reinterpret_cast<uint4*>(yl + (32 / CPH) * kDecElems * i) =
+              *reinterpret_cast<const uint4*>((i & 1 ? s1 : s0) + 512 * i);
+      } else {
+        for (int i = lane; i < kDecTile / 2; i += 32) {
+          const int q = i / EPC;
+          const int64_t e = kDecElems * (q / CPH) + 64 * h + EPC * (q % CPH) + i % EPC;
+          if (e < valid) y[e] = *reinterpret_cast<const OT*>(ost + 16 * (q ^ ((q >> 3) & 7)) + (i % EPC) * ESZ);
+        }
+      }
+      __syncwarp();
       }
     }
     __syncwarp();
@@ -713,7 +741,7 @@ __global__ void __launch_bounds__(kDecWarps * 32) k_decode_fast(const __grid_con
 
 template <typename OT, int B>
 int launch_decode_fast(const DecBatch& b, cudaStream_t st) {
-  constexpr int SMEM = kDecWarps * (2 * DecIn<B>::BYTES + kDecTile * (int)sizeof(OT));
+  constexpr int SMEM = kDecWarps * (2 * DecIn<B>::BYTES + kDecTile / 2 * (int)sizeof(OT));
   auto kern = k_decode_fast<OT, B>;
   static bool attr = false;
   if (!attr) {
