@@ -453,6 +453,10 @@ __device__ __forceinline__ uint32_t code_of(const RunRegs<B>& rr, int k) {
 constexpr int kDecWarps = 4;
 constexpr int kDecElems = 128;            // elements per lane (4 runs of 32)
 constexpr int kDecTile = 32 * kDecElems;  // elements per warp tile
+#ifndef FC2_DEC_STAGES
+#define FC2_DEC_STAGES 1  // the launch gives every warp one tile: a second input stage would sit idle
+#endif
+constexpr int kDecStages = FC2_DEC_STAGES;
 
 template <int B>
 struct DecIn {
@@ -476,11 +480,11 @@ template <typename OT, int B>
 __global__ void __launch_bounds__(kDecWarps * 32) k_decode_fast(const __grid_constant__ DecBatch b) {
   constexpr int ESZ = (int)sizeof(OT);
   constexpr int OUT_BYTES = kDecTile / 2 * ESZ;  // half a tile: runs (0,1) then (2,3) of every lane
-  constexpr int PER_WARP = 2 * DecIn<B>::BYTES + OUT_BYTES;
+  constexpr int PER_WARP = kDecStages * DecIn<B>::BYTES + OUT_BYTES;
   extern __shared__ __align__(16) uint8_t dsm[];
   const int warp = (int)(threadIdx.x >> 5), lane = (int)lane_id();
   uint8_t* in0 = dsm + warp * PER_WARP;
-  uint8_t* ost = in0 + 2 * DecIn<B>::BYTES;
+  uint8_t* ost = in0 + kDecStages * DecIn<B>::BYTES;
   const int64_t nw = (int64_t)gridDim.x * kDecWarps;
   const int rb = rec_bytes(b.sr, b.intlog);
   const int G = b.G;
@@ -534,9 +538,13 @@ __global__ void __launch_bounds__(kDecWarps * 32) k_decode_fast(const __grid_con
     int gin = (int)(e0 - grp * G);
     const bool live = e0 < jb.n;
     if (live) load_record(jb.pay + jb.n * B / 8 + grp * rb, rec, rb);
-    issue(t + nw, in0 + (stage ^ 1) * DecIn<B>::BYTES);
-    cp_async_commit();
-    cp_async_wait<1>();
+    if constexpr (kDecStages == 2) {  // prefetch this warp's next tile (grids that loop)
+      issue(t + nw, in0 + (stage ^ 1) * DecIn<B>::BYTES);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
     __syncwarp();
     constexpr int CPR = 32 * (int)sizeof(OT) / 16;  // output chunks per run
     constexpr int CPH = 2 * CPR;                     // output chunks per lane per half
@@ -734,14 +742,19 @@ __global__ void __launch_bounds__(kDecWarps * 32) k_decode_fast(const __grid_con
       }
     }
     __syncwarp();
-    stage ^= 1;
+    if constexpr (kDecStages == 2) {
+      stage ^= 1;
+    } else if (t + nw < b.total) {  // single stage: refill it for the next tile
+      issue(t + nw, in0);
+      cp_async_commit();
+    }
   }
   cp_async_wait<0>();
 }
 
 template <typename OT, int B>
 int launch_decode_fast(const DecBatch& b, cudaStream_t st) {
-  constexpr int SMEM = kDecWarps * (2 * DecIn<B>::BYTES + kDecTile / 2 * (int)sizeof(OT));
+  constexpr int SMEM = kDecWarps * (kDecStages * DecIn<B>::BYTES + kDecTile / 2 * (int)sizeof(OT));
   auto kern = k_decode_fast<OT, B>;
   static bool attr = false;
   if (!attr) {
