@@ -133,6 +133,66 @@ __device__ __forceinline__ void copy_out(const uint8_t* base, uint8_t* dst, int 
   }
 }
 
+// ---- direct output (FC2_ENC_DIRECT): plane words straight from registers ----
+
+#ifndef FC2_ENC_DIRECT
+#define FC2_ENC_DIRECT 1
+#endif
+
+// NW consecutive 32-bit words to global with the widest stores the (warp-
+// uniform) alignment allows; a lane's pair of runs of a 4- or 8-bit plane is a
+// whole number of 32-byte sectors
+template <int NW>
+__device__ __forceinline__ void store_words_g(uint8_t* p, const uint32_t* w) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  if constexpr (NW % 8 == 0) {
+    if ((a & 31u) == 0) {
+#pragma unroll
+      for (int i = 0; i < NW; i += 8)
+        asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p + 4 * i), "r"(w[i]),
+                     "r"(w[i + 1]), "r"(w[i + 2]), "r"(w[i + 3]), "r"(w[i + 4]), "r"(w[i + 5]), "r"(w[i + 6]),
+                     "r"(w[i + 7])
+                     : "memory");
+      return;
+    }
+  }
+  if constexpr (NW % 4 == 0) {
+    if ((a & 15u) == 0) {
+#pragma unroll
+      for (int i = 0; i < NW; i += 4)
+        *reinterpret_cast<uint4*>(p + 4 * i) = make_uint4(w[i], w[i + 1], w[i + 2], w[i + 3]);
+      return;
+    }
+  }
+  if constexpr (NW % 2 == 0) {
+    if ((a & 7u) == 0) {
+#pragma unroll
+      for (int i = 0; i < NW; i += 2) *reinterpret_cast<uint2*>(p + 4 * i) = make_uint2(w[i], w[i + 1]);
+      return;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NW; ++i) *reinterpret_cast<uint32_t*>(p + 4 * i) = w[i];
+}
+
+// patch element e of absolute group ga in the payload (global) with code c:
+// XOR the difference into the 32-bit word holding it (atomics: other lanes
+// patch other elements of the same word concurrently)
+template <int B, int G>
+__device__ __forceinline__ void payload_patch_xor(uint8_t* out, int64_t n, int64_t ga, int e, int c) {
+#pragma unroll
+  for (int u = 0; u < n_units(B); ++u) {
+    const int W = unit_w(B, u), O = unit_off(B, u);
+    const int bit = e * W;
+    const int64_t byte = n * O / 8 + ga * (G * W / 8) + (bit >> 3);
+    unsigned int* wp = reinterpret_cast<unsigned int*>(out + (byte & ~(int64_t)3));
+    const int sh = (int)(byte & 3) * 8 + (bit & 7);
+    const uint32_t m = (1u << W) - 1u;
+    const uint32_t cur = (atomicOr(wp, 0u) >> sh) & m, want = ((uint32_t)c >> O) & m;
+    if (cur != want) atomicXor(wp, (cur ^ want) << sh);
+  }
+}
+
 // ---- per-chunk helpers on 16-byte chunks -----------------------------------
 
 struct TopState {  // packed bf16x2 running statistics (two independent streams)
@@ -233,18 +293,23 @@ __device__ __forceinline__ void pack_run_fb16(const uint32_t (&X)[32], uint32_t 
 #endif
 template <int B, bool SR, int G, int MODE, int LPG>
 __device__ __forceinline__ void quant_runs(const uint8_t* ist, uint8_t* ost, uint32_t* tms, const GroupParams& p,
-                                           float Lh, bool active) {
+                                           float Lh, bool active, uint8_t* out, int64_t n, int64_t g_abs) {
   using IT = GTile<__nv_bfloat16, G, LPG>;
   constexpr int GPT = 32 / LPG;
   constexpr int RUNS = G / 32 / LPG;  // runs of this lane
+  constexpr int PAIR = RUNS >= 2 ? 2 : 1;
   const int gl = (int)lane_id() / LPG, r0 = ((int)lane_id() % LPG) * RUNS;
   constexpr int FB = FixFor<B>::FB;
   using FX = Fix<FB>;
   constexpr int L = (1 << B) - 1;
   // FB = 16 folded form: one FFMA, y = fma(v, inv, nz + kCM) (bound: Fix<16>)
   const float c16 = __fadd_rn(p.nz, FX::kCM);
-#pragma unroll 2
-  for (int rr = 0; rr < RUNS; ++rr) {
+#pragma unroll 1
+  for (int rp = 0; rp < RUNS; rp += PAIR) {
+  uint32_t pw[PAIR][B];  // plane words of the pair's runs (LaneWords layout)
+#pragma unroll
+  for (int q = 0; q < PAIR; ++q) {
+    const int rr = rp + q;
     const int r = r0 + rr;  // run index inside the group
     LaneWords<B> lw;
     lw.clear();
@@ -293,20 +358,25 @@ __device__ __forceinline__ void quant_runs(const uint8_t* ist, uint8_t* ost, uin
     // fits its width and no masking is needed when the unit is the whole code
     if constexpr (FB == 16) pack_run_fb16<B, SR && MODE != 2 && !FC2_SPIKE_STANDIN>(XR, lw.w);
 #pragma unroll
-    for (int u = 0; u < n_units(B); ++u) {
-      const int W = unit_w(B, u);
-      uint8_t* base = ost + OutStage<B, G, GPT>::off(u);
-      const uint32_t* w = lw.w + LaneWords<B>::base(u);
-      if (W == 1) stage_words<G, 1>(base, gl, r, w);
-      else if (W == 2) stage_words<G, 2>(base, gl, r, w);
-      else if (W == 4) stage_words<G, 4>(base, gl, r, w);
-      else stage_words<G, 8>(base, gl, r, w);
+    for (int i = 0; i < B; ++i) pw[q][i] = lw.w[i];
+    if (!FC2_ENC_DIRECT) {
+#pragma unroll
+      for (int u = 0; u < n_units(B); ++u) {
+        const int W = unit_w(B, u);
+        uint8_t* base = ost + OutStage<B, G, GPT>::off(u);
+        const uint32_t* w = lw.w + LaneWords<B>::base(u);
+        if (W == 1) stage_words<G, 1>(base, gl, r, w);
+        else if (W == 2) stage_words<G, 2>(base, gl, r, w);
+        else if (W == 4) stage_words<G, 4>(base, gl, r, w);
+        else stage_words<G, 8>(base, gl, r, w);
+      }
     }
     // near-tie masks of this run, resolved after all runs (one divergent
     // pass per tile instead of one per run)
 #if FC2_TIE_DEFER
     tms[32 * rr + (int)lane_id()] = tmj[0] | tmj[1];
 #else
+    static_assert(!FC2_ENC_DIRECT, "direct output needs the deferred tie fix-up");
     uint32_t tm = (p.exact ? 0xffffffffu : (tmj[0] | tmj[1])) & (active ? 0xffffffffu : 0u);
     while (tm) {
       const int k = __ffs(tm) - 1;
@@ -317,6 +387,23 @@ __device__ __forceinline__ void quant_runs(const uint8_t* ist, uint8_t* ost, uin
       stage_patch<B, G, GPT>(ost, gl, e, exact_code((double)v, p.off, p.div, (1 << B) - 1));
     }
 #endif
+  }
+  if (FC2_ENC_DIRECT && active) {  // the pair's bytes of every unit: [4W (r0 + rp), +4W PAIR) of the group
+#pragma unroll
+    for (int u = 0; u < n_units(B); ++u) {
+      const int W = unit_w(B, u), O = unit_off(B, u);
+      uint32_t w[PAIR * 8];
+#pragma unroll
+      for (int q = 0; q < PAIR; ++q)
+#pragma unroll
+        for (int i = 0; i < W; ++i) w[q * W + i] = pw[q][O + i];
+      uint8_t* dst = out + n * O / 8 + g_abs * (G * W / 8) + (r0 + rp) * 4 * W;
+      if (W == 1) store_words_g<PAIR * 1>(dst, w);
+      else if (W == 2) store_words_g<PAIR * 2>(dst, w);
+      else if (W == 4) store_words_g<PAIR * 4>(dst, w);
+      else store_words_g<PAIR * 8>(dst, w);
+    }
+  }
   }
 }
 
@@ -353,7 +440,8 @@ __device__ __forceinline__ void stage_patch_xor(uint8_t* ost, int g, int e, int 
 // every element (p.exact) loop on their own.
 template <int B, int G, int LPG>
 __device__ __forceinline__ void resolve_ties_coop(const uint8_t* ist, uint8_t* ost, uint32_t* tms,
-                                                  const GroupParams& p, bool active) {
+                                                  const GroupParams& p, bool active, uint8_t* out, int64_t n,
+                                                  int64_t tile_g0) {
   using IT = GTile<__nv_bfloat16, G, LPG>;
   constexpr int GPT = 32 / LPG;
   constexpr int RUNS = G / 32 / LPG;
@@ -400,7 +488,11 @@ __device__ __forceinline__ void resolve_ties_coop(const uint8_t* ist, uint8_t* o
         const uint32_t ent = i < total ? tms[i] : 0u;
         const int src = (int)(ent >> 16), e = (int)(ent & 0xFFFFu);
         const double off = __shfl_sync(0xffffffffu, p.off, src), div = __shfl_sync(0xffffffffu, p.div, src);
-        if (i < total) stage_patch_xor<B, G, GPT>(ost, src / LPG, e, exact_code(value(src / LPG, e), off, div, L));
+        if (i < total) {
+          const int c = exact_code(value(src / LPG, e), off, div, L);
+          if (FC2_ENC_DIRECT) payload_patch_xor<B, G>(out, n, tile_g0 + src / LPG, e, c);
+          else stage_patch_xor<B, G, GPT>(ost, src / LPG, e, c);
+        }
       }
     } else {  // many ties in one tile (rare): each lane resolves its own
 #pragma unroll 1
@@ -412,15 +504,20 @@ __device__ __forceinline__ void resolve_ties_coop(const uint8_t* ist, uint8_t* o
           const int k = __ffs(t) - 1;
           t &= t - 1;
           const int e = 32 * (r0 + rr) + (k < 16 ? 2 * k : 2 * (k - 16) + 1);
-          stage_patch_xor<B, G, GPT>(ost, gl, e, exact_code(value(gl, e), p.off, p.div, L));
+          const int c = exact_code(value(gl, e), p.off, p.div, L);
+          if (FC2_ENC_DIRECT) payload_patch_xor<B, G>(out, n, tile_g0 + gl, e, c);
+          else stage_patch_xor<B, G, GPT>(ost, gl, e, c);
         }
       }
     }
   }
   if (active && p.exact) {  // every element of the group in float64
 #pragma unroll 1
-    for (int e = r0 * 32; e < (r0 + RUNS) * 32; ++e)
-      stage_patch_xor<B, G, GPT>(ost, gl, e, exact_code(value(gl, e), p.off, p.div, L));
+    for (int e = r0 * 32; e < (r0 + RUNS) * 32; ++e) {
+      const int c = exact_code(value(gl, e), p.off, p.div, L);
+      if (FC2_ENC_DIRECT) payload_patch_xor<B, G>(out, n, tile_g0 + gl, e, c);
+      else stage_patch_xor<B, G, GPT>(ost, gl, e, c);
+    }
   }
   __syncwarp();
 }
@@ -593,13 +690,16 @@ __device__ __forceinline__ void encode_tile_bf16(uint8_t* ist, uint8_t* ost, uin
     if constexpr (LPG > 1) __syncwarp();
   }
   if (cx.intlog) {
-    quant_runs<B, SR, G, 2, LPG>(ist, ost, tms, p, Lh, active);
+    quant_runs<B, SR, G, 2, LPG>(ist, ost, tms, p, Lh, active, out, cx.n, g_abs);
   } else if (__all_sync(0xffffffffu, fold_ok || p.exact || !active)) {
-    quant_runs<B, SR, G, 0, LPG>(ist, ost, tms, p, Lh, active);
+    quant_runs<B, SR, G, 0, LPG>(ist, ost, tms, p, Lh, active, out, cx.n, g_abs);
   } else {
-    quant_runs<B, SR, G, 1, LPG>(ist, ost, tms, p, Lh, active);
+    quant_runs<B, SR, G, 1, LPG>(ist, ost, tms, p, Lh, active, out, cx.n, g_abs);
   }
-  if (FC2_TIE_DEFER) resolve_ties_coop<B, G, LPG>(ist, ost, tms, p, active);
+  if (FC2_TIE_DEFER) {
+    if (FC2_ENC_DIRECT) __syncwarp();  // plane stores of all lanes before the patches read them
+    resolve_ties_coop<B, G, LPG>(ist, ost, tms, p, active, out, cx.n, tile_g0);
+  }
   if constexpr (SR && !FC2_SPIKE_STANDIN) {  // reserved slots are quantized as 0.0 (codec.py:494-496)
     int sc;
     const uint32_t Xs = fixq_clamped<FB>(0.0f, p.off32, p.inv32, (float)L + 0.5f);
@@ -637,7 +737,8 @@ __device__ __forceinline__ void encode_tile_bf16(uint8_t* ist, uint8_t* ost, uin
     store_record(out + cx.meta_off + g_abs * rb, rec, rb);
   }
   __syncwarp();
-  // ---- coalesced copy-out of the plane segments ---------------------------
+  // ---- coalesced copy-out of the plane segments (staged output only) -------
+  if (!FC2_ENC_DIRECT)
 #pragma unroll
   for (int u = 0; u < n_units(B); ++u) {
     const int W = unit_w(B, u), O = unit_off(B, u);

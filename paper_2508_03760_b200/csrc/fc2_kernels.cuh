@@ -242,7 +242,7 @@ __device__ __forceinline__ void issue_grp_tile(const EncBatch& b, int64_t t, uin
 }
 
 #ifndef FC2_ENC_MINB
-#define FC2_ENC_MINB 5  // 5 CTAs of 4 warps per SM: <= 102 registers (smem allows 5)
+#define FC2_ENC_MINB 6  // 6 CTAs of 4 warps per SM: <= 85 registers (direct output: 8.5 KB smem per warp)
 #endif
 template <int B, bool SR, int G, int WARPS, int LPG, int STAGES>
 __global__ void __launch_bounds__(WARPS * 32, FC2_ENC_MINB) k_encode_grp(const __grid_constant__ EncBatch b) {
@@ -250,12 +250,13 @@ __global__ void __launch_bounds__(WARPS * 32, FC2_ENC_MINB) k_encode_grp(const _
   constexpr int GPT = 32 / LPG;                       // groups per warp tile
   constexpr int IN_BYTES = IT::IN_BYTES / LPG;
   constexpr int TIE_BYTES = G / LPG * 4;               // one 32-bit tie mask per run per lane
-  constexpr int PER_WARP = STAGES * IN_BYTES + OutStage<B, G, GPT>::BYTES + TIE_BYTES;
+  constexpr int OUT_BYTES = FC2_ENC_DIRECT ? 0 : OutStage<B, G, GPT>::BYTES;  // direct output: no stage
+  constexpr int PER_WARP = STAGES * IN_BYTES + OUT_BYTES + TIE_BYTES;
   extern __shared__ __align__(16) uint8_t smem[];
   const int warp = (int)(threadIdx.x >> 5), lane = (int)lane_id();
   uint8_t* in0 = smem + warp * PER_WARP;
   uint8_t* ost = in0 + STAGES * IN_BYTES;
-  uint32_t* tms = reinterpret_cast<uint32_t*>(ost + OutStage<B, G, GPT>::BYTES);
+  uint32_t* tms = reinterpret_cast<uint32_t*>(ost + OUT_BYTES);
   const int64_t nw = (int64_t)gridDim.x * WARPS;
   int64_t t = (int64_t)blockIdx.x * WARPS + warp;
   if constexpr (STAGES == 2) {
@@ -311,7 +312,8 @@ struct EncGrp {
   static constexpr int WARPS = FC2_ENC_WARPS;
   static constexpr int STAGES = FC2_ENC_STAGES;
   static constexpr int SMEM =
-      WARPS * (STAGES * GTile<__nv_bfloat16, G>::IN_BYTES / LPG + OutStage<B, G, 32 / LPG>::BYTES + G / LPG * 4);
+      WARPS * (STAGES * GTile<__nv_bfloat16, G>::IN_BYTES / LPG + (FC2_ENC_DIRECT ? 0 : OutStage<B, G, 32 / LPG>::BYTES) +
+               G / LPG * 4);
   static int go(const EncBatch& b, cudaStream_t st) {
     auto kern = k_encode_grp<B, SR, G, WARPS, LPG, STAGES>;
     static bool attr = false;
