@@ -35,6 +35,28 @@ struct GTile {
       return g * CPG + (c ^ ((g >> (CPG == 4 ? 1 : (CPG == 2 ? 2 : 3))) & IM));
     }
   }
+  // The chunks a lane reads are 4 r + j (run r of its group, j < 4) and the
+  // XOR key of in_pos is constant per lane (the part index c / (CPG / LPG) is
+  // the lane's own), so in_pos(g, 4 r + j) = g CPG + (4 r ^ (s & 4)) + (j ^ (s & 3)):
+  // one base per run plus four per-lane offsets.
+  struct Lane {
+    const uint8_t* A;  // group base
+    int s4;            // key bit 2 (flips the run's chunk block)
+    int s3;            // key bits 0-1, pre-scaled: byte offset of chunk j = (16 j) ^ s3
+    __device__ __forceinline__ Lane(const uint8_t* ist, int g, int li) {
+      int sk;
+      if constexpr (CPG >= 8) sk = (g * LPG + li) & 7;
+      else sk = (g >> (CPG == 4 ? 1 : (CPG == 2 ? 2 : 3))) & IM;
+      A = ist + 16 * g * CPG;
+      s4 = sk & 4;
+      s3 = 16 * (sk & 3);
+    }
+    __device__ __forceinline__ int jx(int j) const { return (16 * j) ^ s3; }
+    __device__ __forceinline__ const uint8_t* run(int r) const { return A + 16 * ((4 * r) ^ s4); }
+    __device__ __forceinline__ const uint8_t* chunk(int c) const { return run(c >> 2) + jx(c & 3); }
+    // element e (group-relative, inside this lane's runs)
+    __device__ __forceinline__ const uint8_t* elem(int e) const { return chunk(e >> 3) + 2 * (e & 7); }
+  };
 };
 
 // output staging for one unit of width W: the tile's plane segment
@@ -175,9 +197,8 @@ __device__ __forceinline__ void store_words_g(uint8_t* p, const uint32_t* w) {
   for (int i = 0; i < NW; ++i) *reinterpret_cast<uint32_t*>(p + 4 * i) = w[i];
 }
 
-// patch element e of absolute group ga in the payload (global) with code c:
-// XOR the difference into the 32-bit word holding it (atomics: other lanes
-// patch other elements of the same word concurrently)
+// patch element e of absolute group ga in the payload (global) with code c
+// (other lanes patch other elements of the same 32-bit word concurrently)
 template <int B, int G>
 __device__ __forceinline__ void payload_patch_xor(uint8_t* out, int64_t n, int64_t ga, int e, int c) {
 #pragma unroll
@@ -187,9 +208,11 @@ __device__ __forceinline__ void payload_patch_xor(uint8_t* out, int64_t n, int64
     const int64_t byte = n * O / 8 + ga * (G * W / 8) + (bit >> 3);
     unsigned int* wp = reinterpret_cast<unsigned int*>(out + (byte & ~(int64_t)3));
     const int sh = (int)(byte & 3) * 8 + (bit & 7);
-    const uint32_t m = (1u << W) - 1u;
-    const uint32_t cur = (atomicOr(wp, 0u) >> sh) & m, want = ((uint32_t)c >> O) & m;
-    if (cur != want) atomicXor(wp, (cur ^ want) << sh);
+    const uint32_t m = (1u << W) - 1u, want = ((uint32_t)c >> O) & m;
+    // clear then set this element's bits: two fire-and-forget reductions
+    // (same thread, same address: ordered), commuting with other lanes' patches
+    asm volatile("red.global.and.b32 [%0], %1;" ::"l"(wp), "r"(~(m << sh)) : "memory");
+    asm volatile("red.global.or.b32 [%0], %1;" ::"l"(wp), "r"(want << sh) : "memory");
   }
 }
 
@@ -304,6 +327,7 @@ __device__ __forceinline__ void quant_runs(const uint8_t* ist, uint8_t* ost, uin
   constexpr int L = (1 << B) - 1;
   // FB = 16 folded form: one FFMA, y = fma(v, inv, nz + kCM) (bound: Fix<16>)
   const float c16 = __fadd_rn(p.nz, FX::kCM);
+  const typename IT::Lane la(ist, gl, (int)lane_id() % LPG);
 #pragma unroll 1
   for (int rp = 0; rp < RUNS; rp += PAIR) {
   uint32_t pw[PAIR][B];  // plane words of the pair's runs (LaneWords layout)
@@ -311,6 +335,7 @@ __device__ __forceinline__ void quant_runs(const uint8_t* ist, uint8_t* ost, uin
   for (int q = 0; q < PAIR; ++q) {
     const int rr = rp + q;
     const int r = r0 + rr;  // run index inside the group
+    const uint8_t* rb = la.run(r);
     LaneWords<B> lw;
     lw.clear();
     uint32_t tmj[2] = {0u, 0u};  // two accumulators: shorter dependency chains
@@ -318,7 +343,7 @@ __device__ __forceinline__ void quant_runs(const uint8_t* ist, uint8_t* ost, uin
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       uint32_t& tm = tmj[j & 1];
-      const uint4 q = *reinterpret_cast<const uint4*>(ist + IT::in_pos(gl, 4 * r + j) * 16);
+      const uint4 q = *reinterpret_cast<const uint4*>(rb + la.jx(j));
       const uint32_t ww[4] = {q.x, q.y, q.z, q.w};
       uint32_t X[8];
 #pragma unroll
@@ -383,7 +408,7 @@ __device__ __forceinline__ void quant_runs(const uint8_t* ist, uint8_t* ost, uin
       tm &= tm - 1;
       const int e = 32 * r + (k < 16 ? 2 * k : 2 * (k - 16) + 1);
       const float v = __uint_as_float(
-          (uint32_t)*reinterpret_cast<const uint16_t*>(ist + IT::in_pos(gl, e >> 3) * 16 + (e & 7) * 2) << 16);
+          (uint32_t)*reinterpret_cast<const uint16_t*>(la.elem(e)) << 16);
       stage_patch<B, G, GPT>(ost, gl, e, exact_code((double)v, p.off, p.div, (1 << B) - 1));
     }
 #endif
@@ -537,7 +562,8 @@ __device__ __forceinline__ void encode_tile_bf16(uint8_t* ist, uint8_t* ost, uin
   const int gl = lane / LPG, li = lane % LPG;   // group of the tile, part of the group
   constexpr int RUNS = G / 32 / LPG;            // 32-element runs of this lane
   const int r0 = li * RUNS;                     // first run (group-relative)
-  auto chunk = [&](int c) -> uint4 { return *reinterpret_cast<const uint4*>(ist + IT::in_pos(gl, c) * 16); };
+  const typename IT::Lane la(ist, gl, li);
+  auto chunk = [&](int c) -> uint4 { return *reinterpret_cast<const uint4*>(la.chunk(c)); };
 
   constexpr int FB = FixFor<B>::FB;
   using FX = Fix<FB>;
@@ -659,7 +685,7 @@ __device__ __forceinline__ void encode_tile_bf16(uint8_t* ist, uint8_t* ost, uin
     imin = fi; imax = fa;
     // reserved values are the elements themselves (codec.py:492-493)
     auto elem = [&](int e) -> uint32_t {
-      return *reinterpret_cast<const uint16_t*>(ist + IT::in_pos(gl, e >> 3) * 16 + (e & 7) * 2);
+      return *reinterpret_cast<const uint16_t*>(la.elem(e));
     };
     smin_bits = elem(imin);
     smax_bits = elem(imax);
@@ -683,9 +709,9 @@ __device__ __forceinline__ void encode_tile_bf16(uint8_t* ist, uint8_t* ost, uin
                                   : (zf > 0.f ? __float_as_uint(zf) >> 16 : (vf < 0.f ? __float_as_uint(vf) >> 16 : 0u));
     if (active) {
       if (imin / (G / LPG) == li)
-        *reinterpret_cast<uint16_t*>(ist + IT::in_pos(gl, imin >> 3) * 16 + (imin & 7) * 2) = (uint16_t)sv;
+        *reinterpret_cast<uint16_t*>(const_cast<uint8_t*>(la.elem(imin))) = (uint16_t)sv;
       if (imax / (G / LPG) == li)
-        *reinterpret_cast<uint16_t*>(ist + IT::in_pos(gl, imax >> 3) * 16 + (imax & 7) * 2) = (uint16_t)sv;
+        *reinterpret_cast<uint16_t*>(const_cast<uint8_t*>(la.elem(imax))) = (uint16_t)sv;
     }
     if constexpr (LPG > 1) __syncwarp();
   }
