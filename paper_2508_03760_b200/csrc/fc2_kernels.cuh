@@ -243,10 +243,11 @@ __device__ __forceinline__ void issue_grp_tile(const EncBatch& b, int64_t t, uin
 
 #ifndef FC2_ENC_MINB
 #define FC2_ENC_MINB 6  // 6 CTAs of 4 warps per SM: <= 85 registers (direct output: 8.5 KB smem per warp);
-                        // one fewer at B = 7 (three planes: 14 live plane words per run pair)
+                        // fewer at B = 8 (16 plane words per run pair) and B = 7 (three planes)
 #endif
 template <int B, bool SR, int G, int WARPS, int LPG, int STAGES>
-__global__ void __launch_bounds__(WARPS * 32, B == 7 ? FC2_ENC_MINB - 1 : FC2_ENC_MINB) k_encode_grp(const __grid_constant__ EncBatch b) {
+__global__ void __launch_bounds__(WARPS * 32, B == 7 ? FC2_ENC_MINB - 2 : (B == 8 ? FC2_ENC_MINB - 1 : FC2_ENC_MINB))
+    k_encode_grp(const __grid_constant__ EncBatch b) {
   using IT = GTile<__nv_bfloat16, G, LPG>;
   constexpr int GPT = 32 / LPG;                       // groups per warp tile
   constexpr int IN_BYTES = IT::IN_BYTES / LPG;
