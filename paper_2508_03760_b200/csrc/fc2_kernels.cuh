@@ -241,13 +241,17 @@ __device__ __forceinline__ void issue_grp_tile(const EncBatch& b, int64_t t, uin
   }
 }
 
-#ifndef FC2_ENC_MINB
-#define FC2_ENC_MINB 6  // 6 CTAs of 4 warps per SM: <= 85 registers (direct output: 8.5 KB smem per warp);
-                        // fewer at B = 8 (16 plane words per run pair) and B = 7 (three planes)
+// Register budget per thread of the lane-per-group encoder: 85 lets 24 warps
+// (8.5 KB of smem each with direct output) share an SM; B = 8 (16 plane words
+// per run pair) and B = 7 (three planes) need more to stay spill-free.
+#ifndef FC2_ENC_REGS
+#define FC2_ENC_REGS 85
 #endif
+__host__ __device__ constexpr int enc_min_ctas(int B, int warps) {
+  return 65536 / (warps * 32 * (B == 7 ? 128 : (B == 8 ? 102 : FC2_ENC_REGS)));
+}
 template <int B, bool SR, int G, int WARPS, int LPG, int STAGES>
-__global__ void __launch_bounds__(WARPS * 32, B == 7 ? FC2_ENC_MINB - 2 : (B == 8 ? FC2_ENC_MINB - 1 : FC2_ENC_MINB))
-    k_encode_grp(const __grid_constant__ EncBatch b) {
+__global__ void __launch_bounds__(WARPS * 32, enc_min_ctas(B, WARPS)) k_encode_grp(const __grid_constant__ EncBatch b) {
   using IT = GTile<__nv_bfloat16, G, LPG>;
   constexpr int GPT = 32 / LPG;                       // groups per warp tile
   constexpr int IN_BYTES = IT::IN_BYTES / LPG;
@@ -302,7 +306,7 @@ __global__ void __launch_bounds__(WARPS * 32, B == 7 ? FC2_ENC_MINB - 2 : (B == 
 #define FC2_ENC_STAGES 1
 #endif
 #ifndef FC2_ENC_WARPS
-#define FC2_ENC_WARPS 4
+#define FC2_ENC_WARPS 1  // one-warp CTAs: finest block-scheduling grain for the last wave
 #endif
 #ifndef FC2_ENC_CTAS_PER_SM
 #define FC2_ENC_CTAS_PER_SM 64
