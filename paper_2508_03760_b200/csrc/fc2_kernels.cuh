@@ -458,7 +458,10 @@ __device__ __forceinline__ uint32_t code_of(const RunRegs<B>& rr, int k) {
 // XOR-swizzled per-lane words); the lane's metadata record(s) come straight
 // from global (one record per lane when G >= 128); values are staged in smem
 // and written back with coalesced 16-byte stores.  Requires G % 32 == 0.
-constexpr int kDecWarps = 4;
+#ifndef FC2_DEC_WARPS
+#define FC2_DEC_WARPS 1  // one-warp CTAs (28 resident per SM by registers; finest tail grain)
+#endif
+constexpr int kDecWarps = FC2_DEC_WARPS;
 constexpr int kDecElems = 128;            // elements per lane (4 runs of 32)
 constexpr int kDecTile = 32 * kDecElems;  // elements per warp tile
 #ifndef FC2_DEC_STAGES
