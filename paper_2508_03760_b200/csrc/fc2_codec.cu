@@ -510,7 +510,10 @@ int fc2_decode(const fc2_config* cfg, const void* payload, int64_t n, void* y, i
 
 namespace fc2 {
 
-constexpr int kPipeStreams = 4;  // s[0]: uploads; s[1..3]: kernels + downloads, round robin
+#ifndef FC2_PIPE_STREAMS
+#define FC2_PIPE_STREAMS 4
+#endif
+constexpr int kPipeStreams = FC2_PIPE_STREAMS;  // s[0]: uploads; s[1..]: kernels + downloads, round robin
 constexpr int kPipeEvents = 8;
 struct HostPipe {
   cudaStream_t s[kPipeStreams];
