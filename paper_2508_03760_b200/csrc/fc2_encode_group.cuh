@@ -1,19 +1,23 @@
 // fc2_encode_group.cuh -- lane-per-group encoder (the production fast path).
 //
-// A warp tile is 32 consecutive groups; lane l owns group l of the tile
-// entirely, so every per-group step (statistics, spike search, scale/zero,
-// metadata, tie resolution) runs once per G elements with no shuffles.
+// A warp tile is 32 consecutive groups (32 / LPG at g = 256); lane l owns
+// group l of the tile, so every per-group step (statistics, spike search,
+// scale/zero, metadata) runs once per G elements with no shuffles.
 //
-//   global --cp.async--> input stage (swizzled 16-byte chunks, 2 stages)
-//   pass 1  stats       packed bf16x2 min/max (top-2 for spike reserving)
-//   pass 2  spikes      first argmin / argmax via packed equality masks
-//   pass 3  codes       fp32x2 fixed-point estimate -> packed plane words ->
-//                       output stage (smem); near-tie elements recomputed in
-//                       float64 and patched in smem; spike slots patched
-//   copy-out            coalesced 16-byte stores of each plane segment,
-//                       metadata records straight from the owning lane
+//   global --cp.async--> input stage (swizzled 16-byte chunks, one per warp)
+//   pass 1  stats       packed bf16x2 min/max per 32-element run
+//   pass 2  spikes      first argmin / argmax via packed equality masks (only
+//                       the run holding each extreme is searched); in-range
+//                       stand-ins written over the two reserved slots
+//   pass 3  codes       fp32x2 fixed-point estimate -> byte-gathered plane
+//                       words -> 256-bit stores straight to the payload, one
+//                       per run pair; near-tie masks left in smem
+//   ties                the warp compacts all near-tie elements into one list,
+//                       recomputes them in float64 (32 per round) and patches
+//                       the payload words with red.and / red.or
+//   metadata            one record per group from the owning lane
 //
-// Contract: SURVEY 8.0 R1-R11/R13 (codec.py:477-519), same as encode_lane.
+// Contract: SURVEY 8.0 R1-R11/R13 (codec.py:477-519).
 #pragma once
 
 #include "fc2_encode.cuh"
@@ -155,11 +159,7 @@ __device__ __forceinline__ void copy_out(const uint8_t* base, uint8_t* dst, int 
   }
 }
 
-// ---- direct output (FC2_ENC_DIRECT): plane words straight from registers ----
-
-#ifndef FC2_ENC_DIRECT
-#define FC2_ENC_DIRECT 1
-#endif
+// ---- direct output: plane words straight from registers ----------------------
 
 // NW consecutive 32-bit words to global with the widest stores the (warp-
 // uniform) alignment allows; a lane's pair of runs of a 4- or 8-bit plane is a
@@ -218,55 +218,6 @@ __device__ __forceinline__ void payload_patch_xor(uint8_t* out, int64_t n, int64
 
 // ---- per-chunk helpers on 16-byte chunks -----------------------------------
 
-struct TopState {  // packed bf16x2 running statistics (two independent streams)
-  __nv_bfloat162 a1, a2, b1, b2;
-};
-
-__device__ __forceinline__ void top_init(TopState& s, uint32_t w0) {
-  s.a1 = *reinterpret_cast<const __nv_bfloat162*>(&w0);
-  s.b1 = s.a1;
-  const uint32_t pinf = 0x7F807F80u, ninf = 0xFF80FF80u;
-  s.a2 = *reinterpret_cast<const __nv_bfloat162*>(&pinf);
-  s.b2 = *reinterpret_cast<const __nv_bfloat162*>(&ninf);
-}
-
-template <bool SR>
-__device__ __forceinline__ void top_add(TopState& s, uint32_t w) {
-  const __nv_bfloat162 x = *reinterpret_cast<const __nv_bfloat162*>(&w);
-  if constexpr (SR) {
-    s.a2 = __hmin2_nan(s.a2, __hmax2_nan(s.a1, x));
-    s.b2 = __hmax2_nan(s.b2, __hmin2_nan(s.b1, x));
-  }
-  s.a1 = __hmin2_nan(s.a1, x);
-  s.b1 = __hmax2_nan(s.b1, x);
-}
-
-// merge two independent top-2 states (multiset union)
-template <bool SR>
-__device__ __forceinline__ void top_merge(TopState& s, const TopState& o) {
-  if constexpr (SR) {
-    s.a2 = __hmin2_nan(__hmax2_nan(s.a1, o.a1), __hmin2_nan(s.a2, o.a2));
-    s.b2 = __hmax2_nan(__hmin2_nan(s.b1, o.b1), __hmax2_nan(s.b2, o.b2));
-  }
-  s.a1 = __hmin2_nan(s.a1, o.a1);
-  s.b1 = __hmax2_nan(s.b1, o.b1);
-}
-
-template <bool SR>
-__device__ __forceinline__ void top_final(const TopState& s, float& mn1, float& mn2, float& mx1, float& mx2) {
-  float l1 = __low2float(s.a1), h1 = __high2float(s.a1);
-  mn1 = fmin_nan(l1, h1);
-  float L1 = __low2float(s.b1), H1 = __high2float(s.b1);
-  mx1 = fmax_nan(L1, H1);
-  if constexpr (SR) {
-    mn2 = fmin_nan(fmax_nan(l1, h1), fmin_nan(__low2float(s.a2), __high2float(s.a2)));
-    mx2 = fmax_nan(fmin_nan(L1, H1), fmax_nan(__low2float(s.b2), __high2float(s.b2)));
-  } else {
-    mn2 = mn1;
-    mx2 = mx1;
-  }
-}
-
 // Pack the 32 codes of a run into plane words (LaneWords layout: unit-major,
 // word t of a W-bit unit holds codes [32t/W, 32(t+1)/W) LSB-first).  FB = 16
 // puts each code in byte 2 of its fixed-point word, so four codes are
@@ -308,23 +259,15 @@ __device__ __forceinline__ void pack_run_fb16(const uint32_t (&X)[32], uint32_t 
 // Writes packed words into the output stage; near-tie elements (split-layout
 // tie masks: bit i < 16 element 2i, bit 16 + i element 2i + 1) are recomputed
 // exactly and patched in the stage.
-#ifndef FC2_TIE_DEFER
-#define FC2_TIE_DEFER 1  // 1: warp-cooperative tie resolution after pass 3; 0: per run, per lane
-#endif
-#ifndef FC2_SPIKE_STANDIN
-#define FC2_SPIKE_STANDIN 1
-#endif
 template <int B, bool SR, int G, int MODE, int LPG>
-__device__ __forceinline__ void quant_runs(const uint8_t* ist, uint8_t* ost, uint32_t* tms, const GroupParams& p,
-                                           float Lh, bool active, uint8_t* out, int64_t n, int64_t g_abs) {
+__device__ __forceinline__ void quant_runs(const uint8_t* ist, uint32_t* tms, const GroupParams& p, float Lh,
+                                           bool active, uint8_t* out, int64_t n, int64_t g_abs) {
   using IT = GTile<__nv_bfloat16, G, LPG>;
-  constexpr int GPT = 32 / LPG;
   constexpr int RUNS = G / 32 / LPG;  // runs of this lane
   constexpr int PAIR = RUNS >= 2 ? 2 : 1;
   const int gl = (int)lane_id() / LPG, r0 = ((int)lane_id() % LPG) * RUNS;
   constexpr int FB = FixFor<B>::FB;
   using FX = Fix<FB>;
-  constexpr int L = (1 << B) - 1;
   // FB = 16 folded form: one FFMA, y = fma(v, inv, nz + kCM) (bound: Fix<16>)
   const float c16 = __fadd_rn(p.nz, FX::kCM);
   const typename IT::Lane la(ist, gl, (int)lane_id() % LPG);
@@ -381,39 +324,14 @@ __device__ __forceinline__ void quant_runs(const uint8_t* ist, uint8_t* ost, uin
     }
     // spike slots hold an in-range stand-in (encode_tile_bf16), so every code
     // fits its width and no masking is needed when the unit is the whole code
-    if constexpr (FB == 16) pack_run_fb16<B, SR && MODE != 2 && !FC2_SPIKE_STANDIN>(XR, lw.w);
+    if constexpr (FB == 16) pack_run_fb16<B, false>(XR, lw.w);
 #pragma unroll
     for (int i = 0; i < B; ++i) pw[q][i] = lw.w[i];
-    if (!FC2_ENC_DIRECT) {
-#pragma unroll
-      for (int u = 0; u < n_units(B); ++u) {
-        const int W = unit_w(B, u);
-        uint8_t* base = ost + OutStage<B, G, GPT>::off(u);
-        const uint32_t* w = lw.w + LaneWords<B>::base(u);
-        if (W == 1) stage_words<G, 1>(base, gl, r, w);
-        else if (W == 2) stage_words<G, 2>(base, gl, r, w);
-        else if (W == 4) stage_words<G, 4>(base, gl, r, w);
-        else stage_words<G, 8>(base, gl, r, w);
-      }
-    }
     // near-tie masks of this run, resolved after all runs (one divergent
     // pass per tile instead of one per run)
-#if FC2_TIE_DEFER
     tms[32 * rr + (int)lane_id()] = tmj[0] | tmj[1];
-#else
-    static_assert(!FC2_ENC_DIRECT, "direct output needs the deferred tie fix-up");
-    uint32_t tm = (p.exact ? 0xffffffffu : (tmj[0] | tmj[1])) & (active ? 0xffffffffu : 0u);
-    while (tm) {
-      const int k = __ffs(tm) - 1;
-      tm &= tm - 1;
-      const int e = 32 * r + (k < 16 ? 2 * k : 2 * (k - 16) + 1);
-      const float v = __uint_as_float(
-          (uint32_t)*reinterpret_cast<const uint16_t*>(la.elem(e)) << 16);
-      stage_patch<B, G, GPT>(ost, gl, e, exact_code((double)v, p.off, p.div, (1 << B) - 1));
-    }
-#endif
   }
-  if (FC2_ENC_DIRECT && active) {  // the pair's bytes of every unit: [4W (r0 + rp), +4W PAIR) of the group
+  if (active) {  // the pair's bytes of every unit: [4W (r0 + rp), +4W PAIR) of the group
 #pragma unroll
     for (int u = 0; u < n_units(B); ++u) {
       const int W = unit_w(B, u), O = unit_off(B, u);
@@ -432,29 +350,6 @@ __device__ __forceinline__ void quant_runs(const uint8_t* ist, uint8_t* ost, uin
   }
 }
 
-// patch element e of group g with code c in the output stage by XOR-ing the
-// difference into its 32-bit word: several lanes may patch elements that share
-// a word concurrently (cooperative tie resolution), and each only flips its
-// own bits, which no other lane touches
-template <int B, int G, int GPT = 32>
-__device__ __forceinline__ void stage_patch_xor(uint8_t* ost, int g, int e, int c) {
-#pragma unroll
-  for (int u = 0; u < n_units(B); ++u) {
-    const int W = unit_w(B, u), O = unit_off(B, u);
-    const int bit = e * W;
-    int bp;
-    if (W == 1) bp = OutStage<B, G, GPT>::off(u) + OTile<G, 1>::byte_pos(g, bit >> 3);
-    else if (W == 2) bp = OutStage<B, G, GPT>::off(u) + OTile<G, 2>::byte_pos(g, bit >> 3);
-    else if (W == 4) bp = OutStage<B, G, GPT>::off(u) + OTile<G, 4>::byte_pos(g, bit >> 3);
-    else bp = OutStage<B, G, GPT>::off(u) + OTile<G, 8>::byte_pos(g, bit >> 3);
-    uint32_t* wp = reinterpret_cast<uint32_t*>(ost + (bp & ~3));
-    const int sh = (bp & 3) * 8 + (bit & 7);
-    const uint32_t m = (1u << W) - 1u;
-    const uint32_t cur = (*wp >> sh) & m, want = ((uint32_t)c >> O) & m;
-    if (cur != want) atomicXor(wp, (cur ^ want) << sh);
-  }
-}
-
 // Exact float64 recompute of the near-tie elements of the tile, done by the
 // whole warp: every lane's tie masks (one per run, left in smem by pass 3:
 // bit i < 16 -> element 2i, bit 16 + i -> element 2i + 1) are compacted into
@@ -464,11 +359,9 @@ __device__ __forceinline__ void stage_patch_xor(uint8_t* ost, int g, int e, int 
 // tile instead of one divergent pass per run.  Groups that need float64 for
 // every element (p.exact) loop on their own.
 template <int B, int G, int LPG>
-__device__ __forceinline__ void resolve_ties_coop(const uint8_t* ist, uint8_t* ost, uint32_t* tms,
-                                                  const GroupParams& p, bool active, uint8_t* out, int64_t n,
-                                                  int64_t tile_g0) {
+__device__ __forceinline__ void resolve_ties_coop(const uint8_t* ist, uint32_t* tms, const GroupParams& p,
+                                                  bool active, uint8_t* out, int64_t n, int64_t tile_g0) {
   using IT = GTile<__nv_bfloat16, G, LPG>;
-  constexpr int GPT = 32 / LPG;
   constexpr int RUNS = G / 32 / LPG;
   constexpr int L = (1 << B) - 1;
   constexpr int CAP = RUNS * 32;  // list entries that fit in the mask area
@@ -515,8 +408,7 @@ __device__ __forceinline__ void resolve_ties_coop(const uint8_t* ist, uint8_t* o
         const double off = __shfl_sync(0xffffffffu, p.off, src), div = __shfl_sync(0xffffffffu, p.div, src);
         if (i < total) {
           const int c = exact_code(value(src / LPG, e), off, div, L);
-          if (FC2_ENC_DIRECT) payload_patch_xor<B, G>(out, n, tile_g0 + src / LPG, e, c);
-          else stage_patch_xor<B, G, GPT>(ost, src / LPG, e, c);
+          payload_patch_xor<B, G>(out, n, tile_g0 + src / LPG, e, c);
         }
       }
     } else {  // many ties in one tile (rare): each lane resolves its own
@@ -530,8 +422,7 @@ __device__ __forceinline__ void resolve_ties_coop(const uint8_t* ist, uint8_t* o
           t &= t - 1;
           const int e = 32 * (r0 + rr) + (k < 16 ? 2 * k : 2 * (k - 16) + 1);
           const int c = exact_code(value(gl, e), p.off, p.div, L);
-          if (FC2_ENC_DIRECT) payload_patch_xor<B, G>(out, n, tile_g0 + gl, e, c);
-          else stage_patch_xor<B, G, GPT>(ost, gl, e, c);
+          payload_patch_xor<B, G>(out, n, tile_g0 + gl, e, c);
         }
       }
     }
@@ -540,8 +431,7 @@ __device__ __forceinline__ void resolve_ties_coop(const uint8_t* ist, uint8_t* o
 #pragma unroll 1
     for (int e = r0 * 32; e < (r0 + RUNS) * 32; ++e) {
       const int c = exact_code(value(gl, e), p.off, p.div, L);
-      if (FC2_ENC_DIRECT) payload_patch_xor<B, G>(out, n, tile_g0 + gl, e, c);
-      else stage_patch_xor<B, G, GPT>(ost, gl, e, c);
+      payload_patch_xor<B, G>(out, n, tile_g0 + gl, e, c);
     }
   }
   __syncwarp();
@@ -552,11 +442,10 @@ __device__ __forceinline__ void resolve_ties_coop(const uint8_t* ist, uint8_t* o
 // ---------------------------------------------------------------------------
 
 template <int B, bool SR, int G, int LPG>
-__device__ __forceinline__ void encode_tile_bf16(uint8_t* ist, uint8_t* ost, uint32_t* tms, bool active,
+__device__ __forceinline__ void encode_tile_bf16(uint8_t* ist, uint32_t* tms, bool active,
                                                  int64_t g_abs, const EncCtx& cx, uint8_t* out, int64_t tile_g0,
                                                  int ng) {
   using IT = GTile<__nv_bfloat16, G, LPG>;
-  constexpr int GPT = 32 / LPG;
   constexpr int L = (1 << B) - 1;
   const int lane = (int)lane_id();
   const int gl = lane / LPG, li = lane % LPG;   // group of the tile, part of the group
@@ -698,7 +587,7 @@ __device__ __forceinline__ void encode_tile_bf16(uint8_t* ist, uint8_t* ost, uin
   // 0: folded fma form, 1: explicit (v - off) form, 2: INT_LOG (clamped)
   const bool fold_ok = !p.exact && fabsf(p.nz) <= FX::kFold;
   const float Lh = (float)L + 0.5f;
-  if constexpr (SR && FC2_SPIKE_STANDIN) {
+  if constexpr (SR) {
     // Reserved slots are quantized as 0.0 (codec.py:494-496).  0.0 may lie
     // outside [zero, vmax] and then clips to code 0 (below) or L (above);
     // the in-range bf16 stand-in with the same code is written over both
@@ -716,26 +605,14 @@ __device__ __forceinline__ void encode_tile_bf16(uint8_t* ist, uint8_t* ost, uin
     if constexpr (LPG > 1) __syncwarp();
   }
   if (cx.intlog) {
-    quant_runs<B, SR, G, 2, LPG>(ist, ost, tms, p, Lh, active, out, cx.n, g_abs);
+    quant_runs<B, SR, G, 2, LPG>(ist, tms, p, Lh, active, out, cx.n, g_abs);
   } else if (__all_sync(0xffffffffu, fold_ok || p.exact || !active)) {
-    quant_runs<B, SR, G, 0, LPG>(ist, ost, tms, p, Lh, active, out, cx.n, g_abs);
+    quant_runs<B, SR, G, 0, LPG>(ist, tms, p, Lh, active, out, cx.n, g_abs);
   } else {
-    quant_runs<B, SR, G, 1, LPG>(ist, ost, tms, p, Lh, active, out, cx.n, g_abs);
+    quant_runs<B, SR, G, 1, LPG>(ist, tms, p, Lh, active, out, cx.n, g_abs);
   }
-  if (FC2_TIE_DEFER) {
-    if (FC2_ENC_DIRECT) __syncwarp();  // plane stores of all lanes before the patches read them
-    resolve_ties_coop<B, G, LPG>(ist, ost, tms, p, active, out, cx.n, tile_g0);
-  }
-  if constexpr (SR && !FC2_SPIKE_STANDIN) {  // reserved slots are quantized as 0.0 (codec.py:494-496)
-    int sc;
-    const uint32_t Xs = fixq_clamped<FB>(0.0f, p.off32, p.inv32, (float)L + 0.5f);
-    if (p.exact || (Xs & FX::kTie) == 0u) sc = exact_code(0.0, p.off, p.div, L);
-    else sc = (int)((Xs >> FB) & (uint32_t)L);
-    if (active) {  // the lane owning the element patches it
-      if (imin / (G / LPG) == li) stage_patch<B, G, GPT>(ost, gl, imin, sc);
-      if (imax / (G / LPG) == li) stage_patch<B, G, GPT>(ost, gl, imax, sc);
-    }
-  }
+  __syncwarp();  // plane stores of all lanes before the tie fix-ups modify them
+  resolve_ties_coop<B, G, LPG>(ist, tms, p, active, out, cx.n, tile_g0);
 
   // ---- metadata record (R10), straight from the group's first lane ---------
   if (active && li == 0) {
@@ -763,18 +640,6 @@ __device__ __forceinline__ void encode_tile_bf16(uint8_t* ist, uint8_t* ost, uin
     store_record(out + cx.meta_off + g_abs * rb, rec, rb);
   }
   __syncwarp();
-  // ---- coalesced copy-out of the plane segments (staged output only) -------
-  if (!FC2_ENC_DIRECT)
-#pragma unroll
-  for (int u = 0; u < n_units(B); ++u) {
-    const int W = unit_w(B, u), O = unit_off(B, u);
-    const uint8_t* base = ost + OutStage<B, G, GPT>::off(u);
-    uint8_t* dst = out + (cx.n * O) / 8 + tile_g0 * (G * W / 8);
-    if (W == 1) copy_out<G, 1, GPT>(base, dst, ng);
-    else if (W == 2) copy_out<G, 2, GPT>(base, dst, ng);
-    else if (W == 4) copy_out<G, 4, GPT>(base, dst, ng);
-    else copy_out<G, 8, GPT>(base, dst, ng);
-  }
   __syncwarp();
 }
 

@@ -256,13 +256,11 @@ __global__ void __launch_bounds__(WARPS * 32, enc_min_ctas(B, WARPS)) k_encode_g
   constexpr int GPT = 32 / LPG;                       // groups per warp tile
   constexpr int IN_BYTES = IT::IN_BYTES / LPG;
   constexpr int TIE_BYTES = G / LPG * 4;               // one 32-bit tie mask per run per lane
-  constexpr int OUT_BYTES = FC2_ENC_DIRECT ? 0 : OutStage<B, G, GPT>::BYTES;  // direct output: no stage
-  constexpr int PER_WARP = STAGES * IN_BYTES + OUT_BYTES + TIE_BYTES;
+  constexpr int PER_WARP = STAGES * IN_BYTES + TIE_BYTES;  // plane words go straight to global
   extern __shared__ __align__(16) uint8_t smem[];
   const int warp = (int)(threadIdx.x >> 5), lane = (int)lane_id();
   uint8_t* in0 = smem + warp * PER_WARP;
-  uint8_t* ost = in0 + STAGES * IN_BYTES;
-  uint32_t* tms = reinterpret_cast<uint32_t*>(ost + OUT_BYTES);
+  uint32_t* tms = reinterpret_cast<uint32_t*>(in0 + STAGES * IN_BYTES);
   const int64_t nw = (int64_t)gridDim.x * WARPS;
   int64_t t = (int64_t)blockIdx.x * WARPS + warp;
   if constexpr (STAGES == 2) {
@@ -296,7 +294,7 @@ __global__ void __launch_bounds__(WARPS * 32, enc_min_ctas(B, WARPS)) k_encode_g
     cx.theta = b.theta;
     cx.lut = b.lut;
     cx.err = b.err;
-    encode_tile_bf16<B, SR, G, LPG>(in0 + stage * IN_BYTES, ost, tms, gabs < ngroups, gabs, cx, jb.out, tg0, ng);
+    encode_tile_bf16<B, SR, G, LPG>(in0 + stage * IN_BYTES, tms, gabs < ngroups, gabs, cx, jb.out, tg0, ng);
     if constexpr (STAGES == 2) stage ^= 1;
   }
   cp_async_wait<0>();
@@ -318,8 +316,7 @@ struct EncGrp {
   static constexpr int WARPS = FC2_ENC_WARPS;
   static constexpr int STAGES = FC2_ENC_STAGES;
   static constexpr int SMEM =
-      WARPS * (STAGES * GTile<__nv_bfloat16, G>::IN_BYTES / LPG + (FC2_ENC_DIRECT ? 0 : OutStage<B, G, 32 / LPG>::BYTES) +
-               G / LPG * 4);
+      WARPS * (STAGES * GTile<__nv_bfloat16, G>::IN_BYTES / LPG + G / LPG * 4);
   static int go(const EncBatch& b, cudaStream_t st) {
     auto kern = k_encode_grp<B, SR, G, WARPS, LPG, STAGES>;
     static bool attr = false;
@@ -510,7 +507,6 @@ __global__ void __launch_bounds__(kDecWarps * 32) k_decode_fast(const __grid_con
       const int W = unit_w(B, u), O = unit_off(B, u);
       const uint8_t* src = jb.pay + (jb.n * O) / 8 + e0 * W / 8;
       const int64_t avail = (jb.n - e0) * W / 8;  // bytes of this plane left in the chunk
-      const int total = kDecTile * W / 8;         // 512 * W bytes = 32 * W chunks
       const bool full = avail >= 512 * W;
 #pragma unroll
       for (int k = 0; k < W; ++k) {
