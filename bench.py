@@ -337,6 +337,21 @@ def run_codec(args):
     # on one GPU: stage-2 reduce+requant of one 4 Mi-element shard from 8
     # packed sources, and the final gather-decode of 8 shards to bf16
     stages = two_step_stage_times(fc, x, cfg, flush, max(3, args.steps // 2))
+    # message-size sweep of the codec round trip (BASELINE configs[4] sizes,
+    # 64 KB .. 1 GB of bf16 per call), same cfg, L2 flushed before each step
+    size_sweep = {}
+    if not args.no_sweep:
+        for nb in (1 << 16, 1 << 20, 1 << 24, 1 << 26, 1 << 28, 1 << 30):
+            m = nb // 2
+            xs = x[:m] if m <= n else spiky_bf16(m, 7, dev)
+            e, d, Fm, _, _ = time_roundtrip(fc, xs, cfg, max(3, args.steps // 2), 2, flush)
+            te, td = statistics.mean(e), statistics.mean(d)
+            size_sweep[f"{nb >> 10}KiB" if nb < (1 << 20) else f"{nb >> 20}MiB"] = {
+                "encode_us": round(te * 1e3, 2), "decode_us": round(td * 1e3, 2),
+                "roundtrip_GBps": round(2 * m / ((te + td) * 1e-3) / 1e9, 1),
+                "encode_hbm_GBps": round((2 * m + Fm) / (te * 1e-3) / 1e9, 1),
+                "decode_hbm_GBps": round((Fm + 2 * m) / (td * 1e-3) / 1e9, 1)}
+            del xs
     # end to end through host buffers
     x_host = x.cpu().pin_memory()
     e2e_ms, h2d, d2h = time_e2e(fc, x_host, cfg, max(3, args.steps), 2)
@@ -374,6 +389,7 @@ def run_codec(args):
                       f"(numpy restatement of codec.py), {cpu_dt:.2f} s per round trip"},
         "sweep": sweep,
         "two_step_n8_per_rank_kernels": stages,
+        "size_sweep": size_sweep,
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
