@@ -338,11 +338,11 @@ namespace fc2 {
 // Encode tile granularity of a job (elements): the unit a sub-range launch
 // must start on.  Fast bf16: one warp tile of 32 / LPG groups; fast f32: 1024;
 // generic: one group.
-static int64_t enc_unit(const fc2_config* cfg, int32_t x_dtype, const void* x, int64_t n_valid) {
+static int64_t enc_unit(const fc2_config* cfg, int32_t x_dtype, const void* x, int64_t n_valid, int lpg) {
   const int G = cfg->group_size;
   const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15u) == 0 || n_valid == 0;
   if (!(fast_group(G) && x_dtype != FC2_F64 && aligned)) return G;
-  return x_dtype == FC2_BF16 ? 32 / enc_lpg(G) * (int64_t)G : 1024;
+  return x_dtype == FC2_BF16 ? 32 / lpg * (int64_t)G : 1024;
 }
 
 // e_begin / e_end (nullable): encode only elements [e_begin, e_end) of each
@@ -362,10 +362,16 @@ static int encode_batch_impl(const fc2_config* cfg, int32_t x_dtype, int32_t njo
   const int B = cfg->bitwidth, G = cfg->group_size;
   const bool sr = cfg->scheme == 1;
   const int esz = x_dtype == FC2_BF16 ? 2 : (x_dtype == FC2_F32 ? 4 : 8);
+  // shape of the bf16 lane-per-group encoder: bandwidth tiles, or one run
+  // per lane when the whole launch is smaller than a wave of them
+  int64_t elems = 0;
+  for (int i = 0; i < njobs; ++i)
+    elems += (e_end ? e_end[i] : n[i]) - (e_begin ? e_begin[i] : 0);
+  const int lpg = elems < (int64_t)FC2_ENC_SMALL_TILES * (32 / enc_lpg(G)) * G ? enc_lpg_small(G) : enc_lpg(G);
   EncBatch fast, gen;
   for (EncBatch* b : {&fast, &gen}) {
     b->nj = 0; b->B = B; b->G = G; b->sr = sr; b->intlog = cfg->scale_encoding; b->theta = cfg->theta;
-    b->total = 0; b->lut = lut; b->err = dev_err;
+    b->lpg = lpg; b->total = 0; b->lut = lut; b->err = dev_err;
   }
   for (int i = 0; i < njobs; ++i) {
     if (n[i] < 0 || n[i] % G) return set_err(FC2_ECONFIG, "chunk %lld not a multiple of group_size %d", (long long)n[i], G);
@@ -381,7 +387,7 @@ static int encode_batch_impl(const fc2_config* cfg, int32_t x_dtype, int32_t njo
     j.n_valid = n_valid[i];
     j.n = n[i];
     // fast tiles: bf16 -> 32 / LPG groups per warp tile; f32 -> 1024 elements; generic: groups
-    const int64_t tile = enc_unit(cfg, x_dtype, xs[i], n_valid[i]);
+    const int64_t tile = enc_unit(cfg, x_dtype, xs[i], n_valid[i], lpg);
     const int64_t eb = e_begin ? e_begin[i] : 0, ee = e_end ? e_end[i] : n[i];
     if (eb % tile || eb < 0 || ee > n[i] || ee < eb)
       return set_err(FC2_ECONFIG, "encode range [%lld, %lld) not on a %lld-element boundary", (long long)eb,

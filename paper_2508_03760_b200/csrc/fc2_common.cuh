@@ -282,6 +282,13 @@ __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 #define FC2_ENC_EPL 128
 #endif
 __host__ __device__ constexpr int enc_lpg(int G) { return G > FC2_ENC_EPL ? G / FC2_ENC_EPL : 1; }
+// small chunks (less than one resident wave of bandwidth tiles): one 32-element
+// run per lane, so each warp's serial work (and the launch's latency) shrinks
+// by G / 32 at the cost of a few shuffles per group
+__host__ __device__ constexpr int enc_lpg_small(int G) { return G / 32 > 0 ? G / 32 : 1; }
+#ifndef FC2_ENC_SMALL_TILES
+#define FC2_ENC_SMALL_TILES 1776  // bandwidth tiles below which the small-chunk shape is used (148 SMs x 12)
+#endif
 
 // store nbytes (<= 12) from words[]; widest stores the alignment allows
 __device__ __forceinline__ void store_record(uint8_t* p, const uint32_t* w, int nbytes) {

@@ -574,7 +574,9 @@ __device__ __forceinline__ void encode_tile_bf16(uint8_t* ist, uint32_t* tms, bo
     imin = fi; imax = fa;
     // reserved values are the elements themselves (codec.py:492-493)
     auto elem = [&](int e) -> uint32_t {
-      return *reinterpret_cast<const uint16_t*>(la.elem(e));
+      // (any lane of the group reads them: the element may sit in another
+      // lane's part, so the swizzle key is the chunk's, not this lane's)
+      return *reinterpret_cast<const uint16_t*>(ist + IT::in_pos(gl, e >> 3) * 16 + (e & 7) * 2);
     };
     smin_bits = elem(imin);
     smax_bits = elem(imax);

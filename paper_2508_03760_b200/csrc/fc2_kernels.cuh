@@ -28,6 +28,7 @@ struct EncJob {
 };
 struct EncBatch {
   int nj, B, G, sr, intlog, theta;
+  int lpg;  // lanes per group of the bf16 lane-per-group encoder (enc_lpg / enc_lpg_small)
   int64_t total;
   const double* lut;
   int32_t* err;
@@ -312,12 +313,17 @@ __global__ void __launch_bounds__(WARPS * 32, enc_min_ctas(B, WARPS)) k_encode_g
 
 template <int B, bool SR, int G>
 struct EncGrp {
-  static constexpr int LPG = enc_lpg(G);  // lanes per group
   static constexpr int WARPS = FC2_ENC_WARPS;
   static constexpr int STAGES = FC2_ENC_STAGES;
-  static constexpr int SMEM =
-      WARPS * (STAGES * GTile<__nv_bfloat16, G>::IN_BYTES / LPG + G / LPG * 4);
+  // the launcher picked b.lpg: enc_lpg(G) for bandwidth, enc_lpg_small(G)
+  // (one 32-element run per lane) when the chunk is smaller than a wave
   static int go(const EncBatch& b, cudaStream_t st) {
+    if (b.lpg == enc_lpg_small(G) && enc_lpg_small(G) != enc_lpg(G)) return run<enc_lpg_small(G)>(b, st);
+    return run<enc_lpg(G)>(b, st);
+  }
+  template <int LPG>
+  static int run(const EncBatch& b, cudaStream_t st) {
+    constexpr int SMEM = WARPS * (STAGES * GTile<__nv_bfloat16, G>::IN_BYTES / LPG + G / LPG * 4);
     auto kern = k_encode_grp<B, SR, G, WARPS, LPG, STAGES>;
     static bool attr = false;
     if (!attr) {

@@ -90,6 +90,46 @@ def test_codec_matches_oracle_random(bits, sr, g, kind):
     assert np.array_equal(fc.decode_chunk(chunk), O.decode(planes, meta, n, bits, g, sr))
 
 
+@pytest.mark.parametrize("bits", range(2, 9))
+@pytest.mark.parametrize("sr", [False, True])
+@pytest.mark.parametrize("g", [32, 64, 128, 256])
+@pytest.mark.parametrize("kind", ["spiky", "ties"])
+def test_codec_bf16_device_matches_oracle(bits, sr, g, kind):
+    """The bf16 lane-per-group encoder (k_encode_grp) in its small-chunk
+    shape (one 32-element run per lane) against the oracle, every g."""
+    n = g * 1024
+    x = O.bf16_snap(INPUTS[kind](n, bits * 7 + g)).astype(np.float32)
+    cfg = cfg_of(bits, g, sr, False, n)
+    chunk = fc.encode_chunk(torch.from_numpy(x).cuda().to(torch.bfloat16), cfg)
+    planes, meta = O.encode(x, bits, g, sr)
+    assert bytes(chunk.payload.cpu().numpy()) == b"".join(planes) + meta
+    dec = fc.decode_payload(chunk.payload, cfg, n, out_dtype=torch.float32).cpu().numpy()
+    assert np.array_equal(dec, O.decode(planes, meta, n, bits, g, sr).astype(np.float32))
+
+
+@pytest.mark.parametrize("bits", [2, 3, 4, 5, 7, 8])
+@pytest.mark.parametrize("sr", [False, True])
+@pytest.mark.parametrize("g", [32, 64, 128, 256])
+def test_codec_bf16_bandwidth_shape_slices(bits, sr, g):
+    """The same encoder in its bandwidth shape (chunks of >= one resident
+    wave of tiles): slices of the payload equal the oracle on the same
+    element slices (groups are independent)."""
+    n = 1 << 23
+    x = torch.from_numpy(O.bf16_snap(O.spiky(n, bits + g)).astype(np.float32)).to(torch.bfloat16)
+    cfg = cfg_of(bits, g, sr, False, n)
+    ph = fc.encode_payload(x.cuda(), cfg, n).cpu().numpy()
+    xs = x.float().numpy()
+    rec = 12 if sr else 4
+    for start in (0, 3 * 1024 * 1024 + 8192, n - 16384):
+        m = 16384
+        planes, meta = O.encode(xs[start:start + m], bits, g, sr)
+        off = 0
+        for w, p in zip(O.UNITS[bits], planes):
+            assert ph[off + start * w // 8: off + (start + m) * w // 8].tobytes() == p
+            off += n * w // 8
+        assert ph[off + (start // g) * rec: off + ((start + m) // g) * rec].tobytes() == meta
+
+
 @pytest.mark.parametrize("bits", [2, 3, 4, 8])
 @pytest.mark.parametrize("sr", [False, True])
 def test_codec_intlog_matches_oracle(bits, sr):
