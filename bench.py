@@ -441,7 +441,8 @@ def run_allreduce(args, rank, world, local_rank):
             m = int(a2a_mat[s2, d])
             if s2 != d and m:
                 cap += (fc.footprint_bytes(cfg, -(-m // args.group) * args.group) + 15) // 16 * 16
-    comm = fcd.QComm(dist.group.WORLD, max_elems=n, config=cfg, a2a_bytes=cap + 4096)
+    comm = fcd.QComm(dist.group.WORLD, max_elems=n, config=cfg, a2a_bytes=cap + 4096,
+                     oneshot_max_elems=min(n, 1 << 19))
     y = torch.empty_like(x)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
@@ -488,6 +489,20 @@ def run_allreduce(args, rank, world, local_rank):
     ms_disp = timed(lambda: comm.all2all(send, a2a_mat, out_dtype=torch.bfloat16), args.steps, args.warmup)
     back = spiky_bf16(int(a2a_mat[:, rank].sum()), 8000 + rank, dev)
     ms_comb = timed(lambda: comm.all2all(back, a2a_mat.T.copy(), out_dtype=torch.bfloat16), args.steps, args.warmup)
+    # small messages (BASELINE configs[4], latency end): two-step vs one-shot vs NCCL bf16
+    small = {}
+    for m in (1 << 15, 1 << 17, 1 << 19):
+        if m > n:
+            continue
+        xs, ys = x[:m], y[:m]
+        row = {"two_step_us": round(1e3 * timed(lambda: comm.all_reduce(xs, out=ys, algo="two_step"),
+                                                args.steps, args.warmup), 2),
+               "one_shot_us": round(1e3 * timed(lambda: comm.all_reduce(xs, out=ys, algo="one_shot"),
+                                                args.steps, args.warmup), 2)}
+        if backend == "nccl":
+            xbs = x[:m].clone()
+            row["nccl_bf16_us"] = round(1e3 * timed(lambda: dist.all_reduce(xbs), args.steps, args.warmup), 2)
+        small[f"{2 * m >> 10}KiB"] = row
     ms_disp_nccl = None
     if backend == "nccl":
         recv = torch.empty(int(a2a_mat[:, rank].sum()), dtype=torch.bfloat16, device=dev)
@@ -533,6 +548,7 @@ def run_allreduce(args, rank, world, local_rank):
                 "speedup_vs_nccl": None if ms_disp_nccl is None else round(ms_disp_nccl / ms_disp, 3)},
             "e2e": {"value": round(2 * n * world / (ms_e2e * 1e-3) / 1e9, 2), "unit": "GB/s",
                     "ms_per_step": round(ms_e2e, 4), "h2d_bytes_per_step": 2 * n, "d2h_bytes_per_step": 2 * n},
+            "small_message_allreduce": small,
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }

@@ -104,6 +104,14 @@ int fc2_reduce_requant(const fc2_config* cfg, int32_t nsrc, const void* const* s
                        int64_t n, int32_t ndst, void* const* dst_payloads, int32_t* dev_err,
                        void* stream);
 
+/* The same for nshard independent shards in one launch: shard k's sources are
+ * src_payloads[s] + k * src_stride and its destinations dst_payloads[d] +
+ * k * dst_stride (the one-shot AllReduce reduces every shard on every rank). */
+int fc2_reduce_requant_batch(const fc2_config* cfg, int32_t nsrc, const void* const* src_payloads,
+                             int64_t n, int32_t nshard, int64_t src_stride, int32_t ndst,
+                             void* const* dst_payloads, int64_t dst_stride, int32_t* dev_err,
+                             void* stream);
+
 /* Decode the N gathered shard payloads of a two-step AllReduce straight into
  * the bf16/f32 output on the bf16 grid, stripping padding (collectives.py:313-314,
  * 185-186). */
@@ -186,6 +194,17 @@ int fc2_comm_barrier(fc2_comm* c, int32_t* dev_err, double timeout_s, void* stre
 int fc2_allreduce_2step(fc2_comm* c, const fc2_config* cfg, const void* x, int32_t x_dtype, void* y,
                         int32_t y_dtype, int64_t n, int64_t slot_bytes, int32_t* dev_err, double timeout_s,
                         void* stream);
+
+/* One-shot variant for small messages (latency-bound sizes), same result bit
+ * for bit: every rank stores all N of its packed shards into every peer (one
+ * all-gather of packed bytes instead of the two-step's two exchanges), one
+ * device barrier, then each rank reduces + requantizes every shard itself
+ * (deterministic, so all ranks agree) and decodes.  Uses the region at
+ * region_off of the symmetric buffer: 2 * world * world + world slots of
+ * slot_bytes (double-buffered by call parity, so no trailing barrier). */
+int fc2_allreduce_oneshot(fc2_comm* c, const fc2_config* cfg, const void* x, int32_t x_dtype, void* y,
+                          int32_t y_dtype, int64_t n, int64_t slot_bytes, int64_t region_off,
+                          int32_t* dev_err, double timeout_s, void* stream);
 
 /* Quantized All2All (dispatch, collectives.py:428-482; combine = transposed
  * matrix).  matrix: host int64[world*world] element counts.  The diagonal

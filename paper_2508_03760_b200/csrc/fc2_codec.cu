@@ -18,6 +18,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "fc2_kernels.cuh"
 
@@ -690,7 +691,14 @@ int fc2_gather_decode(const fc2_config* cfg, int32_t nshards, const void* const*
 
 int fc2_reduce_requant(const fc2_config* cfg, int32_t nsrc, const void* const* src_payloads, int64_t n, int32_t ndst,
                        void* const* dst_payloads, int32_t* dev_err, void* stream) {
+  return fc2_reduce_requant_batch(cfg, nsrc, src_payloads, n, 1, 0, ndst, dst_payloads, 0, dev_err, stream);
+}
+
+int fc2_reduce_requant_batch(const fc2_config* cfg, int32_t nsrc, const void* const* src_payloads, int64_t n,
+                             int32_t nshard, int64_t src_stride, int32_t ndst, void* const* dst_payloads,
+                             int64_t dst_stride, int32_t* dev_err, void* stream) {
   int rc = check_cfg(cfg);
+  if (nshard < 1) return set_err(FC2_ECONFIG, "nshard must be >= 1");
   if (rc) return rc;
   if (nsrc < 1 || nsrc > FC2_MAX_PEERS || ndst < 1 || ndst > FC2_MAX_PEERS)
     return set_err(FC2_ECONFIG, "nsrc/ndst out of range");
@@ -702,6 +710,7 @@ int fc2_reduce_requant(const fc2_config* cfg, int32_t nsrc, const void* const* s
   ReduceArgs a;
   a.nsrc = nsrc; a.ndst = ndst; a.B = cfg->bitwidth; a.G = cfg->group_size; a.sr = cfg->scheme == 1;
   a.intlog = cfg->scale_encoding; a.theta = cfg->theta; a.n = n; a.lut = lut; a.err = dev_err;
+  a.nshard = nshard; a.sstride = src_stride; a.dstride = dst_stride;
   for (int i = 0; i < nsrc; ++i) a.src[i] = (const uint8_t*)src_payloads[i];
   for (int i = 0; i < ndst; ++i) a.dst[i] = (uint8_t*)dst_payloads[i];
   if (fast_group(a.G)) {
@@ -709,6 +718,17 @@ int fc2_reduce_requant(const fc2_config* cfg, int32_t nsrc, const void* const* s
     return red_fast(a.B, a.sr != 0, a.G, a, st);
   }
   if (ndst > 8) return set_err(FC2_ECONFIG, "generic reduce supports <= 8 destinations");
+  if (nshard > 1) {  // the generic reducer takes one shard per launch
+    std::vector<const void*> s1(nsrc);
+    std::vector<void*> d1(ndst);
+    for (int64_t k = 0; k < nshard; ++k) {
+      for (int i = 0; i < nsrc; ++i) s1[i] = (const uint8_t*)src_payloads[i] + k * src_stride;
+      for (int i = 0; i < ndst; ++i) d1[i] = (uint8_t*)dst_payloads[i] + k * dst_stride;
+      rc = fc2_reduce_requant_batch(cfg, nsrc, s1.data(), n, 1, 0, ndst, d1.data(), 0, dev_err, stream);
+      if (rc) return rc;
+    }
+    return FC2_OK;
+  }
   a.total = n / a.G;
   int64_t blocks = (a.total + 7) / 8;
   int64_t cap = (int64_t)num_sms() * 8;

@@ -44,6 +44,7 @@ struct fc2_comm {
   uint8_t* peer[FC2_COMM_MAX];
   bool opened[FC2_COMM_MAX];
   uint32_t epoch;
+  uint32_t oneshot_calls;  // parity selects the one-shot landing buffer
 };
 
 namespace {
@@ -209,6 +210,63 @@ int fc2_allreduce_2step(fc2_comm* c, const fc2_config* cfg, const void* x, int32
   // 5. decode every owner's shard into the output (padding stripped)
   std::vector<const void*> gs(N);
   for (int o = 0; o < N; ++o) gs[o] = gath(r, o);
+  return fc2_gather_decode(cfg, N, gs.data(), S, y, y_dtype, n, dev_err, stream);
+}
+
+// One-shot AllReduce: same arithmetic as the two-step
+// (collectives.py:263-315), one exchange.  Region layout at region_off:
+//   landing[parity][src][shard]  2 * N * N slots
+//   result[shard]                N slots (this rank's requantized shards)
+int fc2_allreduce_oneshot(fc2_comm* c, const fc2_config* cfg, const void* x, int32_t x_dtype, void* y,
+                          int32_t y_dtype, int64_t n, int64_t slot_bytes, int64_t region_off, int32_t* dev_err,
+                          double timeout_s, void* stream) {
+  const int N = c->world, r = c->rank;
+  int rc = fc2_check_config(cfg);
+  if (rc) return rc;
+  const int64_t mult = (int64_t)N * cfg->group_size;
+  const int64_t padded = (n + mult - 1) / mult * mult;
+  const int64_t S = padded / N;
+  int64_t F = 0;
+  rc = fc2_footprint(cfg, S, &F);
+  if (rc) return rc;
+  if (F > slot_bytes || (slot_bytes & 15)) return set_err(FC2_ECONFIG, "slot too small for shard footprint");
+  if (region_off < 0 || (region_off & 15) ||
+      region_off + (int64_t)(2 * N * N + N) * slot_bytes > c->bytes - FC2_FLAG_BYTES)
+    return set_err(FC2_ECONFIG, "communicator buffer too small for the one-shot region");
+  if (N * N > FC2_MAX_JOBS) return set_err(FC2_ECONFIG, "one-shot supports world <= 16");
+  const int esz = x_dtype == FC2_BF16 ? 2 : (x_dtype == FC2_F32 ? 4 : 8);
+  const int par = (int)(c->oneshot_calls++ & 1u);
+  auto land = [&](int dst, int src, int shard) {
+    return (uint8_t*)c->peer[dst] + FC2_FLAG_BYTES + region_off +
+           ((int64_t)par * N * N + (int64_t)src * N + shard) * slot_bytes;
+  };
+  uint8_t* result = c->local + FC2_FLAG_BYTES + region_off + (int64_t)2 * N * N * slot_bytes;
+  // 1. my N shards, packed, into every rank's landing row for me (one launch)
+  std::vector<const void*> xs(N * N);
+  std::vector<int64_t> nv(N * N), ns(N * N);
+  std::vector<void*> outs(N * N);
+  for (int d = 0; d < N; ++d)
+    for (int j = 0; j < N; ++j) {
+      const int64_t valid = n - (int64_t)j * S;
+      const int k = d * N + j;
+      nv[k] = valid < 0 ? 0 : (valid > S ? S : valid);
+      ns[k] = S;
+      xs[k] = nv[k] ? (const uint8_t*)x + (int64_t)j * S * esz : x;
+      outs[k] = land(d, r, j);
+    }
+  rc = fc2_encode_batch(cfg, x_dtype, N * N, xs.data(), nv.data(), ns.data(), outs.data(), dev_err, stream);
+  if (rc) return rc;
+  rc = fc2_comm_barrier(c, dev_err, timeout_s, stream);
+  if (rc) return rc;
+  // 2. reduce + requantize every shard locally (sources: landing[par][s][*])
+  std::vector<const void*> srcs(N);
+  for (int s2 = 0; s2 < N; ++s2) srcs[s2] = land(r, s2, 0);
+  void* dst = result;
+  rc = fc2_reduce_requant_batch(cfg, N, srcs.data(), S, N, slot_bytes, 1, &dst, slot_bytes, dev_err, stream);
+  if (rc) return rc;
+  // 3. decode all shards (padding stripped, bf16 grid)
+  std::vector<const void*> gs(N);
+  for (int o = 0; o < N; ++o) gs[o] = result + (int64_t)o * slot_bytes;
   return fc2_gather_decode(cfg, N, gs.data(), S, y, y_dtype, n, dev_err, stream);
 }
 

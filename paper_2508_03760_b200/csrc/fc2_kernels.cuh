@@ -53,6 +53,7 @@ struct DecBatch {
 struct ReduceArgs {
   int nsrc, ndst, B, G, sr, intlog, theta;
   int64_t n, total;
+  int64_t nshard, sstride, dstride;  // independent shards: shard k at src[s] + k sstride, dst[d] + k dstride
   const double* lut;
   int32_t* err;
   const uint8_t* src[FC2_MAX_PEERS];
@@ -1083,8 +1084,11 @@ __global__ void __launch_bounds__(G) k_reduce_cta(const __grid_constant__ Reduce
   const int64_t meta_off = a.n * B / 8;
   EncCtx cx;
   cx.n = a.n; cx.meta_off = meta_off; cx.intlog = a.intlog; cx.theta = a.theta; cx.lut = a.lut; cx.err = a.err;
+  const int64_t tps = (ngroups + 31) / 32;  // tiles per shard
   for (int64_t t = blockIdx.x; t < a.total; t += gridDim.x) {
-    const int64_t tg0 = t * 32;
+    const int64_t sh = t / tps;
+    const int64_t soff = sh * a.sstride, doff = sh * a.dstride;
+    const int64_t tg0 = (t - sh * tps) * 32;
     const int ng = (int)min((int64_t)32, ngroups - tg0);
     // ---- accumulation: warp w = run w, lane = group
     {
@@ -1102,8 +1106,8 @@ __global__ void __launch_bounds__(G) k_reduce_cta(const __grid_constant__ Reduce
 #pragma unroll
         for (int i = 0; i < BATCH; ++i)
           if (s0 + i < a.nsrc) {
-            load_run_words<B>(a.src[s0 + i], a.n, er, cw[i]);
-            load_record(a.src[s0 + i] + meta_off + gc * rb, rec[i], rb);
+            load_run_words<B>(a.src[s0 + i] + soff, a.n, er, cw[i]);
+            load_record(a.src[s0 + i] + soff + meta_off + gc * rb, rec[i], rb);
           }
 #pragma unroll
         for (int i = 0; i < BATCH; ++i) {
@@ -1182,7 +1186,7 @@ __global__ void __launch_bounds__(G) k_reduce_cta(const __grid_constant__ Reduce
     {
       const int gl = w * GPW + lane / LPG, li = lane % LPG;
       const int64_t g_abs = tg0 + gl;
-      encode_run_f32<B, SR, G>(tile, ost, gl, li, g_abs < ngroups, g_abs, cx, a.dst, a.ndst);
+      encode_run_f32<B, SR, G>(tile, ost, gl, li, g_abs < ngroups, g_abs, cx, a.dst, a.ndst, doff);
     }
     __syncthreads();  // whole tile staged (runs of a group come from several warps... same warp here)
     // ---- copy-out: warp w writes groups [w*GPW, w*GPW + GPW) to every destination
@@ -1194,7 +1198,7 @@ __global__ void __launch_bounds__(G) k_reduce_cta(const __grid_constant__ Reduce
         for (int u = 0; u < n_units(B); ++u) {
           const int W = unit_w(B, u), O = unit_off(B, u);
           const uint8_t* base = ost + OutStage<B, G>::off(u);
-          uint8_t* dst = a.dst[dd] + (a.n * O) / 8 + (tg0 + first) * (G * W / 8);
+          uint8_t* dst = a.dst[dd] + doff + (a.n * O) / 8 + (tg0 + first) * (G * W / 8);
           if (W == 1) copy_out_groups<G, 1>(base, dst, first, cnt);
           else if (W == 2) copy_out_groups<G, 2>(base, dst, first, cnt);
           else if (W == 4) copy_out_groups<G, 4>(base, dst, first, cnt);
@@ -1211,7 +1215,7 @@ struct RedCta {
   static constexpr int SMEM = RTile<G>::BYTES + OutStage<B, G>::BYTES;
   static int go(const ReduceArgs& a0, cudaStream_t st) {
     ReduceArgs a = a0;
-    a.total = (a.n / G + 31) / 32;
+    a.total = (a.n / G + 31) / 32 * a.nshard;
     auto kern = k_reduce_cta<B, SR, G>;
     static bool attr = false;
     if (!attr) {
@@ -1290,6 +1294,18 @@ struct Launchers {
     bool grp = a.nsrc <= kRedMaxSrc;
     for (int s = 0; s < a.nsrc; ++s)
       if (reinterpret_cast<uintptr_t>(a.src[s]) & 15u) grp = false;
+    if (grp && a.nshard > 1 && (a.sstride & 15)) grp = false;
+    if (!grp && a.nshard > 1) {  // the other reducers take one shard per launch
+      ReduceArgs one = a;
+      one.nshard = 1;
+      for (int64_t k = 0; k < a.nshard; ++k) {
+        for (int s = 0; s < a.nsrc; ++s) one.src[s] = a.src[s] + k * a.sstride;
+        for (int d = 0; d < a.ndst; ++d) one.dst[d] = a.dst[d] + k * a.dstride;
+        int rc = red<SR>(G, one, st);
+        if (rc) return rc;
+      }
+      return FC2_OK;
+    }
     if (grp) {
       switch (G) {
         case 32: return RedCta<B, SR, 32>::go(a, st);

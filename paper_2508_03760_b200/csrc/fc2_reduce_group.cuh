@@ -302,7 +302,8 @@ struct RTile {
 // encode one 32-element run of group gl (part li) from the f32 tile
 template <int B, bool SR, int G>
 __device__ __forceinline__ void encode_run_f32(const uint8_t* tile, uint8_t* ost, int gl, int li, bool active,
-                                               int64_t g_abs, const EncCtx& cx, uint8_t* const* outs, int nout) {
+                                               int64_t g_abs, const EncCtx& cx, uint8_t* const* outs, int nout,
+                                               int64_t out_off = 0) {
   constexpr int LPG = G / 32;
   constexpr int L = (1 << B) - 1;
   constexpr int FB = FixFor<B>::FB;
@@ -462,7 +463,7 @@ __device__ __forceinline__ void encode_run_f32(const uint8_t* tile, uint8_t* ost
         rb = 2;
       }
     }
-    for (int d = 0; d < nout; ++d) store_record(outs[d] + cx.meta_off + g_abs * rb, rec, rb);
+    for (int d = 0; d < nout; ++d) store_record(outs[d] + out_off + cx.meta_off + g_abs * rb, rec, rb);
   }
 }
 

@@ -157,7 +157,8 @@ class QComm:
     """
 
     def __init__(self, group=None, max_elems: int = 1 << 25, config: QuantConfig | None = None,
-                 transport: str = "ipc", a2a_bytes: int = 0, timeout_s: float = 60.0):
+                 transport: str = "ipc", a2a_bytes: int = 0, timeout_s: float = 60.0,
+                 oneshot_max_elems: int = 1 << 18):
         self.device = _device.require_cuda()
         self.group = group
         self.rank = dist.get_rank(group)
@@ -167,6 +168,9 @@ class QComm:
         self.timeout_s = float(timeout_s)
         self.max_lay = TwoStepLayout.make(max_elems, self.world, self.cfg)
         self.a2a_off = 2 * self.world * self.max_lay.slot_bytes
+        # one-shot region (small messages): 2 N^2 landing slots + N result slots
+        self.os_lay = TwoStepLayout.make(min(int(oneshot_max_elems), max_elems), self.world, self.cfg)
+        self.os_off = self.a2a_off + _round_up(int(a2a_bytes), _SLOT_ALIGN)
         self.codec = CudaCodec(self.cfg, self.device)
         self.err = self.codec.err
         self._c = None
@@ -177,7 +181,7 @@ class QComm:
             hb = lib.fc2_comm_handle_bytes()
             handle = (ctypes.c_uint8 * hb)()
             ptr = ctypes.c_void_p()
-            nbytes = self.a2a_off + _round_up(int(a2a_bytes), _SLOT_ALIGN)
+            nbytes = self.os_off + (2 * self.world * self.world + self.world) * self.os_lay.slot_bytes
             _lib.check(lib.fc2_comm_create(self.rank, self.world, nbytes, ctypes.byref(ptr),
                                            ctypes.cast(handle, ctypes.c_void_p)))
             self._c = ptr
@@ -191,9 +195,15 @@ class QComm:
     def shard_len(self) -> int:
         return self.max_lay.shard_len
 
-    def all_reduce(self, x: torch.Tensor, out: torch.Tensor | None = None, check: bool = False) -> torch.Tensor:
+    def all_reduce(self, x: torch.Tensor, out: torch.Tensor | None = None, check: bool = False,
+                   algo: str = "auto") -> torch.Tensor:
         """Two-step quantized AllReduce of a 1-D bf16/f32 CUDA tensor; every
-        rank gets the identical bf16-grid result (collectives.py:313-314)."""
+        rank gets the identical bf16-grid result (collectives.py:313-314).
+
+        ``algo``: ``"two_step"`` (two packed exchanges), ``"one_shot"`` (one
+        all-gather of packed shards, every rank reduces every shard: fewer
+        barriers for latency-bound sizes, same bits), or ``"auto"`` (one-shot
+        up to ``oneshot_max_elems`` on the ipc transport)."""
         x = x.reshape(-1)
         if not x.is_contiguous():
             x = x.contiguous()
@@ -202,7 +212,18 @@ class QComm:
             raise DataError(f"payload of {n} elements exceeds the communicator's {self.max_lay.n}")
         y = out if out is not None else torch.empty(n, dtype=x.dtype, device=x.device)
         lay = TwoStepLayout.make(n, self.world, self.cfg)
-        if self.transport == "ipc":
+        if algo not in ("auto", "two_step", "one_shot"):
+            raise ConfigError(f"unknown allreduce algorithm {algo!r}")
+        one = self.transport == "ipc" and n <= self.os_lay.n and algo != "two_step"
+        if algo == "one_shot" and not one:
+            raise ConfigError("one_shot needs the ipc transport and n <= oneshot_max_elems")
+        if one:
+            c = self.cfg.c_struct()
+            _lib.check(_lib.lib().fc2_allreduce_oneshot(
+                self._c, ctypes.byref(c), x.data_ptr(), _device.dtype_code(x), y.data_ptr(),
+                _device.dtype_code(y), n, self.os_lay.slot_bytes, self.os_off, self.err.data_ptr(),
+                self.timeout_s, _device.stream_handle()))
+        elif self.transport == "ipc":
             c = self.cfg.c_struct()
             _lib.check(_lib.lib().fc2_allreduce_2step(
                 self._c, ctypes.byref(c), x.data_ptr(), _device.dtype_code(x), y.data_ptr(),

@@ -40,12 +40,15 @@ def _worker(rank, world, port, case, q):
                              chunk_size=g)
         seeds = O.child_seeds(seed, world)
         if kind == "allreduce":
-            comm = QComm(max_elems=n, config=cfg, timeout_s=120.0)
+            comm = QComm(max_elems=n, config=cfg, timeout_s=120.0, oneshot_max_elems=n)
             x = torch.from_numpy(O.bf16_snap(O.spiky(n, seeds[rank])).astype(np.float32)).cuda()
             outs = []
-            for dt in (torch.float32, torch.bfloat16):
-                y = comm.all_reduce(x.to(dt), check=True)
-                outs.append(y.float().cpu().numpy().tobytes())
+            # both algorithms, both output types; the one-shot runs three times
+            # so both landing buffers (call parity) are exercised
+            for algo in ("two_step", "one_shot", "one_shot", "one_shot"):
+                for dt in (torch.float32, torch.bfloat16):
+                    y = comm.all_reduce(x.to(dt), check=True, algo=algo)
+                    outs.append(y.float().cpu().numpy().tobytes())
             q.put((rank, outs))
         else:
             rng = np.random.default_rng(seed)

@@ -131,3 +131,40 @@ def test_a2a_zero_matrix_and_shape_errors():
     assert res.ledger.total_raw == 0
     with pytest.raises(fc.ConfigError):
         fc.all2all_dispatch_q([np.zeros(64, np.float32)] * N, topo, fc.QuantConfig(8), np.zeros((3, 3), int))
+
+
+@pytest.mark.parametrize("bits,g,sr,S,stride_pad", [(4, 128, True, 8192, 0), (3, 64, False, 4096, 16),
+                                                    (4, 128, True, 4096, 8), (5, 96, True, 96 * 40, 0)])
+def test_reduce_requant_batch_equals_per_shard(bits, g, sr, S, stride_pad):
+    """fc2_reduce_requant_batch (the one-shot AllReduce's local reduce of every
+    shard) == one fc2_reduce_requant per shard, byte for byte; covers the CTA
+    kernel, a stride that only the per-launch reducers take (8-byte aligned),
+    and a non-fast group size."""
+    import ctypes
+
+    from paper_2508_03760_b200 import _lib
+    from paper_2508_03760_b200.collectives import reduce_requant
+
+    c = cfg(bits, g, sr)
+    N, K = 4, 3
+    F = fc.footprint_bytes(c, S)
+    slot = (F + 15) // 16 * 16 + stride_pad
+    src = torch.zeros(N * K * slot + 64, dtype=torch.uint8, device="cuda")
+    for s in range(N):
+        for k in range(K):
+            x = torch.from_numpy(O.bf16_snap(O.spiky(S, 100 * s + k)).astype(np.float32)).cuda()
+            src[(s * K + k) * slot:(s * K + k) * slot + F] = fc.encode_payload(x, c, S)
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    want = torch.zeros(K * slot, dtype=torch.uint8, device="cuda")
+    for k in range(K):
+        reduce_requant(c, [src.data_ptr() + (s * K + k) * slot for s in range(N)], S,
+                       [want.data_ptr() + k * slot], err)
+    got = torch.zeros_like(want)
+    cs = c.c_struct()
+    _lib.check(_lib.lib().fc2_reduce_requant_batch(
+        ctypes.byref(cs), N, _lib.ptr_array([src.data_ptr() + s * K * slot for s in range(N)]), S, K, slot, 1,
+        _lib.ptr_array([got.data_ptr()]), slot, err.data_ptr(), torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    assert int(err.item()) == 0
+    for k in range(K):
+        assert torch.equal(got[k * slot:k * slot + F], want[k * slot:k * slot + F])
