@@ -31,9 +31,9 @@ namespace fc2 {
 thread_local std::string g_err;
 static int64_t g_launches = 0;
 static std::mutex g_mu;
-static double* g_lut = nullptr;          // 255 thetas x 256 entries
-static bool g_lut_ok[256] = {false};
-static int g_lut_dev = -1;
+constexpr int kMaxDev = 64;
+static double* g_lut[kMaxDev] = {nullptr};   // per device: 255 thetas x 256 entries
+static bool g_lut_ok[kMaxDev][256] = {{false}};
 
 int set_err(int code, const char* fmt, ...) {
   char buf[512];
@@ -274,11 +274,11 @@ static const double* lut_for(const fc2_config* c, int* rc) {
   std::lock_guard<std::mutex> lk(g_mu);
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!g_lut || g_lut_dev != dev || !g_lut_ok[c->theta]) {
+  if (dev < 0 || dev >= kMaxDev || !g_lut[dev] || !g_lut_ok[dev][c->theta]) {
     *rc = set_err(FC2_ECONFIG, "INT_LOG table for theta=%d not loaded (call fc2_set_intlog_table)", c->theta);
     return nullptr;
   }
-  return g_lut + (size_t)(c->theta - 1) * 256;
+  return g_lut[dev] + (size_t)(c->theta - 1) * 256;
 }
 
 static int64_t rec_nb(const fc2_config* c) { return rec_bytes(c->scheme == 1, c->scale_encoding == 1); }
@@ -321,15 +321,13 @@ int fc2_set_intlog_table(int32_t theta, const double* table256) {
   std::lock_guard<std::mutex> lk(g_mu);
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!g_lut || g_lut_dev != dev) {
-    if (cudaMalloc(&g_lut, sizeof(double) * 255 * 256) != cudaSuccess)
-      return set_err(FC2_ECUDA, "cudaMalloc lut failed");
-    g_lut_dev = dev;
-    for (int i = 0; i < 256; ++i) g_lut_ok[i] = false;
-  }
-  if (cudaMemcpy(g_lut + (size_t)(theta - 1) * 256, table256, 256 * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
+  if (dev < 0 || dev >= kMaxDev) return set_err(FC2_ECUDA, "device %d out of range", dev);
+  if (!g_lut[dev] && cudaMalloc(&g_lut[dev], sizeof(double) * 255 * 256) != cudaSuccess)
+    return set_err(FC2_ECUDA, "cudaMalloc lut failed");
+  if (cudaMemcpy(g_lut[dev] + (size_t)(theta - 1) * 256, table256, 256 * sizeof(double), cudaMemcpyHostToDevice) !=
+      cudaSuccess)
     return set_err(FC2_ECUDA, "lut upload failed");
-  g_lut_ok[theta] = true;
+  g_lut_ok[dev][theta] = true;
   return FC2_OK;
 }
 

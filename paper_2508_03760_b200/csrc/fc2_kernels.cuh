@@ -1,6 +1,7 @@
 // fc2_kernels.cuh -- kernel templates + per-bitwidth launchers (instantiated in
 // fc2_inst_b<B>.cu so the 8 bitwidths compile in parallel).
 #pragma once
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <utility>
@@ -16,6 +17,20 @@ namespace fc2 {
 int set_err(int code, const char* fmt, ...);
 int cuda_check(const char* what);
 int num_sms();
+
+// Opt a kernel into `bytes` of dynamic shared memory, once per device (the
+// attribute is per device; several GPUs may be driven from one process).
+template <auto KERN>
+inline void smem_attr(int bytes) {
+  static std::atomic<uint64_t> done{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(done.load(std::memory_order_acquire) & bit)) {
+    cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    done.fetch_or(bit, std::memory_order_release);
+  }
+}
 
 // ---------------------------------------------------------------------------
 // job tables (passed by value as __grid_constant__ kernel parameters)
@@ -325,12 +340,8 @@ struct EncGrp {
   template <int LPG>
   static int run(const EncBatch& b, cudaStream_t st) {
     constexpr int SMEM = WARPS * (STAGES * GTile<__nv_bfloat16, G>::IN_BYTES / LPG + G / LPG * 4);
-    auto kern = k_encode_grp<B, SR, G, WARPS, LPG, STAGES>;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-      attr = true;
-    }
+    constexpr auto kern = k_encode_grp<B, SR, G, WARPS, LPG, STAGES>;
+    smem_attr<kern>(SMEM);
     int64_t blocks = (b.total + WARPS - 1) / WARPS;
     int64_t cap = (int64_t)num_sms() * FC2_ENC_CTAS_PER_SM;
     if (blocks > cap) blocks = cap;
@@ -769,12 +780,8 @@ __global__ void __launch_bounds__(kDecWarps * 32) k_decode_fast(const __grid_con
 template <typename OT, int B>
 int launch_decode_fast(const DecBatch& b, cudaStream_t st) {
   constexpr int SMEM = kDecWarps * (kDecStages * DecIn<B>::BYTES + kDecTile / 2 * (int)sizeof(OT));
-  auto kern = k_decode_fast<OT, B>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    attr = true;
-  }
+  constexpr auto kern = k_decode_fast<OT, B>;
+  smem_attr<kern>(SMEM);
   // one tile per warp: the block scheduler balances the tail (no persistent loop)
   int64_t blocks = (b.total + kDecWarps - 1) / kDecWarps;
   const int64_t cap = (int64_t)num_sms() * 64;
@@ -889,13 +896,9 @@ template <int B, bool SR, int G>
 struct EncFast {
   template <typename T>
   static int launch(const EncBatch& b, cudaStream_t st) {
-    auto kern = k_encode_fast<T, B, SR, G>;
+    constexpr auto kern = k_encode_fast<T, B, SR, G>;
     const int smem = kEncWarps * kStages * Stage<T>::BYTES;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      attr = true;
-    }
+    smem_attr<kern>(smem);
     int64_t blocks = (b.total + kEncWarps - 1) / kEncWarps;
     int64_t cap = (int64_t)num_sms() * 8;
     if (blocks > cap) blocks = cap;
@@ -1216,12 +1219,8 @@ struct RedCta {
   static int go(const ReduceArgs& a0, cudaStream_t st) {
     ReduceArgs a = a0;
     a.total = (a.n / G + 31) / 32 * a.nshard;
-    auto kern = k_reduce_cta<B, SR, G>;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-      attr = true;
-    }
+    constexpr auto kern = k_reduce_cta<B, SR, G>;
+    smem_attr<kern>(SMEM);
     int64_t blocks = a.total;
     if (blocks < 1) blocks = 1;
     if (blocks > 65535LL * 16) blocks = 65535LL * 16;
@@ -1237,12 +1236,8 @@ struct RedGrp {
   static int go(const ReduceArgs& a0, cudaStream_t st) {
     ReduceArgs a = a0;
     a.total = (a.n / G + 31) / 32;
-    auto kern = k_reduce_grp<B, SR, G, WARPS>;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-      attr = true;
-    }
+    constexpr auto kern = k_reduce_grp<B, SR, G, WARPS>;
+    smem_attr<kern>(SMEM);
     int64_t blocks = (a.total + WARPS - 1) / WARPS;
     if (blocks < 1) blocks = 1;
     kern<<<(unsigned)blocks, WARPS * 32, SMEM, st>>>(a);

@@ -51,3 +51,12 @@ for sl in (1 << 20, 1 << 21, 1 << 22, 1 << 23):
     out[f"roundtrip_slice_{sl >> 20}Mi_ms"] = t(lambda: fc.roundtrip_host(xh, cfg, payload=pay, out=y, slice_elems=sl,
                                                                        check=False))
 print(json.dumps({k: round(v, 4) for k, v in out.items()}))
+out2 = {}
+for sl in (1 << 22, 1 << 23):
+    out2[f"roundtrip_nopayload_slice_{sl >> 20}Mi_ms"] = t(lambda: fc.roundtrip_host(xh, cfg, payload=False, out=y,
+                                                                                  slice_elems=sl, check=False))
+    out2[f"encode_host_slice_{sl >> 20}Mi_ms"] = t(lambda: fc.encode_host(xh, cfg, payload=pay, slice_elems=sl,
+                                                                          check=False))
+    out2[f"decode_host_slice_{sl >> 20}Mi_ms"] = t(lambda: fc.decode_host(pay, cfg, n, out=y, slice_elems=sl,
+                                                                          check=False))
+print(json.dumps({k: round(v, 4) for k, v in out2.items()}))
