@@ -267,80 +267,70 @@ __device__ __forceinline__ void issue_grp_tile(const EncBatch& b, int64_t t, uin
 __host__ __device__ constexpr int enc_min_ctas(int B, int warps) {
   return 65536 / (warps * 32 * (B == 7 ? 128 : (B == 8 ? 102 : FC2_ENC_REGS)));
 }
-template <int B, bool SR, int G, int WARPS, int LPG, int STAGES>
-__global__ void __launch_bounds__(WARPS * 32, enc_min_ctas(B, WARPS)) k_encode_grp(const __grid_constant__ EncBatch b) {
-  using IT = GTile<__nv_bfloat16, G, LPG>;
-  constexpr int GPT = 32 / LPG;                       // groups per warp tile
-  constexpr int IN_BYTES = IT::IN_BYTES / LPG;
-  constexpr int TIE_BYTES = G / LPG * 4;               // one 32-bit tie mask per run per lane
-  constexpr int PER_WARP = STAGES * IN_BYTES + TIE_BYTES;  // plane words go straight to global
-  extern __shared__ __align__(16) uint8_t smem[];
-  const int warp = (int)(threadIdx.x >> 5), lane = (int)lane_id();
-  uint8_t* in0 = smem + warp * PER_WARP;
-  uint32_t* tms = reinterpret_cast<uint32_t*>(in0 + STAGES * IN_BYTES);
-  const int64_t nw = (int64_t)gridDim.x * WARPS;
-  int64_t t = (int64_t)blockIdx.x * WARPS + warp;
-  if constexpr (STAGES == 2) {
-    if (t < b.total) issue_grp_tile<G, LPG>(b, t, in0);
-    cp_async_commit();
-  }
-  int stage = 0;
-  for (; t < b.total; t += nw) {
-    if constexpr (STAGES == 2) {
-      const int64_t tn = t + nw;
-      if (tn < b.total) issue_grp_tile<G, LPG>(b, tn, in0 + (stage ^ 1) * IN_BYTES);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      __syncwarp();  // previous tile fully consumed
-      issue_grp_tile<G, LPG>(b, t, in0);
-      cp_async_commit();
-      cp_async_wait<0>();
-    }
-    __syncwarp();
-    const int ji = find_job(b, t);
-    const EncJob& jb = b.j[ji];
-    const int64_t ngroups = jb.n / G;
-    const int64_t tg0 = (t - jb.t0) * GPT;
-    const int64_t gabs = tg0 + lane / LPG;
-    const int ng = (int)min((int64_t)GPT, ngroups - tg0);
-    EncCtx cx;
-    cx.n = jb.n;
-    cx.meta_off = jb.n * B / 8;
-    cx.intlog = b.intlog;
-    cx.theta = b.theta;
-    cx.lut = b.lut;
-    cx.err = b.err;
-    encode_tile_bf16<B, SR, G, LPG>(in0 + stage * IN_BYTES, tms, gabs < ngroups, gabs, cx, jb.out, tg0, ng);
-    if constexpr (STAGES == 2) stage ^= 1;
-  }
+// one warp tile of the lane-per-group encoder: tile index t in the tile
+// numbering of shape LPG (32 / LPG groups per tile)
+template <int B, bool SR, int G, int LPG>
+__device__ __forceinline__ void encode_grp_tile(const EncBatch& b, int64_t t, uint8_t* in0, uint32_t* tms) {
+  constexpr int GPT = 32 / LPG;  // groups per warp tile
+  const int lane = (int)lane_id();
+  __syncwarp();  // previous tile fully consumed
+  issue_grp_tile<G, LPG>(b, t, in0);
+  cp_async_commit();
   cp_async_wait<0>();
+  __syncwarp();
+  const int ji = find_job(b, t);
+  const EncJob& jb = b.j[ji];
+  const int64_t ngroups = jb.n / G;
+  const int64_t tg0 = (t - jb.t0) * GPT;
+  const int64_t gabs = tg0 + lane / LPG;
+  const int ng = (int)min((int64_t)GPT, ngroups - tg0);
+  EncCtx cx;
+  cx.n = jb.n;
+  cx.meta_off = jb.n * B / 8;
+  cx.intlog = b.intlog;
+  cx.theta = b.theta;
+  cx.lut = b.lut;
+  cx.err = b.err;
+  encode_tile_bf16<B, SR, G, LPG>(in0, tms, gabs < ngroups, gabs, cx, jb.out, tg0, ng);
 }
 
-#ifndef FC2_ENC_STAGES
-#define FC2_ENC_STAGES 1
-#endif
+template <int B, bool SR, int G, int WARPS, int LPG>
+__global__ void __launch_bounds__(WARPS * 32, enc_min_ctas(B, WARPS)) k_encode_grp(const __grid_constant__ EncBatch b) {
+  using IT = GTile<__nv_bfloat16, G, LPG>;
+  constexpr int IN_BYTES = IT::IN_BYTES / LPG;
+  constexpr int TIE_BYTES = G / LPG * 4;               // one 32-bit tie mask per run per lane
+  constexpr int PER_WARP = IN_BYTES + TIE_BYTES;       // plane words go straight to global
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int warp = (int)(threadIdx.x >> 5);
+  uint8_t* in0 = smem + warp * PER_WARP;
+  uint32_t* tms = reinterpret_cast<uint32_t*>(in0 + IN_BYTES);
+  const int64_t nw = (int64_t)gridDim.x * WARPS;
+  for (int64_t t = (int64_t)blockIdx.x * WARPS + warp; t < b.total; t += nw)
+    encode_grp_tile<B, SR, G, LPG>(b, t, in0, tms);
+}
+
 #ifndef FC2_ENC_WARPS
 #define FC2_ENC_WARPS 1  // one-warp CTAs: finest block-scheduling grain for the last wave
 #endif
 #ifndef FC2_ENC_CTAS_PER_SM
-#define FC2_ENC_CTAS_PER_SM 64
+#define FC2_ENC_CTAS_PER_SM 128
 #endif
 
 template <int B, bool SR, int G>
 struct EncGrp {
   static constexpr int WARPS = FC2_ENC_WARPS;
-  static constexpr int STAGES = FC2_ENC_STAGES;
   // the launcher picked b.lpg: enc_lpg(G) for bandwidth, enc_lpg_small(G)
-  // (one 32-element run per lane) when the chunk is smaller than a wave
+  // (one 32-element run per lane; ~2x the instructions per element, 4x the
+  // warps at g = 128) for chunks smaller than a wave
   static int go(const EncBatch& b, cudaStream_t st) {
-    if (b.lpg == enc_lpg_small(G) && enc_lpg_small(G) != enc_lpg(G)) return run<enc_lpg_small(G)>(b, st);
-    return run<enc_lpg(G)>(b, st);
+    constexpr int S = enc_lpg_small(G), L = enc_lpg(G);
+    if (b.lpg == S && S != L) return run<S>(b, st);
+    return run<L>(b, st);
   }
   template <int LPG>
   static int run(const EncBatch& b, cudaStream_t st) {
-    constexpr int SMEM = WARPS * (STAGES * GTile<__nv_bfloat16, G>::IN_BYTES / LPG + G / LPG * 4);
-    constexpr auto kern = k_encode_grp<B, SR, G, WARPS, LPG, STAGES>;
+    constexpr int SMEM = WARPS * (GTile<__nv_bfloat16, G>::IN_BYTES / LPG + G / LPG * 4);
+    constexpr auto kern = k_encode_grp<B, SR, G, WARPS, LPG>;
     smem_attr<kern>(SMEM);
     int64_t blocks = (b.total + WARPS - 1) / WARPS;
     int64_t cap = (int64_t)num_sms() * FC2_ENC_CTAS_PER_SM;
