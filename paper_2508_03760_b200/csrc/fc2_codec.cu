@@ -505,11 +505,13 @@ int fc2_decode(const fc2_config* cfg, const void* payload, int64_t n, void* y, i
 // ---------------------------------------------------------------------------
 // host-buffer pipeline: encode_chunk / decode_chunk / their round trip with
 // the chunk in host memory.  The chunk is cut into slices on tile boundaries;
-// slice k runs on internal stream k % kPipeStreams as
-//   H2D(x slice) -> encode(slice) -> D2H(plane + meta segments of the slice)
-//   [-> decode(slice) -> D2H(y slice)]            (round trip)
-//   H2D(payload segments) -> decode(slice) -> D2H(y slice)   (decode only)
-// so PCIe traffic in both directions overlaps the kernels and each other.
+// slice k goes
+//   H2D(x slice) -> encode(slice) [-> decode(slice)] -> D2H(plane + meta
+//   segments of the slice) [+ D2H(y slice)]
+//   (decode only: H2D(payload segments) -> decode(slice) -> D2H(y slice))
+// with all uploads on one stream, all downloads on another and the kernels on
+// two more, joined by per-slice events, so PCIe traffic in both directions
+// overlaps the kernels and each other.
 // Stream-ordered with respect to the caller's stream (event fork / join).
 // ---------------------------------------------------------------------------
 
@@ -518,11 +520,12 @@ namespace fc2 {
 #ifndef FC2_PIPE_STREAMS
 #define FC2_PIPE_STREAMS 4
 #endif
-constexpr int kPipeStreams = FC2_PIPE_STREAMS;  // s[0]: uploads; s[1..]: kernels + downloads, round robin
+constexpr int kPipeStreams = FC2_PIPE_STREAMS;  // s[0]: uploads; s[1]: downloads; s[2..]: kernels
+static_assert(kPipeStreams >= 3, "host pipeline needs an upload, a download and a kernel stream");
 constexpr int kPipeEvents = 8;
 struct HostPipe {
   cudaStream_t s[kPipeStreams];
-  cudaEvent_t fork, join[kPipeStreams], up[kPipeEvents];
+  cudaEvent_t fork, join[kPipeStreams], up[kPipeEvents], dn[kPipeEvents];
 };
 
 static HostPipe* host_pipe(int* rc) {
@@ -543,7 +546,8 @@ static HostPipe* host_pipe(int* rc) {
     }
     bool ok = cudaEventCreateWithFlags(&p.fork, cudaEventDisableTiming) == cudaSuccess;
     for (int i = 0; i < kPipeEvents; ++i)
-      ok = ok && cudaEventCreateWithFlags(&p.up[i], cudaEventDisableTiming) == cudaSuccess;
+      ok = ok && cudaEventCreateWithFlags(&p.up[i], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&p.dn[i], cudaEventDisableTiming) == cudaSuccess;
     if (!ok) {
       *rc = set_err(FC2_ECUDA, "host pipeline event creation failed");
       return nullptr;
@@ -605,13 +609,14 @@ static int host_pipeline(int mode, const fc2_config* cfg, const void* x_host, in
   if (cudaEventRecord(hp->fork, st) != cudaSuccess) return set_err(FC2_ECUDA, "fork event failed");
   for (int i = 0; i < kPipeStreams; ++i) cudaStreamWaitEvent(hp->s[i], hp->fork, 0);
   const int xs = esize(x_dtype), ys = esize(y_dtype);
-  // uploads stream back to back on s[0] (never queued behind a download);
-  // slice k's kernels and downloads run on s[1 + k % 3] after its upload event
-  cudaStream_t up = hp->s[0];
+  // s[0]: uploads, back to back; s[1]: downloads, in slice order; slice k's
+  // kernels on s[2 + k % 2] between its upload event and its download event.
+  // One stream per copy direction keeps each direction on its own copy engine.
+  cudaStream_t up = hp->s[0], down = hp->s[1];
   int64_t k = 0;
   for (int64_t e0 = 0; e0 < n; e0 += slice, ++k) {
     const int64_t e1 = e0 + slice < n ? e0 + slice : n;
-    cudaStream_t s = hp->s[1 + k % (kPipeStreams - 1)];
+    cudaStream_t s = hp->s[2 + k % (kPipeStreams - 2)];
     if (mode & 5) {
       if (mode & 1) {
         if (cudaMemcpyAsync((uint8_t*)x_dev + e0 * xs, (const uint8_t*)x_host + e0 * xs, (e1 - e0) * xs,
@@ -629,16 +634,21 @@ static int host_pipeline(int mode, const fc2_config* cfg, const void* x_host, in
       rc = encode_batch_impl(cfg, x_dtype, 1, &x_dev, &n, &n, &pay_dev, dev_err, s, &e0, &e1);
       if (rc) return rc;
     }
-    if (mode & 2) {
-      rc = copy_payload_slice(cfg, n, e0, e1, pay_dev, pay_host, cudaMemcpyDeviceToHost, s);
-      if (rc) return rc;
-    }
     if (mode & 8) {
       const void* pd = pay_dev;
       rc = decode_batch_impl(cfg, y_dtype, 1, &pd, &n, &y_dev, &n, dev_err, s, 0, &e0, &e1);
       if (rc) return rc;
-      if (cudaMemcpyAsync((uint8_t*)y_host + e0 * ys, (const uint8_t*)y_dev + e0 * ys, (e1 - e0) * ys,
-                          cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    }
+    if (mode & 10) {
+      cudaEvent_t ev = hp->dn[k % kPipeEvents];
+      if (cudaEventRecord(ev, s) != cudaSuccess || cudaStreamWaitEvent(down, ev, 0) != cudaSuccess)
+        return set_err(FC2_ECUDA, "download event failed");
+      if (mode & 2) {
+        rc = copy_payload_slice(cfg, n, e0, e1, pay_dev, pay_host, cudaMemcpyDeviceToHost, down);
+        if (rc) return rc;
+      }
+      if ((mode & 8) && cudaMemcpyAsync((uint8_t*)y_host + e0 * ys, (const uint8_t*)y_dev + e0 * ys,
+                                        (e1 - e0) * ys, cudaMemcpyDeviceToHost, down) != cudaSuccess)
         return set_err(FC2_ECUDA, "y slice copy failed");
     }
   }
