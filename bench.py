@@ -473,6 +473,22 @@ def run_allreduce(args, rank, world, local_rank):
     launches = lib.fc2_launch_count() - l0
     xb = x.clone()
     ms_nccl = timed(lambda: dist.all_reduce(xb), args.steps, args.warmup) if backend == "nccl" else None
+    # the same NCCL AllReduce with NVLS (NVSwitch in-switch reduction) forced off, on a
+    # second communicator created after the env change (hard part 6)
+    ms_nccl_nonvls = None
+    if backend == "nccl" and os.environ.get("NCCL_NVLS_ENABLE") != "0":
+        prev = os.environ.get("NCCL_NVLS_ENABLE")
+        os.environ["NCCL_NVLS_ENABLE"] = "0"
+        try:
+            g2 = dist.new_group(backend="nccl")
+            ms_nccl_nonvls = timed(lambda: dist.all_reduce(xb, group=g2), args.steps, args.warmup)
+        except Exception:
+            ms_nccl_nonvls = None
+        finally:
+            if prev is None:
+                os.environ.pop("NCCL_NVLS_ENABLE", None)
+            else:
+                os.environ["NCCL_NVLS_ENABLE"] = prev
     # e2e: pinned host in -> allreduce -> host out
     xh = x.cpu().pin_memory()
     yh = torch.empty_like(xh).pin_memory()
@@ -533,7 +549,9 @@ def run_allreduce(args, rank, world, local_rank):
                        "l2": "flushed before every step (256 MiB write, then read back)", "parallelism": f"tp{world}"},
             "nccl_bf16": None if ms_nccl is None else {
                 "ms": round(ms_nccl, 5), "algbw_GBps": round(2 * n / (ms_nccl * 1e-3) / 1e9, 2),
-                "speedup": round(ms_nccl / ms, 3), "nvls_env": os.environ.get("NCCL_NVLS_ENABLE", "default")},
+                "speedup": round(ms_nccl / ms, 3), "nvls_env": os.environ.get("NCCL_NVLS_ENABLE", "default"),
+                "nvls_off_ms": None if ms_nccl_nonvls is None else round(ms_nccl_nonvls, 5),
+                "speedup_vs_nvls_off": None if ms_nccl_nonvls is None else round(ms_nccl_nonvls / ms, 3)},
             "backend": backend,
             "roofline": {"bound": "nvlink", "unit": "GB/s",
                          "achieved": round(2 * (world - 1) / world * F * world / (ms * 1e-3) / 1e9 / world, 2),

@@ -319,19 +319,21 @@ def test_intlog_helpers_match_reference(theta):
         fc.scale_to_int(-1.0)
 
 
-@pytest.mark.parametrize("bits,sr,g,n,slice_elems", [
-    (4, True, 128, 1 << 20, 1 << 16),       # 16 slices over 4 streams
-    (3, False, 128, 3 * 32768 + 4096, 32768),  # ragged last slice, bit-split planes
-    (5, True, 64, 1 << 18, 1 << 22),        # one slice
-    (8, True, 256, 5 * 32768, 32768),
-    (6, False, 96, 96 * 1024, 32768),       # generic group size: slice rounded to lcm
+@pytest.mark.parametrize("bits,sr,g,n,slice_elems,intlog,xdt", [
+    (4, True, 128, 1 << 20, 1 << 16, False, torch.bfloat16),   # 16 slices
+    (3, False, 128, 3 * 32768 + 4096, 32768, False, torch.bfloat16),  # ragged last slice, bit-split planes
+    (5, True, 64, 1 << 18, 1 << 22, False, torch.bfloat16),    # one slice
+    (8, True, 256, 5 * 32768, 32768, False, torch.bfloat16),
+    (6, False, 96, 96 * 1024, 32768, False, torch.bfloat16),   # generic group size: slice rounded to lcm
+    (4, True, 128, 1 << 18, 1 << 16, True, torch.bfloat16),    # INT_LOG metadata
+    (4, True, 128, 1 << 18, 1 << 16, False, torch.float32),    # f32 chunk (k_encode_fast)
 ])
-def test_host_pipeline_matches_device_path(bits, sr, g, n, slice_elems):
+def test_host_pipeline_matches_device_path(bits, sr, g, n, slice_elems, intlog, xdt):
     """encode_host / decode_host / roundtrip_host (fc2_*_host: sliced, PCIe
     overlapped) produce the same payload bytes and values as the device path
     and as the oracle."""
-    cfg = cfg_of(bits, g, sr, False, n)
-    x = torch.from_numpy(O.bf16_snap(O.spiky(n, bits)).astype(np.float32)).to(torch.bfloat16)
+    cfg = cfg_of(bits, g, sr, intlog, n)
+    x = torch.from_numpy(O.bf16_snap(O.spiky(n, bits)).astype(np.float32)).to(xdt)
     xp = x.pin_memory()
     want = fc.encode_payload(x.cuda(), cfg, n).cpu()
     pay = fc.encode_host(xp, cfg, slice_elems=slice_elems)
@@ -342,6 +344,8 @@ def test_host_pipeline_matches_device_path(bits, sr, g, n, slice_elems):
     pay2, y2 = fc.roundtrip_host(xp, cfg, out_dtype=torch.bfloat16, slice_elems=slice_elems)
     assert torch.equal(pay2, want)
     assert torch.equal(y2, ywant.to(torch.bfloat16))
+    if intlog:
+        return  # INT_LOG bytes are pinned against the reference in test_codec_intlog_matches_oracle
     # oracle on a prefix (groups are independent)
     m = 8192 if n >= 8192 else n
     m -= m % g
