@@ -199,7 +199,13 @@ def two_step_stage_times(fc, x, cfg, flush, steps, N=8):
             torch.cuda.current_stream().cuda_stream))
 
     out = {}
-    for name, fn, nbytes in (("reduce_requant_8src", red, N * F + F), ("gather_decode_8shards", gat, N * F + 2 * n)):
+    from paper_2508_03760_b200.collectives import _encode_jobs
+
+    def enc():  # stage 1: this rank's 8 shards into 8 landing slots, one launch
+        _encode_jobs(cfg, 0, [(x.data_ptr() + s * S * 2, S, S, land.data_ptr() + s * slot) for s in range(N)], err)
+
+    for name, fn, nbytes in (("encode_8shards", enc, 2 * n + N * F), ("reduce_requant_8src", red, N * F + F),
+                             ("gather_decode_8shards", gat, N * F + 2 * n)):
         for _ in range(2):
             fn()
         ts = []
