@@ -372,6 +372,23 @@ static int encode_batch_impl(const fc2_config* cfg, int32_t x_dtype, int32_t njo
     b->nj = 0; b->B = B; b->G = G; b->sr = sr; b->intlog = cfg->scale_encoding; b->theta = cfg->theta;
     b->lpg = lpg; b->total = 0; b->lut = lut; b->err = dev_err;
   }
+  auto launch_gen = [&]() -> int {
+    int64_t blocks = (gen.total + 7) / 8;
+    int64_t cap = (int64_t)num_sms() * 8;
+    if (blocks > cap) blocks = cap;
+    if (x_dtype == FC2_BF16) k_encode_gen<__nv_bfloat16><<<(unsigned)blocks, 256, 0, st>>>(gen);
+    else if (x_dtype == FC2_F32) k_encode_gen<float><<<(unsigned)blocks, 256, 0, st>>>(gen);
+    else k_encode_gen<double><<<(unsigned)blocks, 256, 0, st>>>(gen);
+    return cuda_check("k_encode_gen");
+  };
+  // one launch per FC2_KERNEL_JOBS jobs of a kind (small kernel parameters)
+  auto flush = [&](EncBatch& b) -> int {
+    if (!b.nj) return FC2_OK;
+    const int r = &b == &fast ? enc_fast(B, x_dtype, sr, G, fast, st) : launch_gen();
+    b.nj = 0;
+    b.total = 0;
+    return r;
+  };
   for (int i = 0; i < njobs; ++i) {
     if (n[i] < 0 || n[i] % G) return set_err(FC2_ECONFIG, "chunk %lld not a multiple of group_size %d", (long long)n[i], G);
     if (n_valid[i] < 0 || n_valid[i] > n[i]) return set_err(FC2_EDATA, "n_valid %lld outside [0, %lld]", (long long)n_valid[i], (long long)n[i]);
@@ -380,6 +397,7 @@ static int encode_batch_impl(const fc2_config* cfg, int32_t x_dtype, int32_t njo
     const bool aligned = (reinterpret_cast<uintptr_t>(xs[i]) & 15u) == 0 || n_valid[i] == 0;
     const bool use_fast = fast_group(G) && x_dtype != FC2_F64 && aligned;
     EncBatch* b = use_fast ? &fast : &gen;
+    if (b->nj == FC2_KERNEL_JOBS && (rc = flush(*b))) return rc;
     EncJob& j = b->j[b->nj++];
     j.x = xs[i] ? xs[i] : payloads[i];
     j.out = (uint8_t*)payloads[i];
@@ -397,21 +415,8 @@ static int encode_batch_impl(const fc2_config* cfg, int32_t x_dtype, int32_t njo
     b->total += last - first;
     (void)esz;
   }
-  if (fast.nj) {
-    rc = enc_fast(B, x_dtype, sr, G, fast, st);
-    if (rc) return rc;
-  }
-  if (gen.nj) {
-    int64_t blocks = (gen.total + 7) / 8;
-    int64_t cap = (int64_t)num_sms() * 8;
-    if (blocks > cap) blocks = cap;
-    if (x_dtype == FC2_BF16) k_encode_gen<__nv_bfloat16><<<(unsigned)blocks, 256, 0, st>>>(gen);
-    else if (x_dtype == FC2_F32) k_encode_gen<float><<<(unsigned)blocks, 256, 0, st>>>(gen);
-    else k_encode_gen<double><<<(unsigned)blocks, 256, 0, st>>>(gen);
-    rc = cuda_check("k_encode_gen");
-    if (rc) return rc;
-  }
-  return FC2_OK;
+  if ((rc = flush(fast))) return rc;
+  return flush(gen);
 }
 
 }  // namespace fc2
@@ -459,10 +464,30 @@ static int decode_batch_impl(const fc2_config* cfg, int32_t y_dtype, int32_t njo
   b.round_bf16 = round_bf16;
   b.nj = 0; b.B = B; b.G = G; b.sr = cfg->scheme == 1; b.intlog = cfg->scale_encoding; b.theta = cfg->theta;
   b.total = 0; b.lut = lut; b.err = dev_err;
+  // one launch per FC2_KERNEL_JOBS jobs (small kernel parameters)
+  auto flush = [&]() -> int {
+    if (!b.nj) return FC2_OK;
+    int r;
+    if (fastG) {
+      r = dec_fast(B, y_dtype, 0, b, st);
+    } else {
+      int64_t blocks = (b.total + 255) / 256;
+      int64_t cap = (int64_t)num_sms() * 16;
+      if (blocks > cap) blocks = cap;
+      if (y_dtype == FC2_BF16) k_decode_gen<__nv_bfloat16><<<(unsigned)blocks, 256, 0, st>>>(b);
+      else if (y_dtype == FC2_F32) k_decode_gen<float><<<(unsigned)blocks, 256, 0, st>>>(b);
+      else k_decode_gen<double><<<(unsigned)blocks, 256, 0, st>>>(b);
+      r = cuda_check("k_decode_gen");
+    }
+    b.nj = 0;
+    b.total = 0;
+    return r;
+  };
   for (int i = 0; i < njobs; ++i) {
     if (n[i] < 0 || n[i] % G) return set_err(FC2_ECONFIG, "chunk %lld not a multiple of group_size %d", (long long)n[i], G);
     if (n_out[i] < 0 || n_out[i] > n[i]) return set_err(FC2_ECONFIG, "n_out out of range");
     if (n[i] == 0 || n_out[i] == 0) continue;
+    if (b.nj == FC2_KERNEL_JOBS && (rc = flush())) return rc;
     DecJob& j = b.j[b.nj++];
     j.pay = (const uint8_t*)payloads[i];
     j.y = ys[i];
@@ -479,20 +504,7 @@ static int decode_batch_impl(const fc2_config* cfg, int32_t y_dtype, int32_t njo
     j.t0 = b.total - first;
     b.total += last - first;
   }
-  if (!b.nj) return FC2_OK;
-  if (fastG) {
-    int64_t blocks = (b.total + 7) / 8;
-    int64_t cap = (int64_t)num_sms() * 8;
-    if (blocks > cap) blocks = cap;
-return dec_fast(B, y_dtype, blocks, b, st);
-  }
-  int64_t blocks = (b.total + 255) / 256;
-  int64_t cap = (int64_t)num_sms() * 16;
-  if (blocks > cap) blocks = cap;
-  if (y_dtype == FC2_BF16) k_decode_gen<__nv_bfloat16><<<(unsigned)blocks, 256, 0, st>>>(b);
-  else if (y_dtype == FC2_F32) k_decode_gen<float><<<(unsigned)blocks, 256, 0, st>>>(b);
-  else k_decode_gen<double><<<(unsigned)blocks, 256, 0, st>>>(b);
-  return cuda_check("k_decode_gen");
+  return flush();
 }
 
 int fc2_decode(const fc2_config* cfg, const void* payload, int64_t n, void* y, int32_t y_dtype, int64_t n_out,

@@ -36,6 +36,13 @@ inline void smem_attr(int bytes) {
 // job tables (passed by value as __grid_constant__ kernel parameters)
 // ---------------------------------------------------------------------------
 
+// Jobs per launch: the job table travels as a __grid_constant__ kernel
+// parameter, so it is kept small (larger batches become several launches;
+// the public limit per call is FC2_MAX_JOBS).
+#ifndef FC2_KERNEL_JOBS
+#define FC2_KERNEL_JOBS 16
+#endif
+
 struct EncJob {
   const void* x;
   uint8_t* out;
@@ -47,7 +54,7 @@ struct EncBatch {
   int64_t total;
   const double* lut;
   int32_t* err;
-  EncJob j[FC2_MAX_JOBS];
+  EncJob j[FC2_KERNEL_JOBS];
 };
 
 struct DecJob {
@@ -61,7 +68,7 @@ struct DecBatch {
   int64_t total;
   const double* lut;
   int32_t* err;
-  DecJob j[FC2_MAX_JOBS];
+  DecJob j[FC2_KERNEL_JOBS];
 };
 
 #define FC2_MAX_PEERS 16
