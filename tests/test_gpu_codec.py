@@ -110,18 +110,22 @@ def test_codec_bf16_device_matches_oracle(bits, sr, g, kind):
 @pytest.mark.parametrize("bits", [2, 3, 4, 5, 7, 8])
 @pytest.mark.parametrize("sr", [False, True])
 @pytest.mark.parametrize("g", [32, 64, 128, 256])
-def test_codec_bf16_bandwidth_shape_slices(bits, sr, g):
+@pytest.mark.parametrize("extra", [0, 3])
+def test_codec_bf16_bandwidth_shape_slices(bits, sr, g, extra):
     """The same encoder in its bandwidth shape (chunks of >= one resident
     wave of tiles): slices of the payload equal the oracle on the same
-    element slices (groups are independent)."""
-    n = 1 << 23
+    element slices (groups are independent); extra > 0 leaves a partial last
+    warp tile."""
+    if extra and bits not in (3, 4):
+        pytest.skip("partial last tile: two bit widths are enough")
+    n = (1 << 23) + extra * g
     x = torch.from_numpy(O.bf16_snap(O.spiky(n, bits + g)).astype(np.float32)).to(torch.bfloat16)
     cfg = cfg_of(bits, g, sr, False, n)
     ph = fc.encode_payload(x.cuda(), cfg, n).cpu().numpy()
     xs = x.float().numpy()
     rec = 12 if sr else 4
-    for start in (0, 3 * 1024 * 1024 + 8192, n - 16384):
-        m = 16384
+    for start in (0, 3 * 1024 * 1024 + 8192, n - 16384 - extra * g):
+        m = 16384 + (extra * g if start > 3 * 1024 * 1024 + 8192 else 0)
         planes, meta = O.encode(xs[start:start + m], bits, g, sr)
         off = 0
         for w, p in zip(O.UNITS[bits], planes):
