@@ -104,11 +104,6 @@ constexpr float kFixCM = 512.5f + 8.0f / 16384.0f;  // exactly representable
 constexpr uint32_t kTieMask = 0x3FF0u;
 constexpr float kFoldLimit = 1024.0f;               // |off * inv| bound for the folded form
 
-__device__ __forceinline__ uint32_t fix_est(float v, float off32, float inv32) {
-  float d = __fsub_rn(v, off32);
-  float f = __fmaf_rn(d, inv32, kFixC);
-  return __float_as_uint(__fadd_rn(f, kFixMagic));
-}
 __device__ __forceinline__ uint32_t fix_est_clamped(float v, float off32, float inv32, float Lh) {
   float d = __fsub_rn(v, off32);
   float f = __fmaf_rn(d, inv32, kFixC);

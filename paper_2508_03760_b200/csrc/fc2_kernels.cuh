@@ -393,32 +393,6 @@ __device__ __forceinline__ __nv_bfloat16 cvt_out<__nv_bfloat16>(float v) {
   return __ushort_as_bfloat16((unsigned short)bf16_bits(v));  // bfloat16.py:16-25
 }
 
-template <typename OT>
-__device__ __forceinline__ void store_run(OT* y, int64_t e0, int64_t n_out, const float* v) {
-  // 32 values at y[e0..]; vectorized when the whole run is in bounds and aligned
-  constexpr int VE = 16 / sizeof(OT);
-  OT* p = y + e0;
-  if (e0 + 32 <= n_out && (reinterpret_cast<uintptr_t>(p) & 15u) == 0) {
-#pragma unroll
-    for (int i = 0; i < 32; i += VE) {
-      uint4 q;
-      if constexpr (sizeof(OT) == 2) {  // cvt.rn.bf16x2 == bfloat16.py RNE for finite values
-        __nv_bfloat162 h0 = __floats2bfloat162_rn(v[i], v[i + 1]), h1 = __floats2bfloat162_rn(v[i + 2], v[i + 3]);
-        __nv_bfloat162 h2 = __floats2bfloat162_rn(v[i + 4], v[i + 5]), h3 = __floats2bfloat162_rn(v[i + 6], v[i + 7]);
-        q.x = *reinterpret_cast<uint32_t*>(&h0); q.y = *reinterpret_cast<uint32_t*>(&h1);
-        q.z = *reinterpret_cast<uint32_t*>(&h2); q.w = *reinterpret_cast<uint32_t*>(&h3);
-      } else {
-        q.x = __float_as_uint(v[i]); q.y = __float_as_uint(v[i + 1]);
-        q.z = __float_as_uint(v[i + 2]); q.w = __float_as_uint(v[i + 3]);
-      }
-      *reinterpret_cast<uint4*>(p + i) = q;
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < 32; ++i)
-      if (e0 + i < n_out) p[i] = cvt_out<OT>(v[i]);
-  }
-}
 
 // fast decode (G % 32 == 0): lane = 32 consecutive elements (one metadata
 // record per lane), next tile's codes + record prefetched into registers,
@@ -430,29 +404,6 @@ struct RunRegs {
   uint32_t r[3];   // metadata record
 };
 
-template <int B>
-__device__ __forceinline__ void load_run(const uint8_t* pay, int64_t n, int64_t e0, int64_t grp, int rb,
-                                         int64_t meta_off, RunRegs<B>& rr) {
-#pragma unroll
-  for (int u = 0; u < n_units(B); ++u) {
-    const int W = unit_w(B, u), O = unit_off(B, u);
-    const uint8_t* p = pay + (n * O) / 8 + (e0 * W) / 8;  // 4W bytes, >= 4-byte aligned
-    uint32_t* w = rr.w + unit_off(B, u);
-    if (W == 8) {
-      const uint4 a = *reinterpret_cast<const uint4*>(p), b2 = *reinterpret_cast<const uint4*>(p + 16);
-      w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w; w[4] = b2.x; w[5] = b2.y; w[6] = b2.z; w[7] = b2.w;
-    } else if (W == 4) {
-      const uint4 a = *reinterpret_cast<const uint4*>(p);
-      w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
-    } else if (W == 2) {
-      const uint2 a = *reinterpret_cast<const uint2*>(p);
-      w[0] = a.x; w[1] = a.y;
-    } else {
-      w[0] = *reinterpret_cast<const uint32_t*>(p);
-    }
-  }
-  load_record(pay + meta_off + grp * rb, rr.r, rb);
-}
 
 template <int B>
 __device__ __forceinline__ uint32_t code_of(const RunRegs<B>& rr, int k) {
