@@ -315,6 +315,21 @@ def run_codec(args):
         "decode": {"ms": t_dec, "bytes": dec_bytes, "GBps": dec_bytes / (t_dec * 1e-3) / 1e9},
     }
     dom = "encode" if t_enc >= t_dec else "decode"
+    # size-matched context: a plain device copy of the same 64 MiB (read + write
+    # bytes / time), same L2 flush, same event timing
+    yc = torch.empty_like(x)
+    tc = []
+    for i in range(args.steps + 3):
+        flush_l2(flush)
+        a, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        yc.copy_(x)
+        b2.record()
+        torch.cuda.synchronize()
+        if i >= 3:
+            tc.append(a.elapsed_time(b2))
+    copy_gbps = 2 * x.numel() * 2 / (statistics.mean(tc) * 1e-3) / 1e9
+    del yc
     roof = {
         "kernel": "k_encode_grp" if dom == "encode" else "k_decode_fast",
         "bound": "hbm",
@@ -325,6 +340,8 @@ def run_codec(args):
         "frac": kernels[dom]["GBps"] / peak,
         "traffic": _ncu_traffic(f"{dom}_b{args.bits}_{args.scheme}_g{args.group}"),
         "algorithmic_bytes_per_launch": kernels[dom]["bytes"],
+        "copy_same_size_GBps": round(copy_gbps, 1),
+        "frac_of_copy_same_size": round(kernels[dom]["GBps"] / copy_gbps, 4),
     }
     # bit-width sweep (configs[1]): RTN and SR for 2/3/4/5/6/8 bits
     sweep = {}
