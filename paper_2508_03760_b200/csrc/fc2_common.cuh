@@ -282,7 +282,8 @@ __host__ __device__ constexpr int enc_lpg(int G) { return G > FC2_ENC_EPL ? G / 
 // by G / 32 at the cost of a few shuffles per group
 __host__ __device__ constexpr int enc_lpg_small(int G) { return G / 32 > 0 ? G / 32 : 1; }
 #ifndef FC2_ENC_SMALL_TILES
-#define FC2_ENC_SMALL_TILES 1776  // bandwidth tiles below which the small-chunk shape is used (148 SMs x 12)
+#define FC2_ENC_SMALL_TILES 592  // bandwidth tiles below which the small-chunk shape is used (148 SMs x 4;
+                                 // measured crossover ~2.5 Mi elements at g = 128)
 #endif
 
 // store nbytes (<= 12) from words[]; widest stores the alignment allows
