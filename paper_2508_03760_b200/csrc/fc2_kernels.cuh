@@ -40,7 +40,7 @@ inline void smem_attr(int bytes) {
 // parameter, so it is kept small (larger batches become several launches;
 // the public limit per call is FC2_MAX_JOBS).
 #ifndef FC2_KERNEL_JOBS
-#define FC2_KERNEL_JOBS 16
+#define FC2_KERNEL_JOBS 64
 #endif
 
 struct EncJob {
