@@ -1,17 +1,24 @@
-// fc2_codec.cu -- sm_100a kernels and the C ABI for the codec hot path.
+// fc2_codec.cu -- host side of the C ABI for the codec hot path (kernels in
+// fc2_kernels.cuh, instantiated per bit width in fc2_inst_b<B>.cu).
 //
-//   k_encode_fast   encode_chunk (codec.py:477-519) for bf16/f32 input and
-//                   G in {32,64,128,256}: cp.async-staged, warp-tile = 1024
-//                   elements, lane = 32 consecutive elements.
+//   k_encode_grp    encode_chunk (codec.py:477-519) for bf16 input, G in
+//                   {32,64,128,256}: lane-per-group warp tiles, payload words
+//                   stored straight from registers (fc2_encode_group.cuh).
+//   k_encode_fast   the same for f32 input: warp tile = 1024 elements.
 //   k_encode_gen    the same contract for any G (multiple of 8) and f64 input,
 //                   warp-per-group, exact float64.
-//   k_decode_fast   decode_chunk (codec.py:522-563), G % 32 == 0.
+//   k_decode_fast   decode_chunk (codec.py:522-563), G % 32 == 0: lane = 128
+//                   elements, smem-staged coalesced stores.
 //   k_decode_gen    elementwise decode for any G.
-//   k_reduce_fast   two-step middle stage (collectives.py:291-311): decode N
-//                   sources, fp32 rank-order accumulate, re-encode, push to N
-//                   destinations.
-//   k_reduce_gen    the same for any G.
-//   k_pack / k_unpack / bf16 casts: codec.py:204-238, bfloat16.py:16-36.
+//   k_reduce_cta    two-step middle stage (collectives.py:291-311): decode N
+//                   sources, fp32 rank-order accumulate, re-encode, push to up
+//                   to 16 destinations; several shards per launch (one-shot).
+//   k_reduce_fast / k_reduce_grp / k_reduce_gen   fallbacks (misaligned
+//                   sources, > 16 sources, any G).
+//   k_pack / k_unpack / bf16 casts / group and int-log helpers: codec.py:204-238,
+//                   278-392, bfloat16.py:16-36.
+// Host-resident chunks (fc2_*_host) are sliced and pipelined over internal
+// streams (see host_pipeline below).
 #include <cstdarg>
 #include <cstdio>
 #include <utility>

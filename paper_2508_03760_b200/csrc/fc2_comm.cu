@@ -7,6 +7,7 @@
 //   [4096, 4096 + N*slot)          landing slots  land[src]   (stage 1, my shard)
 //   [.., + N*slot)                 gather slots   gath[owner] (stage 2)
 //   [.., + a2a_bytes)              All2All receive region
+//   [.., + (2N^2 + N)*slot_os)     one-shot region (landing[parity][src][shard], results)
 //
 // Two-step AllReduce on rank r (collectives.py:263-315, one call):
 //   1. one batched encode launch quantizes shard j of x straight into
