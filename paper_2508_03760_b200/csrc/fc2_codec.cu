@@ -542,6 +542,9 @@ namespace fc2 {
 constexpr int kPipeStreams = FC2_PIPE_STREAMS;  // s[0]: uploads; s[1]: downloads; s[2..]: kernels
 static_assert(kPipeStreams >= 3, "host pipeline needs an upload, a download and a kernel stream");
 constexpr int kPipeEvents = 8;
+#ifndef FC2_PIPE_PAYLOAD_LAST
+#define FC2_PIPE_PAYLOAD_LAST 1
+#endif
 struct HostPipe {
   cudaStream_t s[kPipeStreams];
   cudaEvent_t fork, join[kPipeStreams], up[kPipeEvents], dn[kPipeEvents];
@@ -662,7 +665,7 @@ static int host_pipeline(int mode, const fc2_config* cfg, const void* x_host, in
       cudaEvent_t ev = hp->dn[k % kPipeEvents];
       if (cudaEventRecord(ev, s) != cudaSuccess || cudaStreamWaitEvent(down, ev, 0) != cudaSuccess)
         return set_err(FC2_ECUDA, "download event failed");
-      if (mode & 2) {
+      if ((mode & 2) && !(FC2_PIPE_PAYLOAD_LAST && (mode & 8))) {
         rc = copy_payload_slice(cfg, n, e0, e1, pay_dev, pay_host, cudaMemcpyDeviceToHost, down);
         if (rc) return rc;
       }
@@ -670,6 +673,12 @@ static int host_pipeline(int mode, const fc2_config* cfg, const void* x_host, in
                                         (e1 - e0) * ys, cudaMemcpyDeviceToHost, down) != cudaSuccess)
         return set_err(FC2_ECUDA, "y slice copy failed");
     }
+  }
+  // round trip: the payload comes back in one copy per plane + one for the
+  // metadata after the last slice (fewer, larger DMA transfers)
+  if (FC2_PIPE_PAYLOAD_LAST && (mode & 2) && (mode & 8)) {
+    rc = copy_payload_slice(cfg, n, 0, n, pay_dev, pay_host, cudaMemcpyDeviceToHost, down);
+    if (rc) return rc;
   }
   for (int i = 0; i < kPipeStreams; ++i) {
     cudaEventRecord(hp->join[i], hp->s[i]);
