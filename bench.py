@@ -618,6 +618,25 @@ def _ref_slice(bounds):
     return b - a
 
 
+_REF_RANKS = None  # padded float32 payloads of the simulated ranks (forked workers)
+
+
+def _ref_shard(job):
+    """One shard of the reference two-step (collectives.py:278-311) in a pool
+    worker: every source's QDQ of the shard summed in fp32 in rank order from
+    +0, then the owner's QDQ of the sum -- the same arithmetic as
+    oracle.two_step, one shard per process."""
+    import numpy as np
+
+    from oracle import fc2_oracle as O
+
+    shard, S, bits, g, sr = job
+    acc = np.zeros(S, dtype=np.float32)
+    for src in range(len(_REF_RANKS)):
+        acc += O.qdq_f32(_REF_RANKS[src][shard * S:(shard + 1) * S], bits, g, sr)[0]
+    return O.qdq_f32(acc, bits, g, sr)[0]
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -627,17 +646,32 @@ def run_reference(args, rank, world):
     from oracle import fc2_oracle as O
     import numpy as np
 
+    cores = 1
     if world > 1:
-        # two-step AllReduce of the oracle on a bounded per-rank sample
+        # two-step AllReduce of the oracle on a bounded per-rank sample, one
+        # shard per pool process (shards are independent, collectives.py:276)
+        import multiprocessing as mproc
+
+        global _REF_RANKS
         payloads = [O.bf16_snap(O.spiky(n_sample, s)).astype(np.float32) for s in O.child_seeds(0, world)]
-        for i in range(args.warmup + args.steps):
-            t0 = time.perf_counter()
-            O.two_step(payloads, args.bits, args.group, sr)
-            if i >= args.warmup:
-                times.append(time.perf_counter() - t0)
+        mult = world * args.group
+        padded = -(-n_sample // mult) * mult
+        _REF_RANKS = [np.pad(p, (0, padded - n_sample)) for p in payloads]
+        S = padded // world
+        cores = max(1, min(os.cpu_count() or 1, world))
+        with mproc.get_context("fork").Pool(cores) as pool:
+            for i in range(args.warmup + args.steps):
+                t0 = time.perf_counter()
+                shards = pool.map(_ref_shard, [(j, S, args.bits, args.group, sr) for j in range(world)])
+                out = O.bf16_snap(np.concatenate(shards)[:n_sample])
+                if i >= args.warmup:
+                    times.append(time.perf_counter() - t0)
+        want, _ = O.two_step(payloads, args.bits, args.group, sr)
+        assert np.array_equal(out, want[0]), "pooled reference differs from oracle.two_step"
         dt = statistics.mean(times)
         value = 2 * n_sample * world / dt / 1e9
-        what = f"oracle two_step over {world} simulated ranks x {n_sample} elements"
+        what = (f"oracle two-step over {world} simulated ranks x {n_sample} elements, one shard per "
+                f"process ({cores} processes)")
     else:
         # the full 64 MiB workload, split into group-aligned slices over a pool
         # of forked processes (all host cores; the reference is single-threaded
@@ -661,7 +695,7 @@ def run_reference(args, rank, world):
         value = 2 * n_sample / dt / 1e9
         what = (f"oracle encode+decode of the full {n_sample}-element bf16 workload in {len(parts)} "
                 f"group-aligned slices over a pool of {cores} processes")
-    cb = {"value": round(value, 5), "unit": "GB/s", "cores": 1 if world > 1 else cores, "kind": "port",
+    cb = {"value": round(value, 5), "unit": "GB/s", "cores": cores, "kind": "port",
           "sample": what + " (numpy restatement of the pure-Python reference; numpy elementwise is single-threaded)"}
     line = {
         "impl": "reference",
