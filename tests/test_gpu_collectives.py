@@ -168,3 +168,33 @@ def test_reduce_requant_batch_equals_per_shard(bits, g, sr, S, stride_pad):
     assert int(err.item()) == 0
     for k in range(K):
         assert torch.equal(got[k * slot:k * slot + F], want[k * slot:k * slot + F])
+
+
+def test_reduce_requant_batch_rejects_bad_shapes():
+    import ctypes
+
+    from paper_2508_03760_b200 import _lib
+
+    c = cfg(4, 128, True).c_struct()
+    buf = torch.zeros(1 << 16, dtype=torch.uint8, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    ptrs = _lib.ptr_array([buf.data_ptr()])
+    # nshard < 1 and a shard that is not a group multiple are ConfigErrors, like fc2_reduce_requant
+    with pytest.raises(fc.ConfigError):
+        _lib.check(_lib.lib().fc2_reduce_requant_batch(ctypes.byref(c), 1, ptrs, 1024, 0, 0, 1, ptrs, 0,
+                                                       err.data_ptr(), st))
+    with pytest.raises(fc.ConfigError):
+        _lib.check(_lib.lib().fc2_reduce_requant_batch(ctypes.byref(c), 1, ptrs, 1000, 2, 4096, 1, ptrs, 4096,
+                                                       err.data_ptr(), st))
+
+
+def test_host_entry_points_validate_buffers():
+    c = cfg(4, 128, True)
+    x = torch.zeros(4096, dtype=torch.bfloat16).pin_memory()
+    with pytest.raises(TypeError):
+        fc.roundtrip_host(x.cuda(), c)
+    with pytest.raises(fc.DecodeFormatError):
+        fc.decode_host(torch.zeros(16, dtype=torch.uint8).pin_memory(), c, 4096)
+    with pytest.raises(fc.ConfigError):
+        fc.encode_host(torch.zeros(1000, dtype=torch.bfloat16).pin_memory(), c)  # not a group multiple
