@@ -223,11 +223,9 @@ __global__ void __launch_bounds__(kEncWarps * 32) k_encode_fast(const __grid_con
 // ---------------------------------------------------------------------------
 
 template <int G, int LPG>
-__device__ __forceinline__ void issue_grp_tile(const EncBatch& b, int64_t t, uint8_t* stage) {
+__device__ __forceinline__ void issue_grp_tile(const EncJob& jb, int64_t t, uint8_t* stage) {
   using IT = GTile<__nv_bfloat16, G, LPG>;
   constexpr int GPT = 32 / LPG;  // groups per warp tile
-  const int ji = find_job(b, t);
-  const EncJob& jb = b.j[ji];
   const int64_t e0 = (t - jb.t0) * GPT * G;
   const int lane = (int)lane_id();
   const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(jb.x);
@@ -280,13 +278,12 @@ template <int B, bool SR, int G, int LPG>
 __device__ __forceinline__ void encode_grp_tile(const EncBatch& b, int64_t t, uint8_t* in0, uint32_t* tms) {
   constexpr int GPT = 32 / LPG;  // groups per warp tile
   const int lane = (int)lane_id();
+  const EncJob& jb = b.j[find_job(b, t)];  // one lookup per tile
   __syncwarp();  // previous tile fully consumed
-  issue_grp_tile<G, LPG>(b, t, in0);
+  issue_grp_tile<G, LPG>(jb, t, in0);
   cp_async_commit();
   cp_async_wait<0>();
   __syncwarp();
-  const int ji = find_job(b, t);
-  const EncJob& jb = b.j[ji];
   const int64_t ngroups = jb.n / G;
   const int64_t tg0 = (t - jb.t0) * GPT;
   const int64_t gabs = tg0 + lane / LPG;
