@@ -165,6 +165,14 @@ int fc2_group_decode_raw(const uint8_t* codes, int64_t n, double scale, double z
 int fc2_scale_to_int(const double* s, int64_t n, int32_t theta, int8_t* out, int32_t* dev_err, void* stream);
 int fc2_int_to_scale(const double* si, int64_t n, int32_t theta, double* out, void* stream);
 
+/* Exact copy of n elements with the collectives' float32 staging
+ * (collectives.py:160: cast to float32; :162-163: non-finite -> DataError via
+ * FC2_ERR_NONFINITE in dev_err): the All2All diagonal block, which never
+ * crosses a wire (collectives.py:466-468).  Output bf16 is the RNE rounding of
+ * the float32 value (exact for bf16 input). */
+int fc2_copy_check(const void* x, int32_t x_dtype, void* y, int32_t y_dtype, int64_t n, int32_t* dev_err,
+                   void* stream);
+
 /* bfloat16.py:16-36 on device arrays. */
 int fc2_f32_to_bf16_bits(const float* x, int64_t n, uint16_t* out, void* stream);
 int fc2_bf16_bits_to_f32(const uint16_t* x, int64_t n, float* out, void* stream);
@@ -207,10 +215,14 @@ int fc2_allreduce_oneshot(fc2_comm* c, const fc2_config* cfg, const void* x, int
                           int32_t* dev_err, double timeout_s, void* stream);
 
 /* Quantized All2All (dispatch, collectives.py:428-482; combine = transposed
- * matrix).  matrix: host int64[world*world] element counts.  The diagonal
- * block is left to the caller (exact copy, collectives.py:466-468). */
+ * matrix).  matrix: host int64[world*world] element counts.  Remote blocks are
+ * encoded straight into the receiver's All2All region [region_off,
+ * region_off + region_bytes) of the symmetric buffer (FC2_ECONFIG when they do
+ * not fit it); the diagonal block is an exact copy (collectives.py:466-468)
+ * whose non-finite values are flagged like the encoder's (:152-164). */
 int fc2_a2a_q(fc2_comm* c, const fc2_config* cfg, const void* x, int32_t x_dtype, const int64_t* matrix,
-              void* y, int32_t y_dtype, int64_t region_off, int32_t* dev_err, double timeout_s, void* stream);
+              void* y, int32_t y_dtype, int64_t region_off, int64_t region_bytes, int32_t* dev_err,
+              double timeout_s, void* stream);
 
 /* Diagnostics. */
 const char* fc2_last_error(void);

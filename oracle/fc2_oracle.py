@@ -323,6 +323,45 @@ def two_step(payloads, bits, g, sr, intlog=False, theta=10):
     return [out.copy() for _ in range(N)], nbytes
 
 
+def hierarchical(payloads, groups, bits, g, sr, intlog=False, theta=10):
+    """Hierarchical quantized AllReduce over two NUMA islands joined by a
+    bridge (collectives.py:318-425).  ``groups``: the two equal-size lists of
+    device ids (cross_numa_partition order).  Stage rs: scatter-reduce inside
+    each island (every member QDQs every segment, fp32 sum in member order from
+    +0).  Stage xn: paired ranks i (island 0) / j (island 1) swap opposite
+    halves -- total_low = low_i + QDQ(low_j), total_high = high_j + QDQ(high_i)
+    -- and both keep QDQ(total_low) ++ QDQ(total_high).  Stage ag: every owner
+    QDQs its segment once more and its island decodes it.  bf16 out, padding
+    stripped."""
+    ranks = _as_f32_payloads(payloads)
+    N = len(ranks)
+    gsz = len(groups[0])
+    n = ranks[0].size
+    mult = N * g
+    padded = -(-n // mult) * mult
+    ranks = [np.pad(p, (0, padded - n)) for p in ranks]
+    seg = padded // gsz
+    half = seg // 2
+    q = lambda v: qdq_f32(v, bits, g, sr, intlog, theta)[0]
+    reduced = {}
+    for members in groups:
+        for li, owner in enumerate(members):
+            acc = np.zeros(seg, dtype=np.float32)
+            for src in members:
+                acc += q(ranks[src][li * seg:(li + 1) * seg])
+            reduced[owner] = acc
+    final = {}
+    for i, j in zip(groups[0], groups[1]):
+        total_low = reduced[i][:half] + q(reduced[j][:half])
+        total_high = reduced[j][half:] + q(reduced[i][half:])
+        final[i] = final[j] = np.concatenate([q(total_low), q(total_high)])
+    outs = []
+    for r in range(N):
+        members = groups[0] if r in groups[0] else groups[1]
+        outs.append(bf16_snap(np.concatenate([q(final[o]) for o in members])[:n]))
+    return outs
+
+
 def a2a_dispatch(payloads, bits, g, sr, matrix=None, intlog=False, theta=10):
     """Quantized All2All dispatch (collectives.py:428-482, rule R15).
 

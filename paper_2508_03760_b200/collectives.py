@@ -28,7 +28,7 @@ import torch
 from . import _device, _lib
 from .config import QuantConfig, footprint_bytes
 from .errors import ConfigError, DataError, NotApplicableError
-from .topology import Topology
+from .topology import Topology, cross_numa_partition
 
 RAW_BYTES_PER_ELEMENT = 2  # bf16 wire baseline (collectives.py:26)
 _SLOT_ALIGN = 16
@@ -310,12 +310,112 @@ def two_step_allreduce_q(payloads, topo: Topology, config: QuantConfig) -> Colle
 
 
 def hierarchical_two_step_q(payloads, topo: Topology, config: QuantConfig) -> CollectiveResult:
-    """The reference's NUMA-bridge variant (collectives.py:318-425) needs a PCIe
-    NUMA bridge; a B200 NVSwitch box has none, so -- exactly like the
-    reference on NVLink presets (topology.py:250-258) -- this raises."""
-    raise NotApplicableError(
-        f"topology {topo.name!r}: hierarchical two-step needs a NUMA bridge; "
-        "B200 NVSwitch fabrics are uniform (use two_step_allreduce_q)")
+    """Quantized AllReduce over two NUMA islands joined by a bridge
+    (collectives.py:318-425): scatter-reduce inside each island, a half-segment
+    swap between paired ranks across the bridge, all-gather inside each island.
+
+    Every quantize-dequantize runs on the GPU codec (batched encode + decode
+    launches per stage, the encode of stage s+1 fed by the fp32 sums of stage
+    s); the fp32 sums keep the reference's order (member order from +0.0, then
+    ``mine + peer``).  Raises NotApplicableError without a bridge -- a B200
+    NVSwitch box has none, where ``two_step_allreduce_q`` is the algorithm.
+    """
+    groups, _bridge = cross_numa_partition(topo)
+    if len(groups) != 2 or len(groups[0]) != len(groups[1]):
+        raise ConfigError("hierarchical all-reduce needs two equal NUMA groups")
+    N = topo.n_devices
+    gsz = len(groups[0])
+    xs, device_in, dev = _stage_payloads(payloads, N)
+    n = xs[0].numel()
+    padded = _round_up(n, N * config.group_size)
+    seg = padded // gsz
+    half = seg // 2
+    f_seg, f_half = footprint_bytes(config, seg), footprint_bytes(config, half)
+    xp = []
+    for x in xs:  # zero padding (collectives.py:167-172), float32 like _check_payloads
+        t = torch.zeros(padded, dtype=torch.float32, device=dev)
+        t[:n] = x
+        xp.append(t)
+
+    def qdq(blocks):
+        return _quantized_blocks(config, [(0, 0, b) for b in blocks], dev)[0] if blocks else []
+
+    trace, ledger = StageTrace(), TrafficLedger(topo)
+
+    # ---- stage rs: scatter-reduce inside each island
+    st = trace.stage("rs")
+    reduced = {}
+    for members in groups:
+        dq = qdq([xp[src][li * seg:(li + 1) * seg] for src in members for li in range(gsz)])
+        for a, src in enumerate(members):
+            for li, owner in enumerate(members):
+                st.computes.append(ComputeEvent(st.name, 0, src, "quantize", seg))
+                if src != owner:
+                    ev = TransferEvent(st.name, 1, src, owner, seg, f_seg)
+                    st.transfers.append(ev)
+                    ledger.record(ev)
+                st.computes.append(ComputeEvent(st.name, 2, owner, "dequantize", seg))
+        for li, owner in enumerate(members):
+            acc = torch.zeros(seg, dtype=torch.float32, device=dev)
+            for a in range(gsz):
+                acc += dq[a * gsz + li]
+            reduced[owner] = acc
+            st.computes.append(ComputeEvent(st.name, 3, owner, "reduce", gsz * seg))
+
+    # ---- stage xn: paired ranks swap opposite halves across the bridge
+    st = trace.stage("xn")
+    pairs = list(zip(groups[0], groups[1]))
+    first = qdq([b for i, j in pairs for b in (reduced[i][half:], reduced[j][:half])])
+    totals = []
+    for k, (i, j) in enumerate(pairs):
+        dq_high_i, dq_low_j = first[2 * k], first[2 * k + 1]
+        totals += [reduced[i][:half] + dq_low_j, reduced[j][half:] + dq_high_i]
+    second = qdq(totals)
+    final = {}
+    for k, (i, j) in enumerate(pairs):
+        st.computes.append(ComputeEvent(st.name, 0, i, "quantize", half))
+        for ev in (TransferEvent(st.name, 1, i, j, half, f_half),):
+            st.transfers.append(ev)
+            ledger.record(ev)
+        st.computes.append(ComputeEvent(st.name, 0, j, "quantize", half))
+        ev = TransferEvent(st.name, 1, j, i, half, f_half)
+        st.transfers.append(ev)
+        ledger.record(ev)
+        st.computes += [ComputeEvent(st.name, 2, i, "dequantize", half), ComputeEvent(st.name, 2, j, "dequantize", half),
+                        ComputeEvent(st.name, 3, i, "reduce", 2 * half), ComputeEvent(st.name, 3, j, "reduce", 2 * half),
+                        ComputeEvent(st.name, 4, i, "quantize", half)]
+        ev = TransferEvent(st.name, 5, i, j, half, f_half)
+        st.transfers.append(ev)
+        ledger.record(ev)
+        st.computes.append(ComputeEvent(st.name, 4, j, "quantize", half))
+        ev = TransferEvent(st.name, 5, j, i, half, f_half)
+        st.transfers.append(ev)
+        ledger.record(ev)
+        st.computes += [ComputeEvent(st.name, 6, i, "dequantize", half), ComputeEvent(st.name, 6, j, "dequantize", half)]
+        final[i] = final[j] = torch.cat([second[2 * k], second[2 * k + 1]])
+
+    # ---- stage ag: all-gather inside each island
+    st = trace.stage("ag")
+    outs = {}
+    for members in groups:
+        dq = qdq([final[o] for o in members])
+        merged = torch.cat(dq)
+        for li, owner in enumerate(members):
+            st.computes.append(ComputeEvent(st.name, 0, owner, "quantize", seg))
+            for dst in members:
+                if dst != owner:
+                    ev = TransferEvent(st.name, 1, owner, dst, seg, f_seg)
+                    st.transfers.append(ev)
+                    ledger.record(ev)
+                st.computes.append(ComputeEvent(st.name, 2, dst, "dequantize", seg))
+        y = torch.empty(n, dtype=torch.bfloat16, device=dev)
+        if n:
+            _lib.check(_lib.lib().fc2_f32_to_bf16_bits(merged.data_ptr(), n, y.data_ptr(), _device.stream_handle()))
+        out = y.to(torch.float32)
+        for dst in members:
+            outs[dst] = out
+    outputs = [outs[r].clone() if device_in else outs[r].cpu().numpy() for r in range(N)]
+    return CollectiveResult(outputs, ledger, trace)
 
 
 # ---------------------------------------------------------------------------
@@ -370,6 +470,17 @@ def _quantized_blocks(config: QuantConfig, blocks, dev):
     return outs, [F for (_, F, _) in metas]
 
 
+def _exact_block(v: torch.Tensor, err: torch.Tensor) -> torch.Tensor:
+    """A block that never crosses a wire (diagonal, collectives.py:466-468):
+    exact float32 copy; non-finite values set the DataError bit
+    (collectives.py:152-164 checks every payload before dispatch)."""
+    out = torch.empty(v.numel(), dtype=torch.float32, device=v.device)
+    if v.numel():
+        _lib.check(_lib.lib().fc2_copy_check(v.data_ptr(), _device.dtype_code(v), out.data_ptr(), _lib.F32,
+                                              v.numel(), err.data_ptr(), _device.stream_handle()))
+    return out
+
+
 def all2all_dispatch_q(payloads, topo: Topology, config: QuantConfig, dispatch_matrix=None) -> CollectiveResult:
     """Quantized All2All dispatch (collectives.py:428-482, rule R15).
 
@@ -392,11 +503,12 @@ def all2all_dispatch_q(payloads, topo: Topology, config: QuantConfig, dispatch_m
     trace, ledger = StageTrace(), TrafficLedger(topo)
     st = trace.stage("dispatch")
     out = [[None] * N for _ in range(N)]
+    err = _device.new_err(dev)
     for src in range(N):
         for dst in range(N):
             v = views[(src, dst)]
             if src == dst or v.numel() == 0:
-                out[dst][src] = v.to(torch.float32).clone()
+                out[dst][src] = _exact_block(v, err)
                 continue
             o, f = got[(src, dst)]
             st.computes.append(ComputeEvent(st.name, 0, src, "quantize", v.numel()))
@@ -405,6 +517,7 @@ def all2all_dispatch_q(payloads, topo: Topology, config: QuantConfig, dispatch_m
             ledger.record(ev)
             st.computes.append(ComputeEvent(st.name, 2, dst, "dequantize", v.numel()))
             out[dst][src] = o
+    _device.check_err(err)
     if not device_in:
         out = [[t.cpu().numpy() for t in row] for row in out]
     return CollectiveResult(out, ledger, trace)
@@ -429,11 +542,12 @@ def all2all_combine_q(blocks, topo: Topology, config: QuantConfig) -> Collective
     trace, ledger = StageTrace(), TrafficLedger(topo)
     st = trace.stage("combine")
     out = [[None] * N for _ in range(N)]
+    err = _device.new_err(dev)
     for src in range(N):
         for dst in range(N):
             v = views[(src, dst)]
             if src == dst or v.numel() == 0:
-                out[dst][src] = v.to(torch.float32).clone()
+                out[dst][src] = _exact_block(v, err)
                 continue
             o, f = got[(src, dst)]
             st.computes.append(ComputeEvent(st.name, 0, src, "quantize", v.numel()))
@@ -442,6 +556,7 @@ def all2all_combine_q(blocks, topo: Topology, config: QuantConfig) -> Collective
             ledger.record(ev)
             st.computes.append(ComputeEvent(st.name, 2, dst, "dequantize", v.numel()))
             out[dst][src] = o
+    _device.check_err(err)
     if not device_in:
         out = [[t.cpu().numpy() for t in row] for row in out]
     return CollectiveResult(out, ledger, trace)

@@ -153,6 +153,37 @@ __global__ void k_bf16_to_f32(const uint16_t* x, int64_t n, float* y) {
     y[i] = bf16_val(x[i]);
 }
 
+// exact block copy with the collectives' float32 staging (collectives.py:160:
+// every payload is cast to float32 first, then checked for non-finite values,
+// :162-163) -- the All2All diagonal block (:466-468), which never crosses a wire
+__device__ __forceinline__ float cc_f32(__nv_bfloat16 v) { return __bfloat162float(v); }
+__device__ __forceinline__ float cc_f32(float v) { return v; }
+__device__ __forceinline__ float cc_f32(double v) { return __double2float_rn(v); }
+__device__ __forceinline__ void cc_put(__nv_bfloat16* y, float v) { *y = __ushort_as_bfloat16((unsigned short)bf16_bits(v)); }
+__device__ __forceinline__ void cc_put(float* y, float v) { *y = v; }
+__device__ __forceinline__ void cc_put(double* y, float v) { *y = (double)v; }
+
+template <typename TI, typename TO>
+__global__ void k_copy_check(const TI* __restrict__ x, TO* __restrict__ y, int64_t n, int32_t* err) {
+  bool bad = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = cc_f32(x[i]);
+    bad |= !isfinite(v);
+    cc_put(y + i, v);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(err, FC2_ERR_NONFINITE);
+}
+
+template <typename TI>
+static int launch_copy_check(const void* x, void* y, int32_t y_dtype, int64_t n, int32_t* err, cudaStream_t st) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
+  const TI* xi = (const TI*)x;
+  if (y_dtype == FC2_BF16) k_copy_check<<<(unsigned)blocks, 256, 0, st>>>(xi, (__nv_bfloat16*)y, n, err);
+  else if (y_dtype == FC2_F32) k_copy_check<<<(unsigned)blocks, 256, 0, st>>>(xi, (float*)y, n, err);
+  else k_copy_check<<<(unsigned)blocks, 256, 0, st>>>(xi, (double*)y, n, err);
+  return cuda_check("k_copy_check");
+}
 
 // ---------------------------------------------------------------------------
 // per-group scalar API (codec.py:278-343) and int-log scales (codec.py:366-392)
@@ -465,8 +496,14 @@ static int decode_batch_impl(const fc2_config* cfg, int32_t y_dtype, int32_t njo
   const int B = cfg->bitwidth, G = cfg->group_size;
   // fast decode: G % 32 == 0, bf16/f32 output, payloads 16-byte aligned
   bool fastG = y_dtype != FC2_F64 && G % 32 == 0;
-  for (int i = 0; i < njobs; ++i)
+  for (int i = 0; i < njobs; ++i) {
     if (reinterpret_cast<uintptr_t>(payloads[i]) & 15u) fastG = false;
+    // the fast decoder cp.asyncs 16-byte chunks of every plane: each plane's
+    // offset n * unit_off / 8 must be 16-byte aligned too (B = 3, 7 with
+    // n % 64 != 0, e.g. G = 32 and an odd group count, is not)
+    for (int u = 1; u < n_units(B); ++u)
+      if ((n[i] * unit_off(B, u) / 8) & 15) fastG = false;
+  }
   DecBatch b;
   b.round_bf16 = round_bf16;
   b.nj = 0; b.B = B; b.G = G; b.sr = cfg->scheme == 1; b.intlog = cfg->scale_encoding; b.theta = cfg->theta;
@@ -798,6 +835,16 @@ int fc2_f32_to_bf16_bits(const float* x, int64_t n, uint16_t* out, void* stream)
   if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
   k_f32_to_bf16<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(x, n, out);
   return cuda_check("k_f32_to_bf16");
+}
+
+int fc2_copy_check(const void* x, int32_t x_dtype, void* y, int32_t y_dtype, int64_t n, int32_t* dev_err,
+                   void* stream) {
+  if (x_dtype < 0 || x_dtype > 2 || y_dtype < 0 || y_dtype > 2) return set_err(FC2_ECONFIG, "bad dtype");
+  if (n <= 0) return FC2_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (x_dtype == FC2_BF16) return launch_copy_check<__nv_bfloat16>(x, y, y_dtype, n, dev_err, st);
+  if (x_dtype == FC2_F32) return launch_copy_check<float>(x, y, y_dtype, n, dev_err, st);
+  return launch_copy_check<double>(x, y, y_dtype, n, dev_err, st);
 }
 
 int fc2_bf16_bits_to_f32(const uint16_t* x, int64_t n, float* out, void* stream) {

@@ -279,7 +279,8 @@ int fc2_allreduce_oneshot(fc2_comm* c, const fc2_config* cfg, const void* x, int
 //    (y_dtype F32 or BF16); the diagonal block is NOT written here (exact copy,
 //    done by the caller).  region_off: byte offset of the All2All region.
 int fc2_a2a_q(fc2_comm* c, const fc2_config* cfg, const void* x, int32_t x_dtype, const int64_t* matrix,
-              void* y, int32_t y_dtype, int64_t region_off, int32_t* dev_err, double timeout_s, void* stream) {
+              void* y, int32_t y_dtype, int64_t region_off, int64_t region_bytes, int32_t* dev_err,
+              double timeout_s, void* stream) {
   const int N = c->world, r = c->rank;
   int rc = fc2_check_config(cfg);
   if (rc) return rc;
@@ -298,10 +299,15 @@ int fc2_a2a_q(fc2_comm* c, const fc2_config* cfg, const void* x, int32_t x_dtype
     }
     return off;
   };
-  for (int d = 0; d < N; ++d) {  // capacity check of every receiver's region
+  if (region_off < 0 || region_bytes < 0 || region_off + region_bytes + FC2_FLAG_BYTES > c->bytes)
+    return set_err(FC2_ECONFIG, "a2a region [%lld, +%lld) outside the communicator buffer", (long long)region_off,
+                   (long long)region_bytes);
+  for (int d = 0; d < N; ++d) {  // every receiver's blocks must fit the All2All region itself
     int64_t F = 0;
     int64_t end = slot_off(d, N - 1, &F) + F;
-    if (region_off + end + FC2_FLAG_BYTES > c->bytes) return set_err(FC2_ECONFIG, "a2a region too small");
+    if (end > region_bytes)
+      return set_err(FC2_ECONFIG, "All2All blocks for rank %d need %lld bytes; the All2All region holds %lld", d,
+                     (long long)end, (long long)region_bytes);
   }
   std::vector<const void*> xs;
   std::vector<int64_t> nv, ns;
@@ -348,6 +354,17 @@ int fc2_a2a_q(fc2_comm* c, const fc2_config* cfg, const void* x, int32_t x_dtype
     rc = fc2_decode_batch(cfg, y_dtype, nj, ps.data() + i, pn.data() + i, ys.data() + i, po.data() + i, dev_err,
                           stream);
     if (rc) return rc;
+  }
+  // diagonal block: exact copy, non-finite values flagged (collectives.py:152-164, 466-468)
+  {
+    int64_t so = 0, ro = 0;
+    for (int d = 0; d < r; ++d) so += matrix[(int64_t)r * N + d];
+    for (int s = 0; s < r; ++s) ro += matrix[(int64_t)s * N + r];
+    const int64_t m = matrix[(int64_t)r * N + r];
+    if (m > 0) {
+      rc = fc2_copy_check((const uint8_t*)x + so * esz, x_dtype, (uint8_t*)y + ro * ysz, y_dtype, m, dev_err, stream);
+      if (rc) return rc;
+    }
   }
   // everyone has consumed its region before anyone writes the next call's blocks
   return fc2_comm_barrier(c, dev_err, timeout_s, stream);

@@ -126,7 +126,10 @@ class CudaCodec:
             _device.stream_handle()))
 
     def check(self) -> None:
-        _device.check_err(self.err)
+        bits = int(self.err.item())
+        if bits:
+            self.err.zero_()  # later calls start from a clean word
+            _lib.raise_dev_err(bits)
 
 
 def two_step_via_collectives(x: torch.Tensor, codec, lay: TwoStepLayout, group=None,
@@ -170,7 +173,8 @@ class QComm:
         self.a2a_off = 2 * self.world * self.max_lay.slot_bytes
         # one-shot region (small messages): 2 N^2 landing slots + N result slots
         self.os_lay = TwoStepLayout.make(min(int(oneshot_max_elems), max_elems), self.world, self.cfg)
-        self.os_off = self.a2a_off + _round_up(int(a2a_bytes), _SLOT_ALIGN)
+        self.a2a_bytes = _round_up(int(a2a_bytes), _SLOT_ALIGN)
+        self.os_off = self.a2a_off + self.a2a_bytes
         self.codec = CudaCodec(self.cfg, self.device)
         self.err = self.codec.err
         self._c = None
@@ -232,7 +236,7 @@ class QComm:
         else:
             two_step_via_collectives(x, self.codec, lay, self.group, y)
         if check:
-            self.codec.check()
+            self.check()
         return y
 
     def all2all(self, x: torch.Tensor, matrix, out: torch.Tensor | None = None,
@@ -256,19 +260,24 @@ class QComm:
         x = x.reshape(-1).contiguous()
         c = self.cfg.c_struct()
         mp = m.reshape(-1)
+        # remote blocks into the receivers' All2All regions, the diagonal block
+        # copied exactly (non-finite values flagged, collectives.py:152-164)
         _lib.check(_lib.lib().fc2_a2a_q(
             self._c, ctypes.byref(c), x.data_ptr(), _device.dtype_code(x),
             mp.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), y.data_ptr(), _device.dtype_code(y),
-            self.a2a_off, self.err.data_ptr(), self.timeout_s, _device.stream_handle()))
-        # diagonal block: exact copy (collectives.py:466-468)
-        so = int(m[r, :r].sum())
-        ro = int(m[:r, r].sum())
-        d = int(m[r, r])
-        if d:
-            y[ro:ro + d].copy_(x[so:so + d])
+            self.a2a_off, self.a2a_bytes, self.err.data_ptr(), self.timeout_s, _device.stream_handle()))
         if check:
-            self.codec.check()
+            self.check()
         return y
+
+    def check(self) -> None:
+        """Raise for any error bit the device set since the last check (the
+        reference's DataError / DecodeFormatError, or a cross-rank timeout), then
+        clear the word so later calls start clean.  Synchronizes the stream."""
+        bits = int(self.err.item())
+        if bits:
+            self.err.zero_()
+            _lib.raise_dev_err(bits)
 
     def close(self) -> None:
         if self._c is not None:

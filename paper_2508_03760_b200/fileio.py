@@ -93,8 +93,12 @@ def quantize_tensor(values, config: QuantConfig, device_payload: bool = False) -
         raise DataError(f"tensor has {n} elements, not a multiple of group size {config.group_size}")
     bounds = list(_chunk_bounds(n, config.chunk_size))
     sizes = [footprint_bytes(config, s) for _, s in bounds]
-    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
-    out = torch.empty(int(offs[-1]), dtype=torch.uint8, device=dev)
+    # every chunk gets a 16-byte aligned slot (the encoder stores whole words;
+    # footprints such as 19 or 1938 bytes are not word multiples); the chunks
+    # are sliced back to their exact footprints below
+    slots = [(f + 15) // 16 * 16 for f in sizes]
+    offs = np.concatenate([[0], np.cumsum(slots)]).astype(np.int64)
+    out = torch.empty(max(int(offs[-1]), 1), dtype=torch.uint8, device=dev)
     err = _device.new_err(dev)
     es = x.element_size()
     jobs = [(x.data_ptr() + p * es, s, s, out.data_ptr() + int(offs[i])) for i, (p, s) in enumerate(bounds)]
@@ -104,12 +108,12 @@ def quantize_tensor(values, config: QuantConfig, device_payload: bool = False) -
     if device_payload:
         for i, (_, s) in enumerate(bounds):
             chunks.append(QuantizedChunk(replace(config, chunk_size=s), element_count=s,
-                                         payload=out[int(offs[i]):int(offs[i + 1])]))
+                                         payload=out[int(offs[i]):int(offs[i]) + sizes[i]]))
         return chunks
     host = out.cpu().numpy()
     for i, (_, s) in enumerate(bounds):
         c = QuantizedChunk(replace(config, chunk_size=s), element_count=s,
-                           payload=torch.from_numpy(host[int(offs[i]):int(offs[i + 1])]))
+                           payload=torch.from_numpy(host[int(offs[i]):int(offs[i]) + sizes[i]]))
         c._materialize()
         c._payload = None
         chunks.append(c)
@@ -135,7 +139,12 @@ def dequantize_chunks(chunks, out_dtype=np.float64):
         for c in host:
             if len(c.planes) != len(bit_split(c.config.bitwidth)):
                 raise DecodeFormatError("chunk plane count does not match its bitwidth")
-        blob = np.frombuffer(b"".join(b"".join(c.planes) + c.meta for c in host), dtype=np.uint8)
+        # each chunk at a 16-byte aligned slot so the vectorised decoder applies
+        parts = []
+        for c in host:
+            b = b"".join(c.planes) + c.meta
+            parts.append(b + bytes(-len(b) % 16))
+        blob = np.frombuffer(b"".join(parts), dtype=np.uint8)
         dblob = torch.from_numpy(blob.copy()).to(dev)
     groups: dict = {}
     hoff = 0
@@ -147,7 +156,7 @@ def dequantize_chunks(chunks, out_dtype=np.float64):
             if c.payload_nbytes != want:
                 raise DecodeFormatError(f"chunk {i} holds {c.payload_nbytes} payload bytes, expected {want}")
             ptr = dblob.data_ptr() + hoff
-            hoff += want
+            hoff += (want + 15) // 16 * 16
         key = replace(c.config, chunk_size=c.config.group_size)
         groups.setdefault(key, []).append((ptr, c.element_count, y.data_ptr() + int(pos[i]) * y.element_size(),
                                            c.element_count))

@@ -263,7 +263,49 @@ def file_fixture():
     return len(index)
 
 
+def hier_fixture():
+    """hierarchical_two_step_q (collectives.py:318-425) on bridged fabrics:
+    the 8-GPU L40 preset and a 4-GPU two-island JSON fabric."""
+    four = qcomm.Topology.from_json({
+        "name": "pcie4",
+        "devices": [{"id": i, "sm_count": 142, "numa_group": i // 2} for i in range(4)],
+        "links": [{"name": f"pcie{i}", "kind": "PCIe", "a": f"gpu{i}", "b": f"numa{i // 2}", "bandwidth": 64e9}
+                  for i in range(4)] + [{"name": "bridge", "kind": "NumaBridge", "a": "numa0", "b": "numa1",
+                                          "bandwidth": 32e9}]})
+    cases = [
+        # (topology, n, bits, g, sr, seed)
+        ("L40", 16384, 4, 128, True, 20),
+        ("L40", 5000, 3, 128, True, 21),
+        ("L40", 8192, 2, 32, False, 22),
+        ("pcie4", 3000, 5, 64, True, 23),
+        ("pcie4", 4096, 8, 128, False, 24),
+    ]
+    arrays, index = {}, []
+    for tname, n, bits, g, sr, seed in cases:
+        topo = preset(tname) if tname == "L40" else four
+        N = topo.n_devices
+        cfg = QuantConfig(bits, group_size=g, scheme=Scheme.SPIKE_RESERVING if sr else Scheme.RTN)
+        payloads = [bf16_round(gen_synthetic(default_spiky_spec(n, s))).astype(np.float32)
+                    for s in rank_seeds(seed, N)]
+        res = qcomm.hierarchical_two_step_q(payloads, topo, cfg)
+        rep = volume_report(res.ledger, topo)
+        key = f"hier_{tname}_n{n}_b{bits}_g{g}_{'sr' if sr else 'rtn'}"
+        arrays[f"in_{key}"] = np.stack(payloads)
+        arrays[f"out_{key}"] = np.stack(res.outputs)
+        index.append(dict(key=key, topo=tname, N=N, n=n, bits=bits, g=g, sr=sr, report=rep,
+                          events=[[e.stage, e.wave, e.src, e.dst, e.elements, e.actual_bytes]
+                                  for e in res.ledger.events],
+                          stages=[[st.name, len(st.transfers), len(st.computes)] for st in res.trace.stages]))
+    arrays["index"] = np.frombuffer(json.dumps(index).encode(), dtype=np.uint8)
+    arrays["topo_pcie4"] = np.frombuffer(json.dumps(four.to_json()).encode(), dtype=np.uint8)
+    np.savez_compressed(OUT / "hier_golden.npz", **arrays)
+    return len(index)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["hier"]:
+        print("hierarchical cases", hier_fixture())
+        sys.exit(0)
     print("file cases", file_fixture())
     print("group cases", group_fixture())
     print("codec cases", codec_fixture())

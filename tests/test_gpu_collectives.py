@@ -198,3 +198,31 @@ def test_host_entry_points_validate_buffers():
         fc.decode_host(torch.zeros(16, dtype=torch.uint8).pin_memory(), c, 4096)
     with pytest.raises(fc.ConfigError):
         fc.encode_host(torch.zeros(1000, dtype=torch.bfloat16).pin_memory(), c)  # not a group multiple
+
+
+HIER, HIER_IDX = load("hier_golden.npz")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", HIER_IDX, ids=lambda c: c["key"])
+def test_hierarchical_matches_reference(case):
+    """hierarchical_two_step_q on the GPU codec == the reference's outputs,
+    ledger events and volume report on bridged fabrics (collectives.py:318-425)."""
+    import json
+
+    topo = fc.preset("L40") if case["topo"] == "L40" else fc.Topology.from_json(
+        json.loads(bytes(HIER["topo_pcie4"]).decode()))
+    payloads = list(HIER["in_" + case["key"]])
+    c = fc.QuantConfig(case["bits"], group_size=case["g"],
+                       scheme=fc.Scheme.SPIKE_RESERVING if case["sr"] else fc.Scheme.RTN)
+    res = fc.hierarchical_two_step_q(payloads, topo, c)
+    want = HIER["out_" + case["key"]]
+    for r in range(case["N"]):
+        assert np.array_equal(res.outputs[r], want[r])
+    got_ev = [[e.stage, e.wave, e.src, e.dst, e.elements, e.actual_bytes] for e in res.ledger.events]
+    assert got_ev == case["events"]
+    assert [[s.name, len(s.transfers), len(s.computes)] for s in res.trace.stages] == case["stages"]
+    assert fc.volume_report(res.ledger, topo) == case["report"]
+    # device-resident payloads give the same values
+    dres = fc.hierarchical_two_step_q([torch.from_numpy(p).cuda() for p in payloads], topo, c)
+    assert np.array_equal(dres.outputs[0].cpu().numpy(), want[0])

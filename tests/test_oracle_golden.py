@@ -162,3 +162,20 @@ def test_oracle_intlog_helpers_match_reference(theta):
     assert np.array_equal(O.int_to_scale(np.arange(-128, 128), theta), GRP[f"i2s_t{theta}"])
     # known points (test_intlog_scale.py:15-20)
     assert int(O.scale_to_int(1.0)) == 0 and int(O.scale_to_int(2.0)) == 10 and int(O.scale_to_int(0.3)) == -17
+
+
+HIER, HIER_IDX = load("hier_golden.npz")
+
+
+@pytest.mark.parametrize("case", HIER_IDX, ids=lambda c: c["key"])
+def test_oracle_hierarchical_matches_reference(case):
+    """oracle.hierarchical == the reference's hierarchical_two_step_q
+    (collectives.py:318-425) on the L40 preset and a 4-GPU bridged fabric."""
+    payloads = list(HIER["in_" + case["key"]])
+    N = case["N"]
+    half = N // 2
+    groups = [list(range(half)), list(range(half, N))]
+    outs = O.hierarchical(payloads, groups, case["bits"], case["g"], case["sr"])
+    want = HIER["out_" + case["key"]]
+    for r in range(N):
+        assert np.array_equal(outs[r], want[r])
