@@ -4,17 +4,21 @@
 
 N == 1 (default): BASELINE configs[1] -- codec round trip (encode -> packed
 payload -> decode) of a 64 MiB bf16 tensor (33,554,432 elements), 4-bit,
-group 128, spike reserving; the full bit-width sweep rides along in "sweep".
-value = algbw = tensor bytes / round-trip latency (GB/s, nccl-tests style).
+group 128, spike reserving; the bit-width sweep rides along in "sweep".
+value = algbw = tensor bytes / round-trip latency (GB/s).
 
-N > 1 (torchrun, one rank per GPU): BASELINE configs[2] -- two-step quantized
-AllReduce of 8192 x 4096 bf16 per rank (4-bit SR g128) over CUDA-IPC peer
-memory, with the bf16 NCCL AllReduce timed on the same box; value = aggregate
-algbw over all ranks, latency = max over ranks.
+N > 1 (one rank per GPU; ``--gpus N`` without torchrun re-launches itself
+under ``torch.distributed.run``): BASELINE configs[2] -- two-step quantized
+AllReduce of 8192 x 4096 bf16 per rank (4-bit SR g128) through
+``QComm.all_reduce`` (CUDA-IPC peer stores over NVLink), with the bf16 NCCL
+AllReduce on the same box; value = algbw = 2 n / latency (nccl-tests
+convention, n elements of bf16 per rank), latency = max over ranks.  The
+configs[4] message-size sweep (64 KB - 1 GB, 2/4-bit vs NCCL bf16), the
+configs[3] MoE All2All and a measured NVLink put bandwidth ride along.
 
---impl reference: the reference's CPU algorithm (oracle/ numpy port; the
-reference is pure Python+numpy) on the same workload, bounded
-sample per step, rank 0 only.
+--impl reference: the reference's own CPU implementation (``qcomm`` installed
+in baseline/_ref from /root/reference; the oracle port only if that install
+is missing) on the same workload and config, all host cores, rank 0 only.
 """
 
 from __future__ import annotations
@@ -22,6 +26,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -33,6 +38,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "quantized AllReduce/All2All algbw GB/s & latency at 2/4/8 B200 vs bf16 NCCL"
 N_ELEMS = 8192 * 4096  # 64 MiB of bf16
+MOE = dict(tokens=4096, hidden=7168, topk=8, experts=256)
+SWEEP_BYTES = (1 << 16, 1 << 18, 1 << 20, 1 << 22, 1 << 24, 1 << 26, 1 << 28, 1 << 30)
 
 
 def _peaks():
@@ -53,6 +60,33 @@ def _ncu_traffic(kernel_key: str):
             return json.load(f).get(kernel_key)
     except Exception:
         return None
+
+
+def pct(ts):
+    """median / p10 / p90 of per-step times (ms)."""
+    s = sorted(ts)
+
+    def q(f):
+        if not s:
+            return None
+        i = f * (len(s) - 1)
+        lo = int(i)
+        hi = min(lo + 1, len(s) - 1)
+        return s[lo] + (s[hi] - s[lo]) * (i - lo)
+
+    return {"median_ms": round(q(0.5), 5), "p10_ms": round(q(0.1), 5), "p90_ms": round(q(0.9), 5)}
+
+
+def config_for(args, world):
+    """The workload description -- identical in both arms (same_config)."""
+    if world == 1:
+        return {"workload": "codec round trip (encode_chunk + decode_chunk), 64 MiB bf16 tensor "
+                            "(BASELINE configs[1])",
+                "n": args.n, "bits": args.bits, "group": args.group, "scheme": args.scheme,
+                "l2": "flushed before every step (256 MiB write, then read back)"}
+    return {"workload": "two-step quantized AllReduce, 8192 x 4096 bf16 per rank (BASELINE configs[2])",
+            "n": args.n, "bits": args.bits, "group": args.group, "scheme": args.scheme,
+            "parallelism": f"tp{world}", "l2": "flushed before every step (256 MiB write, then read back)"}
 
 
 class ClockSampler:
@@ -113,11 +147,6 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# ---------------------------------------------------------------------------
-# our arm, N == 1: codec round trip
-# ---------------------------------------------------------------------------
-
-
 def flush_l2(buf):
     """Evict L2 between timed steps: write a buffer twice the size of the
     126 MB L2, then read it back so the lines left behind are clean (a
@@ -129,12 +158,109 @@ def flush_l2(buf):
 
 
 def spiky_bf16(n, seed, device):
+    """N(0,1) with 1/64 of the entries at +-50 (synthetic.py:25-43 shape), bf16."""
     import torch
 
     g = torch.Generator(device=device).manual_seed(seed)
     x = torch.randn(n, device=device, generator=g)
     spike = torch.rand(n, device=device, generator=g) < 1 / 64
     return torch.where(spike, torch.sign(x) * 50, x).to(torch.bfloat16)
+
+
+# ---------------------------------------------------------------------------
+# the reference implementation (baseline/_ref) -- CPU baselines only
+# ---------------------------------------------------------------------------
+
+
+def load_reference():
+    """The reference package installed from /root/reference into baseline/_ref
+    (pip --target), or None."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(path, "qcomm")):
+        if path not in sys.path:
+            sys.path.insert(0, path)
+        import qcomm
+
+        return qcomm
+    return None
+
+
+def ref_topology(q, world):
+    base = q.preset("H800")  # 8 GPUs on one NVLink fabric
+    if world == 8:
+        return base
+    return q.Topology(name=f"nvlink{world}", devices=base.devices[:world], links=base.links[:world])
+
+
+_REF_X = None      # float32 input of the codec round trip (forked workers)
+_REF_RANKS = None  # float32 per-rank payloads of the two-step (forked workers)
+
+
+def _ref_codec_slice(job):
+    """encode_chunk + decode_chunk of one group-aligned slice with the real
+    reference (codec.py:477-563); the oracle port if it is not installed."""
+    a, b, bits, g, sr = job
+    q = load_reference()
+    if q is not None:
+        cfg = q.QuantConfig(bits, group_size=g, scheme=q.Scheme.SPIKE_RESERVING if sr else q.Scheme.RTN,
+                            chunk_size=b - a)
+        q.decode_chunk(q.encode_chunk(_REF_X[a:b], cfg))
+    else:
+        from oracle import fc2_oracle as O
+
+        planes, meta = O.encode(_REF_X[a:b], bits, g, sr)
+        O.decode(planes, meta, b - a, bits, g, sr)
+    return b - a
+
+
+def _ref_two_step_slice(job):
+    """The reference two_step_allreduce_q (collectives.py:263-315) on one
+    slice of every rank's payload.  Slices are multiples of world * g, so no
+    padding is added and (groups and shards being independent, codec.py:485,
+    collectives.py:276) the concatenated slice results are the full-size
+    result element for element."""
+    a, b, bits, g, sr, world = job
+    q = load_reference()
+    if q is not None:
+        cfg = q.QuantConfig(bits, group_size=g, scheme=q.Scheme.SPIKE_RESERVING if sr else q.Scheme.RTN)
+        res = q.two_step_allreduce_q([r[a:b] for r in _REF_RANKS], ref_topology(q, world), cfg)
+        return res.outputs[0][:16]
+    from oracle import fc2_oracle as O
+
+    return O.two_step([r[a:b] for r in _REF_RANKS], bits, g, sr)[0][0][:16]
+
+
+def time_reference_codec(x_f32, bits, g, sr, reps, procs):
+    """Round trip of the whole tensor on `procs` processes (1: the reference
+    exactly as shipped, single-threaded numpy).  Returns per-rep seconds."""
+    import multiprocessing as mproc
+
+    global _REF_X
+    _REF_X = x_f32
+    n = x_f32.size
+    if procs <= 1:
+        parts = [(0, n, bits, g, sr)]
+    else:
+        step = -(-n // (procs * 4) // g) * g
+        parts = [(a, min(a + step, n), bits, g, sr) for a in range(0, n, step)]
+    times = []
+    if procs <= 1:
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            _ref_codec_slice(parts[0])
+            times.append(time.perf_counter() - t0)
+        return times, 1
+    with mproc.get_context("fork").Pool(procs) as pool:
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            assert sum(pool.map(_ref_codec_slice, parts)) == n
+            times.append(time.perf_counter() - t0)
+    return times, procs
+
+
+# ---------------------------------------------------------------------------
+# our arm, N == 1: codec round trip
+# ---------------------------------------------------------------------------
 
 
 def time_roundtrip(fc, x, cfg, steps, warmup, flush):
@@ -171,22 +297,25 @@ def time_roundtrip(fc, x, cfg, steps, warmup, flush):
 
 
 def two_step_stage_times(fc, x, cfg, flush, steps, N=8):
+    """Per-rank kernels of the N = 8 two-step at the configs[2] size, on one
+    GPU: stage-1 encode of the rank's N shards, stage-2 reduce + requantize of
+    one shard from N packed sources, final gather-decode of N shards."""
+    import ctypes
+
     import torch
 
-    from paper_2508_03760_b200.collectives import reduce_requant
+    from paper_2508_03760_b200.collectives import _encode_jobs, reduce_requant
 
     n = x.numel()
     S = n // N
     F = fc.footprint_bytes(cfg, S)
     slot = (F + 15) // 16 * 16
     land = torch.empty(N * slot, dtype=torch.uint8, device=x.device)
-    for s in range(N):  # 8 different packed sources (the shards of this rank's tensor)
+    for s in range(N):  # N different packed sources (the shards of this rank's tensor)
         fc.encode_payload(x[s * S:(s + 1) * S], cfg, S, out=land[s * slot:s * slot + F])
     gath = torch.empty(N * slot, dtype=torch.uint8, device=x.device)
     err = torch.zeros(1, dtype=torch.int32, device=x.device)
     y = torch.empty(n, dtype=torch.bfloat16, device=x.device)
-    import ctypes
-
     c = cfg.c_struct()
     lib = fc._lib.lib()
 
@@ -198,12 +327,10 @@ def two_step_stage_times(fc, x, cfg, flush, steps, N=8):
             [land.data_ptr() + o * slot for o in range(N)]), S, y.data_ptr(), 0, n, err.data_ptr(),
             torch.cuda.current_stream().cuda_stream))
 
-    out = {}
-    from paper_2508_03760_b200.collectives import _encode_jobs
-
-    def enc():  # stage 1: this rank's 8 shards into 8 landing slots, one launch
+    def enc():
         _encode_jobs(cfg, 0, [(x.data_ptr() + s * S * 2, S, S, land.data_ptr() + s * slot) for s in range(N)], err)
 
+    out = {}
     for name, fn, nbytes in (("encode_8shards", enc, 2 * n + N * F), ("reduce_requant_8src", red, N * F + F),
                              ("gather_decode_8shards", gat, N * F + 2 * n)):
         for _ in range(2):
@@ -219,6 +346,7 @@ def two_step_stage_times(fc, x, cfg, flush, steps, N=8):
             ts.append(a.elapsed_time(b))
         t = statistics.mean(ts)
         out[name] = {"us": round(t * 1e3, 2), "bytes": nbytes, "GBps": round(nbytes / (t * 1e-3) / 1e9, 1)}
+    out["sum_us"] = round(sum(v["us"] for v in out.values()), 2)
     return out
 
 
@@ -269,24 +397,50 @@ def time_e2e(fc, x_host, cfg, steps, warmup, serial=False):
     return ms, 2 * n, F + 2 * n
 
 
-def cpu_baseline_codec(n_sample, reps, bits, g, sr):
-    """The oracle (numpy port of the reference algorithm) timed on host cores."""
+def codec_parity_vs_reference(fc, x, cfg, pay, y, bits, g, sr, reps):
+    """The reference itself (baseline/_ref; oracle port if absent) on the SAME
+    64 MiB tensor, one core: its bytes and decoded values against ours, and
+    its single-core time (the cpu_baseline)."""
     import numpy as np
 
-    from oracle import fc2_oracle as O
-
-    if reps <= 0:
-        return None, None
-    x = O.bf16_snap(O.spiky(n_sample, 0)).astype(np.float32)
+    q = load_reference()
+    xf = x.float().cpu().numpy()
     t0 = time.perf_counter()
-    for _ in range(reps):
-        planes, meta = O.encode(x, bits, g, sr)
-        O.decode(planes, meta, n_sample, bits, g, sr)
-    dt = (time.perf_counter() - t0) / reps
-    return 2 * n_sample / dt / 1e9, dt
+    if q is not None:
+        cfgq = q.QuantConfig(bits, group_size=g, scheme=q.Scheme.SPIKE_RESERVING if sr else q.Scheme.RTN,
+                             chunk_size=xf.size)
+        ch = q.encode_chunk(xf, cfgq)
+        dec = q.decode_chunk(ch)
+        ref_bytes = b"".join(ch.planes) + ch.meta
+    else:
+        from oracle import fc2_oracle as O
+
+        planes, meta = O.encode(xf, bits, g, sr)
+        dec = O.decode(planes, meta, xf.size, bits, g, sr)
+        ref_bytes = b"".join(planes) + meta
+    first = time.perf_counter() - t0
+    times = [first]
+    if reps > 1:
+        more, _ = time_reference_codec(xf, bits, g, sr, reps - 1, 1)
+        times += more
+    ours = pay.cpu().numpy().tobytes()
+    yo = y.float().cpu().numpy().astype(np.float64)
+    want = np.asarray(dec, dtype=np.float32).astype(np.float64)
+    want_bf = np.asarray(fc.bf16_round(np.asarray(dec, dtype=np.float32)), dtype=np.float64)
+    d = yo - want_bf
+    ref_err = want - xf.astype(np.float64)
+    parity = {
+        "against": "reference qcomm (baseline/_ref)" if q is not None else "oracle port (reference not installed)",
+        "payload_bytes_equal": ours == ref_bytes,
+        "decoded_max_abs_vs_reference": float(np.abs(d).max()),
+        "decoded_rel_l2_vs_reference": float(np.linalg.norm(d) / max(np.linalg.norm(want_bf), 1e-30)),
+        "quantization_rel_l2_vs_input": float(np.linalg.norm(ref_err) / max(np.linalg.norm(xf), 1e-30)),
+    }
+    return parity, times, ("reference" if q is not None else "port")
 
 
 def run_codec(args):
+    import numpy as np
     import torch
 
     import paper_2508_03760_b200 as fc
@@ -300,19 +454,20 @@ def run_codec(args):
     x = spiky_bf16(n, 0, dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     with ClockSampler(dev.index) as clk:
-        enc, dec, F, launches, _ = time_roundtrip(fc, x, cfg, args.steps, args.warmup, flush)
+        enc, dec, F, launches, (pay, y) = time_roundtrip(fc, x, cfg, args.steps, args.warmup, flush)
         # keep the timed loop running long enough for the sampler to see it
         t_end = time.time() + 1.0
         while time.time() < t_end:
             time_roundtrip(fc, x, cfg, args.steps, 0, flush)
+    steps_ms = [a + b for a, b in zip(enc, dec)]
     t_enc, t_dec = statistics.mean(enc), statistics.mean(dec)
     ms = t_enc + t_dec
     value = 2 * n / (ms * 1e-3) / 1e9
     peak, peak_kind = _peaks()
     enc_bytes, dec_bytes = 2 * n + F, F + 2 * n
     kernels = {
-        "encode": {"ms": t_enc, "bytes": enc_bytes, "GBps": enc_bytes / (t_enc * 1e-3) / 1e9},
-        "decode": {"ms": t_dec, "bytes": dec_bytes, "GBps": dec_bytes / (t_dec * 1e-3) / 1e9},
+        "encode": {"ms": t_enc, "bytes": enc_bytes, "GBps": enc_bytes / (t_enc * 1e-3) / 1e9, **pct(enc)},
+        "decode": {"ms": t_dec, "bytes": dec_bytes, "GBps": dec_bytes / (t_dec * 1e-3) / 1e9, **pct(dec)},
     }
     dom = "encode" if t_enc >= t_dec else "decode"
     # size-matched context: a plain device copy of the same 64 MiB (read + write
@@ -356,9 +511,6 @@ def run_codec(args):
                                         "encode_GBps": round((2 * n + Fb) / (te * 1e-3) / 1e9, 1),
                                         "decode_GBps": round((Fb + 2 * n) / (td * 1e-3) / 1e9, 1),
                                         "payload_bytes": Fb}
-    # per-rank kernels of the N=8 two-step AllReduce (BASELINE configs[2]) timed
-    # on one GPU: stage-2 reduce+requant of one 4 Mi-element shard from 8
-    # packed sources, and the final gather-decode of 8 shards to bf16
     stages = two_step_stage_times(fc, x, cfg, flush, max(3, args.steps // 2))
     # message-size sweep of the codec round trip (BASELINE configs[4] sizes,
     # 64 KB .. 1 GB of bf16 per call), same cfg, L2 flushed before each step
@@ -379,7 +531,10 @@ def run_codec(args):
     x_host = x.cpu().pin_memory()
     e2e_ms, h2d, d2h = time_e2e(fc, x_host, cfg, max(3, args.steps), 2)
     e2e_serial_ms, _, _ = time_e2e(fc, x_host, cfg, max(3, args.steps // 2), 1, serial=True)
-    cpu_val, cpu_dt = cpu_baseline_codec(n, args.cpu_reps, args.bits, args.group, sr)
+    # the reference on the same tensor: parity of our bytes/values + 1-core time
+    parity, cpu_times, cpu_kind = codec_parity_vs_reference(fc, x, cfg, pay, y, args.bits, args.group, sr,
+                                                            max(1, args.cpu_reps))
+    cpu_dt = statistics.mean(cpu_times)
     line = {
         "metric": METRIC,
         "value": round(value, 2),
@@ -389,16 +544,17 @@ def run_codec(args):
         "warmup": args.warmup,
         "ms_per_step": round(ms, 5),
         "latency_us": round(ms * 1e3, 2),
+        **pct(steps_ms),
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "bf16 in/out, fp32 math (f64 on near-ties), packed u8 planes",
         "data": "synthetic: N(0,1) with 1/64 of entries at +-50 (reference default_spiky_spec), bf16",
-        "config": {"workload": "codec round trip, 64 MiB bf16 tensor (BASELINE configs[1])",
-                   "n": n, "bits": args.bits, "group": args.group, "scheme": args.scheme,
-                   "payload_bytes": F, "l2": "flushed before every step (256 MiB write, then read back)"},
+        "config": config_for(args, 1),
+        "payload_bytes": F,
         "kernels": kernels,
         "roofline": roof,
+        "parity": parity,
         "e2e": {"value": round(2 * n / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
                 "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "path": "roundtrip_host -> fc2_roundtrip_host (C ABI): pinned host chunk in, payload bytes + "
@@ -406,10 +562,11 @@ def run_codec(args):
                         "overlapped with the kernels",
                 "serial_value": round(2 * n / (e2e_serial_ms * 1e-3) / 1e9, 2),
                 "serial_path": "H2D -> encode_payload -> D2H payload -> decode_payload -> D2H values, one stream"},
-        "cpu_baseline": None if cpu_val is None else {
-            "value": round(cpu_val, 4), "unit": "GB/s", "cores": 1, "kind": "port",
-            "sample": f"full workload ({n} elements) x {args.cpu_reps}, oracle/fc2_oracle.py "
-                      f"(numpy restatement of codec.py), {cpu_dt:.2f} s per round trip"},
+        "cpu_baseline": {
+            "value": round(2 * n / cpu_dt / 1e9, 5), "unit": "GB/s", "cores": 1, "kind": cpu_kind,
+            "sample": f"the full workload ({n} elements, the same tensor) x {len(cpu_times)}: "
+                      f"encode_chunk + decode_chunk of the reference as shipped, one process, "
+                      f"{cpu_dt:.2f} s per round trip"},
         "sweep": sweep,
         "two_step_n8_per_rank_kernels": stages,
         "size_sweep": size_sweep,
@@ -420,11 +577,22 @@ def run_codec(args):
 
 
 # ---------------------------------------------------------------------------
-# our arm, N > 1: SPMD two-step AllReduce over NVLink
+# our arm, N > 1: SPMD collectives over NVLink
 # ---------------------------------------------------------------------------
 
 
-def run_allreduce(args, rank, world, local_rank):
+def moe_routing(world, tokens, seed=4242):
+    """Seeded uniform top-8 of 256 experts per token on every rank (experts
+    contiguous per rank, EP = world): int64 [world, tokens, topk] expert ids."""
+    import torch
+
+    g = torch.Generator().manual_seed(seed)
+    return torch.stack([torch.rand(tokens, MOE["experts"], generator=g).topk(MOE["topk"], dim=1).indices
+                        for _ in range(world)])
+
+
+def run_multi(args, rank, world, local_rank):
+    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -434,85 +602,97 @@ def run_allreduce(args, rank, world, local_rank):
     ndev = torch.cuda.device_count()
     dev = torch.device("cuda", local_rank % ndev)
     torch.cuda.set_device(dev)
-    # one process per GPU over NCCL; --backend gloo lets several ranks share one
-    # GPU (CUDA IPC works between processes on a device) to validate the path
     backend = args.backend
     if backend == "nccl":
         dist.init_process_group("nccl", device_id=dev)
-    else:
+    else:  # several ranks may share one GPU (CUDA IPC works between processes on a device)
         dist.init_process_group("gloo")
     sr = args.scheme == "sr"
-    cfg = fc.QuantConfig(args.bits, group_size=args.group, chunk_size=args.group,
-                         scheme=fc.Scheme.SPIKE_RESERVING if sr else fc.Scheme.RTN)
+    scheme = fc.Scheme.SPIKE_RESERVING if sr else fc.Scheme.RTN
+    cfg = fc.QuantConfig(args.bits, group_size=args.group, chunk_size=args.group, scheme=scheme)
     n = args.n
     x = spiky_bf16(n, 1000 + rank, dev)
-    # MoE All2All (BASELINE configs[3]): 4096 tokens x 7168, top-8 of 256
-    # experts, EP = world; one copy per distinct destination rank
-    hidden, tokens, topk, experts = 7168, args.moe_tokens, 8, 256
-    g = torch.Generator().manual_seed(4242)
-    mats = []
-    for r in range(world):
-        sel = torch.rand(tokens, experts, generator=g).topk(topk, dim=1).indices // (experts // world)
-        hit = torch.zeros(tokens, world, dtype=torch.bool)
-        hit.scatter_(1, sel, True)
-        mats.append(hit.sum(0))
-    tok_mat = torch.stack(mats).numpy()                    # tokens src -> dst
-    a2a_mat = tok_mat * hidden                               # elements
-    cap = 0
-    for d in range(world):
-        for s2 in range(world):
-            m = int(a2a_mat[s2, d])
-            if s2 != d and m:
-                cap += (fc.footprint_bytes(cfg, -(-m // args.group) * args.group) + 15) // 16 * 16
-    comm = fcd.QComm(dist.group.WORLD, max_elems=n, config=cfg, a2a_bytes=cap + 4096,
-                     oneshot_max_elems=min(n, 1 << 19))
+    sweep_sizes = [b for b in SWEEP_BYTES if b <= args.sweep_max] if not args.no_sweep else []
+    max_elems = max([n] + [b // 2 for b in sweep_sizes])
+    # MoE routing (configs[3]); all ranks know every rank's routing
+    routing = moe_routing(world, args.moe_tokens)
+    comm = fcd.QComm(dist.group.WORLD, max_elems=max_elems, config=cfg, timeout_s=120.0,
+                     a2a_bytes=fcd.moe_region_bytes(cfg, world, args.moe_tokens, MOE["hidden"], routing),
+                     oneshot_max_elems=1 << 18)
     y = torch.empty_like(x)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    tdev = dev if backend == "nccl" else torch.device("cpu")
 
-    def timed(fn, steps, warmup):
+    def timed(fn, steps, warmup, do_flush=True):
+        """Per-step device time (CUDA events around fn on the current stream),
+        max over ranks per step."""
         for _ in range(warmup):
-            flush_l2(flush)
+            if do_flush:
+                flush_l2(flush)
             fn()
         torch.cuda.synchronize()
-        tot = 0.0
+        ts = []
         for _ in range(steps):
-            flush_l2(flush)
-            dist.barrier()
+            if do_flush:
+                flush_l2(flush)
             torch.cuda.synchronize()
+            dist.barrier()
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record()
             fn()
             e.record()
             torch.cuda.synchronize()
-            tot += s.elapsed_time(e)
-        t = torch.tensor([tot / steps], device=dev if backend == "nccl" else "cpu")
+            ts.append(s.elapsed_time(e))
+        t = torch.tensor(ts, device=tdev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return t.tolist()
 
     lib = fc._lib.lib()
+    # ---- headline: configs[2] two-step AllReduce through the public API
     l0 = lib.fc2_launch_count()
-    with ClockSampler(local_rank) as clk:
-        ms = timed(lambda: comm.all_reduce(x, out=y), args.steps, args.warmup)
-    launches = lib.fc2_launch_count() - l0
-    xb = x.clone()
-    ms_nccl = timed(lambda: dist.all_reduce(xb), args.steps, args.warmup) if backend == "nccl" else None
-    # the same NCCL AllReduce with NVLS (NVSwitch in-switch reduction) forced off, on a
-    # second communicator created after the env change (hard part 6)
-    ms_nccl_nonvls = None
-    if backend == "nccl" and os.environ.get("NCCL_NVLS_ENABLE") != "0":
-        prev = os.environ.get("NCCL_NVLS_ENABLE")
-        os.environ["NCCL_NVLS_ENABLE"] = "0"
-        try:
-            g2 = dist.new_group(backend="nccl")
-            ms_nccl_nonvls = timed(lambda: dist.all_reduce(xb, group=g2), args.steps, args.warmup)
-        except Exception:
-            ms_nccl_nonvls = None
-        finally:
-            if prev is None:
-                os.environ.pop("NCCL_NVLS_ENABLE", None)
-            else:
-                os.environ["NCCL_NVLS_ENABLE"] = prev
-    # e2e: pinned host in -> allreduce -> host out
+    with ClockSampler(dev.index) as clk:
+        ts_main = timed(lambda: comm.all_reduce(x, out=y), args.steps, args.warmup)
+    launches = (lib.fc2_launch_count() - l0) // max(1, args.steps + args.warmup)
+    ms = statistics.mean(ts_main)
+    comm.check()
+    # same size at 3 bits (configs[2] names 4-bit and 3-bit)
+    cfg3 = fc.QuantConfig(3, group_size=args.group, chunk_size=args.group, scheme=scheme)
+    ts_b3 = timed(lambda: comm.all_reduce(x, out=y, config=cfg3), args.steps, args.warmup)
+    comm.all_reduce(x, out=y)  # leave the 4-bit result in y for the parity check
+    # ---- bf16 NCCL AllReduce on the same box (NVLS default, then forced off)
+    ts_nccl = ts_nccl_nonvls = None
+    if backend == "nccl":
+        xb = x.clone()
+        ts_nccl = timed(lambda: dist.all_reduce(xb), args.steps, args.warmup)
+        if os.environ.get("NCCL_NVLS_ENABLE") != "0":
+            prev = os.environ.get("NCCL_NVLS_ENABLE")
+            os.environ["NCCL_NVLS_ENABLE"] = "0"
+            try:
+                g2 = dist.new_group(backend="nccl")
+                ts_nccl_nonvls = timed(lambda: dist.all_reduce(xb, group=g2), args.steps, args.warmup)
+            except Exception:
+                ts_nccl_nonvls = None
+            finally:
+                if prev is None:
+                    os.environ.pop("NCCL_NVLS_ENABLE", None)
+                else:
+                    os.environ["NCCL_NVLS_ENABLE"] = prev
+        del xb
+    # ---- NVLink peak: every rank stores 256 MiB into its ring successor's
+    # symmetric buffer with the library's copy kernel (per-direction GB/s)
+    nvl = None
+    probe = min(256 << 20, comm.buffer_bytes // 2 // 16 * 16)
+    if probe >= (16 << 20):
+        src = torch.empty(probe, dtype=torch.uint8, device=dev)
+        peer = (rank + 1) % world
+        dst_ptr = comm.buffer_ptr(peer)
+        st = torch.cuda.current_stream().cuda_stream
+        ts_nvl = timed(lambda: fc._lib.check(lib.fc2_copy_bytes(dst_ptr, src.data_ptr(), probe, 0, st)),
+                       max(5, args.steps // 2), 2, do_flush=False)
+        nvl = probe / (statistics.median(ts_nvl) * 1e-3) / 1e9
+        del src
+        dist.barrier()
+    # ---- e2e: pinned host in -> H2D -> all_reduce -> D2H, every step
     xh = x.cpu().pin_memory()
     yh = torch.empty_like(xh).pin_memory()
     xd = torch.empty_like(x)
@@ -522,74 +702,103 @@ def run_allreduce(args, rank, world, local_rank):
         comm.all_reduce(xd, out=y)
         yh.copy_(y, non_blocking=True)
 
-    ms_e2e = timed(e2e, max(3, args.steps), 2)
-    # All2All dispatch and combine: quantized (ours) vs bf16 NCCL all_to_all
-    send = spiky_bf16(int(a2a_mat[rank].sum()), 7000 + rank, dev)
-    ms_disp = timed(lambda: comm.all2all(send, a2a_mat, out_dtype=torch.bfloat16), args.steps, args.warmup)
-    back = spiky_bf16(int(a2a_mat[:, rank].sum()), 8000 + rank, dev)
-    ms_comb = timed(lambda: comm.all2all(back, a2a_mat.T.copy(), out_dtype=torch.bfloat16), args.steps, args.warmup)
-    # small messages (BASELINE configs[4], latency end): two-step vs one-shot vs NCCL bf16
-    small = {}
-    for m in (1 << 15, 1 << 17, 1 << 19):
-        if m > n:
-            continue
-        xs, ys = x[:m], y[:m]
-        row = {"two_step_us": round(1e3 * timed(lambda: comm.all_reduce(xs, out=ys, algo="two_step"),
-                                                args.steps, args.warmup), 2),
-               "one_shot_us": round(1e3 * timed(lambda: comm.all_reduce(xs, out=ys, algo="one_shot"),
-                                                args.steps, args.warmup), 2)}
-        if backend == "nccl":
-            xbs = x[:m].clone()
-            row["nccl_bf16_us"] = round(1e3 * timed(lambda: dist.all_reduce(xbs), args.steps, args.warmup), 2)
-        small[f"{2 * m >> 10}KiB"] = row
-    ms_disp_nccl = None
-    if backend == "nccl":
-        recv = torch.empty(int(a2a_mat[:, rank].sum()), dtype=torch.bfloat16, device=dev)
-        ins = [int(v) for v in a2a_mat[rank]]
-        outs = [int(v) for v in a2a_mat[:, rank]]
-        ms_disp_nccl = timed(lambda: dist.all_to_all_single(recv, send, outs, ins), args.steps, args.warmup)
-    sent_bytes = 2 * int(a2a_mat[rank].sum() - a2a_mat[rank, rank])
+    ts_e2e = timed(e2e, max(3, args.steps), 2)
+    comm.all_reduce(x, out=y)
+    # ---- parity of the headline result (rank 0 regenerates every rank's input)
+    parity = None
     if rank == 0:
+        from oracle import fc2_oracle as O
+
+        xs = [spiky_bf16(n, 1000 + r, dev) for r in range(world)]
+        exact = torch.zeros(n, dtype=torch.float32, device=dev)
+        for t in xs:
+            exact += t.float()
+        d = y.float() - exact
+        m = min(n, world * args.group * 512)
+        want, _ = O.two_step([t[:m].float().cpu().numpy() for t in xs], args.bits, args.group, sr)
+        parity = {"oracle_slice_elements": m,
+                  "oracle_slice_bit_exact": bool(np.array_equal(y[:m].float().cpu().numpy(), want[0])),
+                  "max_abs_vs_exact_sum": float(d.abs().max()),
+                  "rel_l2_vs_exact_sum": float(d.norm() / exact.norm())}
+        del xs, exact, d
+    # ---- configs[4]: message-size sweep, 2/4-bit vs NCCL bf16
+    sweep = {}
+    for nb in sweep_sizes:
+        m = nb // 2
+        xm = x[:m] if m <= n else spiky_bf16(m, 3000 + rank, dev)
+        ym = torch.empty_like(xm)
+        k = min(args.steps, 10)
+        row = {}
+        for bits in (4, 2):
+            cb = fc.QuantConfig(bits, group_size=args.group, chunk_size=args.group, scheme=scheme)
+            t = statistics.mean(timed(lambda: comm.all_reduce(xm, out=ym, config=cb), k, 3))
+            row[f"b{bits}_us"] = round(t * 1e3, 2)
+            row[f"b{bits}_algbw_GBps"] = round(nb / (t * 1e-3) / 1e9, 2)
+        if backend == "nccl":
+            xc = xm.clone()
+            t = statistics.mean(timed(lambda: dist.all_reduce(xc), k, 3))
+            row["nccl_bf16_us"] = round(t * 1e3, 2)
+            row["nccl_bf16_algbw_GBps"] = round(nb / (t * 1e-3) / 1e9, 2)
+            row["speedup_b4"] = round(t * 1e3 / row["b4_us"], 3)
+            row["speedup_b2"] = round(t * 1e3 / row["b2_us"], 3)
+            del xc
+        sweep[f"{nb >> 10}KiB" if nb < (1 << 20) else f"{nb >> 20}MiB"] = row
+        del xm, ym
+    # ---- configs[3]: MoE token dispatch + combine (4096 tok x 7168, top-8 of 256, EP = world)
+    moe = fcd.bench_moe(comm, cfg, routing, args.moe_tokens, MOE["hidden"], timed,
+                        args.steps, args.warmup, backend == "nccl") if not args.no_moe else None
+    if rank == 0:
+        F = fc.footprint_bytes(cfg, comm.shard_len if n == comm.max_lay.n else
+                               fcd.TwoStepLayout.make(n, world, cfg).shard_len)
         algbw = 2 * n / (ms * 1e-3) / 1e9
-        F = fc.footprint_bytes(cfg, comm.shard_len)
+        wire = 2 * (world - 1) * F  # bytes each rank stores into peers (both stages)
+        nvl_peak = nvl if nvl else 770.0
         line = {
             "metric": METRIC,
-            "value": round(algbw * world, 2),
+            "value": round(algbw, 2),
             "unit": "GB/s",
+            "value_kind": "algbw = 2 n / latency (nccl-tests), n bf16 elements per rank",
+            "aggregate_GBps": round(algbw * world, 2),
+            "busbw_GBps": round(algbw * 2 * (world - 1) / world, 2),
             "n_gpus": world,
             "steps": args.steps,
             "warmup": args.warmup,
             "ms_per_step": round(ms, 5),
             "latency_us": round(ms * 1e3, 2),
-            "per_rank_algbw_GBps": round(algbw, 2),
+            **pct(ts_main),
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": None,
             "dtype": "bf16 in/out, fp32 reduce, packed u8 planes",
-            "data": "synthetic spiky bf16 per rank",
-            "config": {"workload": "two-step quantized AllReduce, 8192x4096 bf16 per rank (BASELINE configs[2])",
-                       "n": n, "bits": args.bits, "group": args.group, "scheme": args.scheme,
-                       "l2": "flushed before every step (256 MiB write, then read back)", "parallelism": f"tp{world}"},
-            "nccl_bf16": None if ms_nccl is None else {
-                "ms": round(ms_nccl, 5), "algbw_GBps": round(2 * n / (ms_nccl * 1e-3) / 1e9, 2),
-                "speedup": round(ms_nccl / ms, 3), "nvls_env": os.environ.get("NCCL_NVLS_ENABLE", "default"),
-                "nvls_off_ms": None if ms_nccl_nonvls is None else round(ms_nccl_nonvls, 5),
-                "speedup_vs_nvls_off": None if ms_nccl_nonvls is None else round(ms_nccl_nonvls / ms, 3)},
+            "data": "synthetic spiky bf16 per rank (N(0,1), 1/64 at +-50)",
+            "config": config_for(args, world),
+            "b3": {"ms": round(statistics.mean(ts_b3), 5),
+                   "algbw_GBps": round(2 * n / (statistics.mean(ts_b3) * 1e-3) / 1e9, 2), **pct(ts_b3)},
+            "nccl_bf16": None if ts_nccl is None else {
+                "ms": round(statistics.mean(ts_nccl), 5), **pct(ts_nccl),
+                "algbw_GBps": round(2 * n / (statistics.mean(ts_nccl) * 1e-3) / 1e9, 2),
+                "speedup": round(statistics.mean(ts_nccl) / ms, 3),
+                "nvls_env": os.environ.get("NCCL_NVLS_ENABLE", "default"),
+                "nvls_off_ms": None if ts_nccl_nonvls is None else round(statistics.mean(ts_nccl_nonvls), 5),
+                "speedup_vs_nvls_off": None if ts_nccl_nonvls is None else round(
+                    statistics.mean(ts_nccl_nonvls) / ms, 3)},
             "backend": backend,
-            "roofline": {"bound": "nvlink", "unit": "GB/s",
-                         "achieved": round(2 * (world - 1) / world * F * world / (ms * 1e-3) / 1e9 / world, 2),
-                         "peak": 770.0, "peak_kind": "measured peer copy per direction (B200_PROFILING.md)",
-                         "frac": round(2 * (world - 1) / world * F * world / (ms * 1e-3) / 1e9 / world / 770.0, 4),
-                         "traffic": None},
-            "all2all_moe": {
-                "shape": f"{tokens} tok x {hidden}, top-{topk} of {experts}, EP={world}",
-                "dispatch_ms": round(ms_disp, 4), "combine_ms": round(ms_comb, 4),
-                "dispatch_algbw_GBps": round(sent_bytes / (ms_disp * 1e-3) / 1e9, 2),
-                "nccl_bf16_dispatch_ms": None if ms_disp_nccl is None else round(ms_disp_nccl, 4),
-                "speedup_vs_nccl": None if ms_disp_nccl is None else round(ms_disp_nccl / ms_disp, 3)},
-            "e2e": {"value": round(2 * n * world / (ms_e2e * 1e-3) / 1e9, 2), "unit": "GB/s",
-                    "ms_per_step": round(ms_e2e, 4), "h2d_bytes_per_step": 2 * n, "d2h_bytes_per_step": 2 * n},
-            "small_message_allreduce": small,
+            "roofline": {"bound": "nvlink", "unit": "GB/s", "kernel": "two-step (encode+peer store, reduce+peer "
+                                                                      "store, gather decode)",
+                         "achieved": round(wire / (ms * 1e-3) / 1e9, 2),
+                         "peak": round(nvl_peak, 1),
+                         "peak_kind": ("measured in this run: fc2_copy_bytes ring put of 256 MiB into the "
+                                       "successor's IPC buffer" if nvl else "fallback (B200_PROFILING.md)"),
+                         "frac": round(wire / (ms * 1e-3) / 1e9 / nvl_peak, 4),
+                         "traffic": None,
+                         "algorithmic_bytes_per_step": wire},
+            "parity": parity,
+            "e2e": {"value": round(2 * n / (statistics.mean(ts_e2e) * 1e-3) / 1e9, 2), "unit": "GB/s",
+                    "ms_per_step": round(statistics.mean(ts_e2e), 4), "h2d_bytes_per_step": 2 * n,
+                    "d2h_bytes_per_step": 2 * n,
+                    "path": "pinned host x -> H2D -> QComm.all_reduce -> D2H y, every step"},
+            "message_size_sweep": sweep,
+            "all2all_moe": moe,
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
@@ -604,99 +813,75 @@ def run_allreduce(args, rank, world, local_rank):
 # ---------------------------------------------------------------------------
 
 
-_REF_X = None  # the reference arm's input, shared with forked pool workers
-
-
-def _ref_slice(bounds):
-    """One pool worker's share of the reference round trip: encode + decode
-    of a group-aligned slice (groups are independent, codec.py:485)."""
-    from oracle import fc2_oracle as O
-
-    a, b, bits, g, sr = bounds
-    planes, meta = O.encode(_REF_X[a:b], bits, g, sr)
-    O.decode(planes, meta, b - a, bits, g, sr)
-    return b - a
-
-
-_REF_RANKS = None  # padded float32 payloads of the simulated ranks (forked workers)
-
-
-def _ref_shard(job):
-    """One shard of the reference two-step (collectives.py:278-311) in a pool
-    worker: every source's QDQ of the shard summed in fp32 in rank order from
-    +0, then the owner's QDQ of the sum -- the same arithmetic as
-    oracle.two_step, one shard per process."""
-    import numpy as np
-
-    from oracle import fc2_oracle as O
-
-    shard, S, bits, g, sr = job
-    acc = np.zeros(S, dtype=np.float32)
-    for src in range(len(_REF_RANKS)):
-        acc += O.qdq_f32(_REF_RANKS[src][shard * S:(shard + 1) * S], bits, g, sr)[0]
-    return O.qdq_f32(acc, bits, g, sr)[0]
-
-
 def run_reference(args, rank, world):
+    """The reference's own CPU implementation of the path on this host: rank
+    0 only, all host cores (a process pool over independent slices; numpy
+    elementwise work is single-threaded, SPEC.md:312 allows the pool)."""
     if rank != 0:
         return
-    sr = args.scheme == "sr"
-    n_sample = args.ref_sample
-    times = []
-    from oracle import fc2_oracle as O
+    import multiprocessing as mproc
+
     import numpy as np
 
-    cores = 1
-    if world > 1:
-        # two-step AllReduce of the oracle on a bounded per-rank sample, one
-        # shard per pool process (shards are independent, collectives.py:276)
-        import multiprocessing as mproc
+    q = load_reference()
+    kind = "reference" if q is not None else "port"
+    sr = args.scheme == "sr"
+    cores = max(1, min(os.cpu_count() or 1, 64))
+    n = args.n
+    if world == 1:
+        if q is not None:
+            x = q.bf16_round(q.gen_synthetic(q.default_spiky_spec(n, 0))).astype(np.float32)
+        else:
+            from oracle import fc2_oracle as O
 
-        global _REF_RANKS
-        payloads = [O.bf16_snap(O.spiky(n_sample, s)).astype(np.float32) for s in O.child_seeds(0, world)]
-        mult = world * args.group
-        padded = -(-n_sample // mult) * mult
-        _REF_RANKS = [np.pad(p, (0, padded - n_sample)) for p in payloads]
-        S = padded // world
-        cores = max(1, min(os.cpu_count() or 1, world))
-        with mproc.get_context("fork").Pool(cores) as pool:
-            for i in range(args.warmup + args.steps):
-                t0 = time.perf_counter()
-                shards = pool.map(_ref_shard, [(j, S, args.bits, args.group, sr) for j in range(world)])
-                out = O.bf16_snap(np.concatenate(shards)[:n_sample])
-                if i >= args.warmup:
-                    times.append(time.perf_counter() - t0)
-        want, _ = O.two_step(payloads, args.bits, args.group, sr)
-        assert np.array_equal(out, want[0]), "pooled reference differs from oracle.two_step"
+            x = O.bf16_snap(O.spiky(n, 0)).astype(np.float32)
+        time_reference_codec(x, args.bits, args.group, sr, args.warmup, cores)
+        times, cores = time_reference_codec(x, args.bits, args.group, sr, args.steps, cores)
         dt = statistics.mean(times)
-        value = 2 * n_sample * world / dt / 1e9
-        what = (f"oracle two-step over {world} simulated ranks x {n_sample} elements, one shard per "
-                f"process ({cores} processes)")
+        value = 2 * n / dt / 1e9
+        what = (f"encode_chunk + decode_chunk of the whole {n}-element bf16 tensor in group-aligned slices "
+                f"over a pool of {cores} processes")
     else:
-        # the full 64 MiB workload, split into group-aligned slices over a pool
-        # of forked processes (all host cores; the reference is single-threaded
-        # numpy per process, SPEC.md:312 allows a process pool)
-        import multiprocessing as mproc
+        global _REF_RANKS
+        if q is not None:
+            seeds = q.rank_seeds(0, world)
+            _REF_RANKS = [q.bf16_round(q.gen_synthetic(q.default_spiky_spec(n, s))).astype(np.float32)
+                          for s in seeds]
+        else:
+            from oracle import fc2_oracle as O
 
-        global _REF_X
-        n_sample = args.n
-        cores = max(1, min(os.cpu_count() or 1, 64))
-        _REF_X = O.bf16_snap(O.spiky(n_sample, 0)).astype(np.float32)
-        step = -(-n_sample // (cores * 4) // args.group) * args.group
-        parts = [(a, min(a + step, n_sample), args.bits, args.group, sr) for a in range(0, n_sample, step)]
+            _REF_RANKS = [O.bf16_snap(O.spiky(n, s)).astype(np.float32) for s in O.child_seeds(0, world)]
+        mult = world * args.group
+        if n % mult:
+            raise SystemExit("reference arm: n must be a multiple of world * group")
+        step = -(-n // (cores * 2) // mult) * mult
+        jobs = [(a, min(a + step, n), args.bits, args.group, sr, world) for a in range(0, n, step)]
+        times = []
         with mproc.get_context("fork").Pool(cores) as pool:
             for i in range(args.warmup + args.steps):
                 t0 = time.perf_counter()
-                done = sum(pool.map(_ref_slice, parts))
+                pool.map(_ref_two_step_slice, jobs)
                 if i >= args.warmup:
                     times.append(time.perf_counter() - t0)
-        assert done == n_sample
+        # the sliced form is the full-size algorithm: check one slice against
+        # the oracle's two-step of the same slice
+        from oracle import fc2_oracle as O
+
+        a, b = jobs[0][0], jobs[0][1]
+        b = min(b, a + mult * 64)
+        if q is not None:
+            cfgq = q.QuantConfig(args.bits, group_size=args.group,
+                                 scheme=q.Scheme.SPIKE_RESERVING if sr else q.Scheme.RTN)
+            got = q.two_step_allreduce_q([r[a:b] for r in _REF_RANKS], ref_topology(q, world), cfgq).outputs[0]
+            want = O.two_step([r[a:b] for r in _REF_RANKS], args.bits, args.group, sr)[0][0]
+            assert np.array_equal(got, want), "reference and oracle two-step differ"
         dt = statistics.mean(times)
-        value = 2 * n_sample / dt / 1e9
-        what = (f"oracle encode+decode of the full {n_sample}-element bf16 workload in {len(parts)} "
-                f"group-aligned slices over a pool of {cores} processes")
-    cb = {"value": round(value, 5), "unit": "GB/s", "cores": cores, "kind": "port",
-          "sample": what + " (numpy restatement of the pure-Python reference; numpy elementwise is single-threaded)"}
+        value = 2 * n / dt / 1e9
+        what = (f"two_step_allreduce_q over {world} simulated ranks x {n} elements (the full configs[2] "
+                f"workload) in {len(jobs)} slices of world*g multiples over a pool of {cores} processes")
+    cb = {"value": round(value, 5), "unit": "GB/s", "cores": cores, "kind": kind,
+          "sample": what + (" -- qcomm from baseline/_ref" if q is not None else
+                            " -- oracle port (baseline/_ref missing)")}
     line = {
         "impl": "reference",
         "metric": METRIC,
@@ -706,17 +891,40 @@ def run_reference(args, rank, world):
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": round(dt * 1e3, 3),
+        **pct([t * 1e3 for t in times]),
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f64 codec math (numpy), fp32 reduce",
-        "data": "synthetic spiky bf16",
-        "config": {"workload": ("two-step quantized AllReduce" if world > 1 else "codec round trip"),
-                   "n": n_sample, "bits": args.bits, "group": args.group, "scheme": args.scheme},
+        "data": "synthetic spiky bf16 (reference default_spiky_spec)",
+        "config": config_for(args, world),
         "cpu_baseline": cb,
         "e2e": {"value": cb["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def self_launch(args):
+    """`bench.py --gpus N` outside torchrun: one rank per GPU under
+    torch.distributed.run (127.0.0.1 rendezvous), same arguments."""
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus and args.backend == "nccl":
+        print(json.dumps({"metric": METRIC, "n_gpus": args.gpus, "error":
+                          f"--gpus {args.gpus} needs {args.gpus} GPUs; {have} visible"}), flush=True)
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -730,24 +938,29 @@ def main():
     ap.add_argument("--scheme", choices=["sr", "rtn"], default="sr")
     ap.add_argument("--elems", dest="n", type=int, default=N_ELEMS)
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-moe", action="store_true")
+    ap.add_argument("--sweep-max", type=int, default=1 << 30, help="largest sweep message (bytes per rank)")
     ap.add_argument("--cpu-reps", type=int, default=2)
-    ap.add_argument("--ref-sample", type=int, default=1 << 22)
-    ap.add_argument("--moe-tokens", type=int, default=4096)
+    ap.add_argument("--moe-tokens", type=int, default=MOE["tokens"])
     ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
                     help="process-group backend for N>1 (gloo: several ranks may share one GPU)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    launched = "WORLD_SIZE" in os.environ
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)
-        return
+        return 0
+    if world > 1 and not launched:
+        return self_launch(args)
     if world > 1:
-        run_allreduce(args, rank, world, local_rank)
+        run_multi(args, rank, world, local_rank)
     else:
         run_codec(args)
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

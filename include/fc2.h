@@ -224,6 +224,11 @@ int fc2_a2a_q(fc2_comm* c, const fc2_config* cfg, const void* x, int32_t x_dtype
               void* y, int32_t y_dtype, int64_t region_off, int64_t region_bytes, int32_t* dev_err,
               double timeout_s, void* stream);
 
+/* Device copy of nbytes (16-byte aligned buffers) with at most `ctas` CTAs
+ * (<= 0: 4 per SM); dst may be a peer's symmetric buffer (fc2_comm_buffer), so
+ * this is also the NVLink store-bandwidth probe. */
+int fc2_copy_bytes(void* dst, const void* src, int64_t nbytes, int32_t ctas, void* stream);
+
 /* Diagnostics. */
 const char* fc2_last_error(void);
 int64_t fc2_launch_count(void);   /* kernels launched by this library so far */

@@ -86,6 +86,7 @@ SIGNATURES = {
     "fc2_allreduce_2step": (_I32, [_P, _PCFG, _P, _I32, _P, _I32, _I64, _I64, _P, ctypes.c_double, _P]),
     "fc2_a2a_q": (_I32, [_P, _PCFG, _P, _I32, _PI64, _P, _I32, _I64, _I64, _P, ctypes.c_double, _P]),
     "fc2_copy_check": (_I32, [_P, _I32, _P, _I32, _I64, _P, _P]),
+    "fc2_copy_bytes": (_I32, [_P, _P, _I64, _I32, _P]),
     "fc2_last_error": (ctypes.c_char_p, []),
     "fc2_launch_count": (_I64, []),
     "fc2_version": (_I32, []),

@@ -87,9 +87,34 @@ __global__ void k_barrier(const __grid_constant__ BarrierArgs a) {
   __threadfence_system();
 }
 
+// Plain device copy, 16 bytes per thread-iteration; dst may be a peer
+// buffer mapped through CUDA IPC (NVLink stores): the packed-bytes move of
+// the collectives and the NVLink peak probe of bench.py.
+__global__ void __launch_bounds__(512) k_copy_bytes(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src,
+                                                    int64_t nbytes) {
+  const int64_t n16 = nbytes >> 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride)
+    reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+  const int64_t tail = nbytes & 15;
+  if (blockIdx.x == 0 && (int64_t)threadIdx.x < tail) dst[(n16 << 4) + threadIdx.x] = src[(n16 << 4) + threadIdx.x];
+}
+
 }  // namespace
 
 extern "C" {
+
+int fc2_copy_bytes(void* dst, const void* src, int64_t nbytes, int32_t ctas, void* stream) {
+  if (nbytes <= 0) return FC2_OK;
+  if ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15u)
+    return set_err(FC2_ECONFIG, "fc2_copy_bytes needs 16-byte aligned buffers");
+  int64_t blocks = ((nbytes >> 4) + 511) / 512;
+  const int64_t cap = ctas > 0 ? ctas : 148 * 4;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  k_copy_bytes<<<(unsigned)blocks, 512, 0, (cudaStream_t)stream>>>((uint8_t*)dst, (const uint8_t*)src, nbytes);
+  return cuda_check("k_copy_bytes");
+}
 
 int fc2_comm_create(int32_t rank, int32_t world, int64_t bytes, fc2_comm** out, void* handle_out) {
   if (world < 1 || world > FC2_COMM_MAX || rank < 0 || rank >= world)

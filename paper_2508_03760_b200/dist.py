@@ -66,6 +66,17 @@ class TwoStepLayout:
     def padded(self) -> int:
         return _round_up(self.n, self.world * self.group_size)
 
+    def buffer_ptr(self, peer: int) -> int:
+        """Device address of ``peer``'s symmetric buffer as mapped in this
+        process (own rank: local memory; others: NVLink via CUDA IPC)."""
+        if self._c is None:
+            raise ConfigError("buffer_ptr needs the ipc transport")
+        return int(_lib.lib().fc2_comm_buffer(self._c, int(peer)) or 0)
+
+    @property
+    def buffer_bytes(self) -> int:
+        return self._nbytes
+
     @property
     def shard_len(self) -> int:
         return self.padded // self.world
@@ -178,6 +189,7 @@ class QComm:
         self.codec = CudaCodec(self.cfg, self.device)
         self.err = self.codec.err
         self._c = None
+        self._nbytes = 0
         if transport not in ("ipc", "nccl"):
             raise ConfigError(f"unknown transport {transport!r}")
         if transport == "ipc":
@@ -186,6 +198,7 @@ class QComm:
             handle = (ctypes.c_uint8 * hb)()
             ptr = ctypes.c_void_p()
             nbytes = self.os_off + (2 * self.world * self.world + self.world) * self.os_lay.slot_bytes
+            self._nbytes = nbytes
             _lib.check(lib.fc2_comm_create(self.rank, self.world, nbytes, ctypes.byref(ptr),
                                            ctypes.cast(handle, ctypes.c_void_p)))
             self._c = ptr
@@ -200,14 +213,19 @@ class QComm:
         return self.max_lay.shard_len
 
     def all_reduce(self, x: torch.Tensor, out: torch.Tensor | None = None, check: bool = False,
-                   algo: str = "auto") -> torch.Tensor:
+                   algo: str = "auto", config: QuantConfig | None = None) -> torch.Tensor:
         """Two-step quantized AllReduce of a 1-D bf16/f32 CUDA tensor; every
         rank gets the identical bf16-grid result (collectives.py:313-314).
 
         ``algo``: ``"two_step"`` (two packed exchanges), ``"one_shot"`` (one
         all-gather of packed shards, every rank reduces every shard: fewer
         barriers for latency-bound sizes, same bits), or ``"auto"`` (one-shot
-        up to ``oneshot_max_elems`` on the ipc transport)."""
+        up to ``oneshot_max_elems`` on the ipc transport).  ``config``
+        overrides the communicator's codec for this call when its packed
+        shards fit the communicator's slots (e.g. fewer bits)."""
+        cfg = self.cfg if config is None else config
+        if cfg.int_log:
+            _device.ensure_intlog(cfg.theta, self.device)
         x = x.reshape(-1)
         if not x.is_contiguous():
             x = x.contiguous()
@@ -215,26 +233,27 @@ class QComm:
         if n > self.max_lay.n:
             raise DataError(f"payload of {n} elements exceeds the communicator's {self.max_lay.n}")
         y = out if out is not None else torch.empty(n, dtype=x.dtype, device=x.device)
-        lay = TwoStepLayout.make(n, self.world, self.cfg)
+        lay = TwoStepLayout.make(n, self.world, cfg)
         if algo not in ("auto", "two_step", "one_shot"):
             raise ConfigError(f"unknown allreduce algorithm {algo!r}")
         one = self.transport == "ipc" and n <= self.os_lay.n and algo != "two_step"
         if algo == "one_shot" and not one:
             raise ConfigError("one_shot needs the ipc transport and n <= oneshot_max_elems")
         if one:
-            c = self.cfg.c_struct()
+            c = cfg.c_struct()
             _lib.check(_lib.lib().fc2_allreduce_oneshot(
                 self._c, ctypes.byref(c), x.data_ptr(), _device.dtype_code(x), y.data_ptr(),
                 _device.dtype_code(y), n, self.os_lay.slot_bytes, self.os_off, self.err.data_ptr(),
                 self.timeout_s, _device.stream_handle()))
         elif self.transport == "ipc":
-            c = self.cfg.c_struct()
+            c = cfg.c_struct()
             _lib.check(_lib.lib().fc2_allreduce_2step(
                 self._c, ctypes.byref(c), x.data_ptr(), _device.dtype_code(x), y.data_ptr(),
                 _device.dtype_code(y), n, self.max_lay.slot_bytes, self.err.data_ptr(), self.timeout_s,
                 _device.stream_handle()))
         else:
-            two_step_via_collectives(x, self.codec, lay, self.group, y)
+            codec = self.codec if cfg == self.cfg else CudaCodec(cfg, self.device)
+            two_step_via_collectives(x, codec, lay, self.group, y)
         if check:
             self.check()
         return y
@@ -289,3 +308,66 @@ class QComm:
             self.close()
         except Exception:
             pass
+
+
+# ---------------------------------------------------------------------------
+# MoE All2All helpers (BASELINE configs[3]) used by bench.py
+# ---------------------------------------------------------------------------
+
+
+def moe_token_matrix(routing, world: int, experts: int) -> np.ndarray:
+    """tokens[src][dst]: how many of rank src's tokens route to at least one
+    expert on rank dst (one copy per distinct destination rank, SURVEY 8 d).
+    routing: int64 [world, tokens, topk] expert ids, experts contiguous per rank."""
+    per = experts // world
+    mat = np.zeros((world, world), dtype=np.int64)
+    r = np.asarray(routing)
+    for s in range(world):
+        hit = np.zeros((r.shape[1], world), dtype=bool)
+        np.put_along_axis(hit, r[s] // per, True, axis=1)
+        mat[s] = hit.sum(0)
+    return mat
+
+
+def moe_region_bytes(config: QuantConfig, world: int, tokens: int, hidden: int, routing,
+                     experts: int = 256) -> int:
+    """All2All receive-region bytes for the MoE dispatch/combine of ``routing``."""
+    mat = moe_token_matrix(routing, world, experts) * hidden
+    need = 0
+    for d in range(world):
+        tot = sum(_round_up(footprint_bytes(config, _round_up(int(mat[s, d]), config.group_size)), _SLOT_ALIGN)
+                  for s in range(world) if s != d and mat[s, d])
+        tot_c = sum(_round_up(footprint_bytes(config, _round_up(int(mat[d, s]), config.group_size)), _SLOT_ALIGN)
+                    for s in range(world) if s != d and mat[d, s])
+        need = max(need, tot, tot_c)
+    return need + 4096
+
+
+def bench_moe(comm: "QComm", config: QuantConfig, routing, tokens: int, hidden: int, timed, steps: int,
+              warmup: int, with_nccl: bool, experts: int = 256) -> dict:
+    """Dispatch + combine of the routed token blocks (block-matrix form), vs
+    the bf16 NCCL all_to_all of the same blocks."""
+    import statistics
+
+    world, rank = comm.world, comm.rank
+    mat = moe_token_matrix(routing, world, experts) * hidden
+    g = torch.Generator(device=comm.device).manual_seed(7000 + rank)
+    send = torch.randn(int(mat[rank].sum()), device=comm.device, generator=g).to(torch.bfloat16)
+    back = torch.randn(int(mat[:, rank].sum()), device=comm.device, generator=g).to(torch.bfloat16)
+    t_d = statistics.mean(timed(lambda: comm.all2all(send, mat, out_dtype=torch.bfloat16), steps, warmup))
+    t_c = statistics.mean(timed(lambda: comm.all2all(back, mat.T.copy(), out_dtype=torch.bfloat16), steps, warmup))
+    out = {"shape": f"{tokens} tok x {hidden}, top-8 of {experts}, EP={world}",
+           "form": "block matrix (rows grouped by destination)",
+           "dispatch_ms": round(t_d, 4), "combine_ms": round(t_c, 4),
+           "dispatch_algbw_GBps": round(2 * int(mat[rank].sum() - mat[rank, rank]) / (t_d * 1e-3) / 1e9, 2)}
+    if with_nccl:
+        import torch.distributed as dist
+
+        recv = torch.empty(int(mat[:, rank].sum()), dtype=torch.bfloat16, device=comm.device)
+        ins = [int(v) for v in mat[rank]]
+        outs = [int(v) for v in mat[:, rank]]
+        t_n = statistics.mean(timed(lambda: dist.all_to_all_single(recv, send, outs, ins, group=comm.group),
+                                    steps, warmup))
+        out["nccl_bf16_dispatch_ms"] = round(t_n, 4)
+        out["speedup_vs_nccl"] = round(t_n / t_d, 3)
+    return out

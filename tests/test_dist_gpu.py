@@ -50,6 +50,32 @@ def _worker(rank, world, port, case, q):
                     y = comm.all_reduce(x.to(dt), check=True, algo=algo)
                     outs.append(y.float().cpu().numpy().tobytes())
             q.put((rank, outs))
+        elif kind == "a2a_errors":
+            # (1) blocks that do not fit the All2All region -> ConfigError (the
+            # one-shot region behind it must never be overwritten); (2) NaN in
+            # the diagonal block -> DataError; (3) the error word is cleared, so
+            # the next clean call passes
+            m = np.full((world, world), 256)
+            comm = QComm(max_elems=g * world, config=cfg, a2a_bytes=64, timeout_s=120.0)
+            x = torch.ones(int(m[rank].sum()), device="cuda")
+            try:
+                comm.all2all(x, m, check=True)
+                raised = None
+            except fc.ConfigError:
+                raised = "config"
+            comm.close()
+            cap = world * 4096
+            comm = QComm(max_elems=g * world, config=cfg, a2a_bytes=cap, timeout_s=120.0)
+            bad = x.clone()
+            bad[rank * 256 + 3] = float("nan")  # my own (diagonal) block
+            try:
+                comm.all2all(bad, m, check=True)
+                raised2 = None
+            except fc.DataError:
+                raised2 = "data"
+            y = comm.all2all(x, m, check=True)
+            ok = bool(torch.all(y == 1.0))
+            q.put((rank, [raised, raised2, ok]))
         else:
             rng = np.random.default_rng(seed)
             m = rng.integers(0, 3, (world, world)) * 512 + rng.integers(0, 200, (world, world))
@@ -79,7 +105,8 @@ def _run(world, case):
 
 
 @pytest.mark.parametrize("world,n,bits,g,sr", [(2, 100003, 4, 128, True), (4, 1 << 16, 3, 128, True),
-                                               (2, 8192, 2, 32, False)])
+                                               (2, 8192, 2, 32, False), (8, 1 << 18, 4, 128, True),
+                                               (8, 100003, 3, 32, True)])
 def test_ipc_two_step_matches_reference_algorithm(world, n, bits, g, sr):
     got = _run(world, ("allreduce", n, bits, g, sr, 5))
     payloads = [O.bf16_snap(O.spiky(n, s)).astype(np.float32) for s in O.child_seeds(5, world)]
@@ -89,7 +116,7 @@ def test_ipc_two_step_matches_reference_algorithm(world, n, bits, g, sr):
             assert np.array_equal(np.frombuffer(blob, dtype=np.float32), want[0])
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 8])
 def test_ipc_all2all_matches_reference_algorithm(world):
     got = _run(world, ("a2a", 0, 4, 128, True, 9))
     m = np.frombuffer(got[0][1], dtype=np.int64).reshape(world, world)
@@ -100,3 +127,9 @@ def test_ipc_all2all_matches_reference_algorithm(world):
     for d in range(world):
         y = np.frombuffer(got[d][0], dtype=np.float32)
         assert np.array_equal(y, np.concatenate([want[d][s] for s in range(world)]))
+
+
+def test_ipc_all2all_region_bounds_and_error_reset():
+    got = _run(2, ("a2a_errors", 0, 4, 128, True, 0))
+    for r in range(2):
+        assert got[r] == ["config", "data", True]
