@@ -66,17 +66,6 @@ class TwoStepLayout:
     def padded(self) -> int:
         return _round_up(self.n, self.world * self.group_size)
 
-    def buffer_ptr(self, peer: int) -> int:
-        """Device address of ``peer``'s symmetric buffer as mapped in this
-        process (own rank: local memory; others: NVLink via CUDA IPC)."""
-        if self._c is None:
-            raise ConfigError("buffer_ptr needs the ipc transport")
-        return int(_lib.lib().fc2_comm_buffer(self._c, int(peer)) or 0)
-
-    @property
-    def buffer_bytes(self) -> int:
-        return self._nbytes
-
     @property
     def shard_len(self) -> int:
         return self.padded // self.world
@@ -207,6 +196,17 @@ class QComm:
             allh = (ctypes.c_uint8 * (hb * self.world)).from_buffer_copy(b"".join(handles))
             _lib.check(lib.fc2_comm_open_peers(self._c, ctypes.cast(allh, ctypes.c_void_p)))
             dist.barrier(group=group)
+
+    def buffer_ptr(self, peer: int) -> int:
+        """Device address of ``peer``'s symmetric buffer as mapped in this
+        process (own rank: local memory; others: NVLink via CUDA IPC)."""
+        if self._c is None:
+            raise ConfigError("buffer_ptr needs the ipc transport")
+        return int(_lib.lib().fc2_comm_buffer(self._c, int(peer)) or 0)
+
+    @property
+    def buffer_bytes(self) -> int:
+        return self._nbytes
 
     @property
     def shard_len(self) -> int:
