@@ -2,6 +2,7 @@
 // fc2_inst_b<B>.cu so the 8 bitwidths compile in parallel).
 #pragma once
 #include <atomic>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <utility>
@@ -833,6 +834,10 @@ __global__ void __launch_bounds__(kRedWarps * 32) k_reduce_fast(const __grid_con
   }
 }
 
+}  // namespace fc2
+#include "fc2_reduce_run.cuh"
+namespace fc2 {
+
 // ---------------------------------------------------------------------------
 // template dispatch
 // ---------------------------------------------------------------------------
@@ -1245,6 +1250,20 @@ struct Launchers {
         if (rc) return rc;
       }
       return FC2_OK;
+    }
+    // default: bulk-copy staged tiles, sums in registers (k_reduce_run);
+    // FC2_REDUCE=cta selects the round-1 CTA kernel (A/B measurements)
+    static const bool use_cta = [] {
+      const char* e = getenv("FC2_REDUCE");
+      return e && e[0] == 'c';
+    }();
+    if (!use_cta) {
+      switch (G) {
+        case 32: if (RedRun<B, SR, 32>::ok(a)) return RedRun<B, SR, 32>::go(a, st); break;
+        case 64: if (RedRun<B, SR, 64>::ok(a)) return RedRun<B, SR, 64>::go(a, st); break;
+        case 128: if (RedRun<B, SR, 128>::ok(a)) return RedRun<B, SR, 128>::go(a, st); break;
+        case 256: if (RedRun<B, SR, 256>::ok(a)) return RedRun<B, SR, 256>::go(a, st); break;
+      }
     }
     if (grp) {
       switch (G) {
