@@ -7,7 +7,7 @@ SRC := $(PKG)/csrc
 OBJ := $(PKG)/_build
 
 LIB := $(PKG)/libfc2.so
-OBJS := $(OBJ)/fc2_codec.o $(OBJ)/fc2_comm.o $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(wildcard $(SRC)/fc2_inst_b*.cu))
+OBJS := $(OBJ)/fc2_codec.o $(OBJ)/fc2_comm.o $(OBJ)/fc2_moe.o $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(wildcard $(SRC)/fc2_inst_b*.cu))
 
 all: $(LIB)
 

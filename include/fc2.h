@@ -36,6 +36,7 @@ extern "C" {
 #define FC2_ERR_TIMEOUT     8  /* cross-rank flag wait timed out */
 #define FC2_ERR_CODE_RANGE 16  /* pack: code outside [0, 2^bits) -> CodeRangeError (codec.py:216-217) */
 #define FC2_ERR_NEGATIVE   32  /* scale_to_int: negative scale -> DataError (codec.py:373-374) */
+#define FC2_ERR_EXPERT_RANGE 64 /* MoE routing: expert id outside [0, n_experts) -> ConfigError */
 
 /* ---- element types ----------------------------------------------------- */
 #define FC2_BF16 0
@@ -83,6 +84,16 @@ int fc2_encode(const fc2_config* cfg, const void* x, int32_t x_dtype, int64_t n_
 int fc2_encode_batch(const fc2_config* cfg, int32_t x_dtype, int32_t njobs,
                      const void* const* xs, const int64_t* n_valid, const int64_t* n,
                      void* const* payloads, int32_t* dev_err, void* stream);
+
+/* Batched encode with the token-row gather fused in (MoE dispatch): chunk i
+ * is the rows rows[i][0..n_valid[i] / row_len) of x (row_len elements each,
+ * row_len % 8 == 0), i.e. element e is x[rows[i][e / row_len] * row_len +
+ * e % row_len]; the encoders read the rows directly, nothing is gathered
+ * into HBM first.  Same payload bytes as fc2_encode_batch on the gathered
+ * block (collectives.py:462-480 on the block of routed tokens). */
+int fc2_encode_batch_rows(const fc2_config* cfg, int32_t x_dtype, int32_t njobs, const void* x,
+                          const int32_t* const* rows, int64_t row_len, const int64_t* n_valid, const int64_t* n,
+                          void* const* payloads, int32_t* dev_err, void* stream);
 
 /* decode_chunk (codec.py:522-563): payload of n elements -> y (y_dtype).
  * Only the first n_out <= n values are written (padding strip,
@@ -223,6 +234,46 @@ int fc2_allreduce_oneshot(fc2_comm* c, const fc2_config* cfg, const void* x, int
 int fc2_a2a_q(fc2_comm* c, const fc2_config* cfg, const void* x, int32_t x_dtype, const int64_t* matrix,
               void* y, int32_t y_dtype, int64_t region_off, int64_t region_bytes, int32_t* dev_err,
               double timeout_s, void* stream);
+
+/* ---- MoE token dispatch / combine (BASELINE configs[3]; the reference's
+ * block All2All, collectives.py:428-482, applied to routed token rows) ----- */
+
+/* Routing: topk_ids [tokens][topk] (int32, or int64 when ids_are_int64),
+ * experts split contiguously over world ranks (n_experts / world each).  A
+ * token goes once to every rank holding at least one of its experts.
+ * counts[d]: tokens for rank d; rows[d * tokens + i]: the i-th such token
+ * (ascending); pos[t * world + d]: its index in that list or -1.  Expert ids
+ * outside [0, n_experts) set FC2_ERR_EXPERT_RANGE. */
+int fc2_moe_route(const void* topk_ids, int32_t ids_are_int64, int64_t tokens, int32_t topk, int32_t n_experts,
+                  int32_t world, int32_t* counts, int32_t* rows, int32_t* pos, int32_t* dev_err, void* stream);
+/* y[i] = x[rows[i]] for nrows rows of row_len elements (bf16/f32, 16-byte
+ * aligned); non-finite values set FC2_ERR_NONFINITE (the diagonal block). */
+int fc2_gather_rows_check(const void* x, int32_t x_dtype, const int32_t* rows, int64_t nrows, int64_t row_len,
+                          void* y, int32_t y_dtype, int32_t* dev_err, void* stream);
+/* Combine reduction: out[t] = sum over d = 0..world-1 with pos[t*world+d] >= 0
+ * of srcs[d][pos[t*world+d]] (rows of row_len, dtype src_dtypes[d]), fp32 from
+ * +0.0 in rank order; check_finite[d] flags non-finite rows of source d. */
+int fc2_moe_combine_sum(int32_t world, const void* const* srcs, const int32_t* src_dtypes,
+                        const int32_t* check_finite, const int32_t* pos, int64_t tokens, int64_t row_len, void* out,
+                        int32_t out_dtype, int32_t* dev_err, void* stream);
+/* Small all-gather of n <= 16 int32 values per rank through the communicator
+ * (the token counts): all_out[p * n + k] = value k of rank p (device). */
+int fc2_comm_allgather_i32(fc2_comm* c, const int32_t* mine, int32_t n, int32_t* all_out, int32_t* dev_err,
+                           double timeout_s, void* stream);
+/* SPMD dispatch: token_matrix[s*world + d] = rows rank s sends to d (host,
+ * same on all ranks); rows_dev from fc2_moe_route.  y: the received rows,
+ * per source rank in order (QDQ'd; exact for the rank's own tokens). */
+int fc2_moe_dispatch(fc2_comm* c, const fc2_config* cfg, const void* x, int32_t x_dtype, int64_t tokens,
+                     int64_t row_len, const int32_t* rows_dev, const int64_t* token_matrix, void* y, int32_t y_dtype,
+                     int64_t region_off, int64_t region_bytes, int32_t* dev_err, double timeout_s, void* stream);
+/* SPMD combine: y = the expert outputs in dispatch order; every block goes
+ * back to its source rank with the same codec, and the source sums, per
+ * token, the returned rows in rank order (fc2_moe_combine_sum) into out
+ * [tokens][row_len].  scratch: float32, sum_d token_matrix[rank*world+d] rows. */
+int fc2_moe_combine(fc2_comm* c, const fc2_config* cfg, const void* y, int32_t y_dtype, int64_t tokens,
+                    int64_t row_len, const int64_t* token_matrix, const int32_t* pos_dev, float* scratch, void* out,
+                    int32_t out_dtype, int64_t region_off, int64_t region_bytes, int32_t* dev_err,
+                    double timeout_s, void* stream);
 
 /* Device copy of nbytes (16-byte aligned buffers) with at most `ctas` CTAs
  * (<= 0: 4 per SM); dst may be a peer's symmetric buffer (fc2_comm_buffer), so

@@ -412,6 +412,74 @@ def a2a_combine(blocks, bits, g, sr, intlog=False, theta=10):
 
 
 # ---------------------------------------------------------------------------
+# MoE token dispatch / combine (BASELINE configs[3]) -- the reference's block
+# All2All (collectives.py:428-482) applied to routed token rows
+# ---------------------------------------------------------------------------
+
+
+def moe_route(topk_ids, world: int, n_experts: int):
+    """Per destination rank, the ascending token indices that route to at
+    least one of its experts (experts split contiguously, n_experts // world
+    per rank), and pos[t, d] = the token's index in that list or -1."""
+    ids = np.asarray(topk_ids, dtype=np.int64)
+    per = n_experts // world
+    hit = np.zeros((ids.shape[0], world), dtype=bool)
+    if ids.size:
+        np.put_along_axis(hit, ids // per, True, axis=1)
+    rows = [np.flatnonzero(hit[:, d]) for d in range(world)]
+    pos = np.full((ids.shape[0], world), -1, dtype=np.int64)
+    for d in range(world):
+        pos[rows[d], d] = np.arange(rows[d].size)
+    return rows, pos
+
+
+def moe_dispatch(tokens, topk_ids, bits, g, sr, n_experts, intlog=False, theta=10):
+    """tokens[s]: [T_s, H] float32 of rank s; topk_ids[s]: [T_s, K].
+    Block (s -> d) = rows routes[s][d] of tokens[s], flattened, through
+    :func:`a2a_dispatch` (QDQ'd as one zero-padded chunk, the diagonal exact).
+    Returns recv[d] ([sum_s rows, H] float32, sources in rank order) and the
+    per-source routing (rows, pos)."""
+    N = len(tokens)
+    H = np.asarray(tokens[0]).shape[1]
+    routes = [moe_route(topk_ids[s], N, n_experts) for s in range(N)]
+    matrix = np.array([[routes[s][0][d].size * H for d in range(N)] for s in range(N)], dtype=np.int64)
+    flat = [np.concatenate([np.asarray(tokens[s], dtype=np.float32)[routes[s][0][d]].reshape(-1)
+                            for d in range(N)]) for s in range(N)]
+    out = a2a_dispatch(flat, bits, g, sr, matrix, intlog, theta)
+    recv = [np.concatenate([out[d][s] for s in range(N)]).reshape(-1, H) for d in range(N)]
+    return recv, routes
+
+
+def moe_combine(expert_out, routes, bits, g, sr, intlog=False, theta=10):
+    """expert_out[e]: [rows, H] float32 in rank e's dispatch order (the rows
+    it received, sources in rank order).  Block (e -> s) = the rows that came
+    from s, QDQ'd like dispatch (:func:`a2a_combine`, diagonal exact); rank s
+    sums per token the returned rows over e = 0..N-1 in fp32 from +0.0."""
+    N = len(expert_out)
+    H = np.asarray(expert_out[0]).shape[1]
+    counts = np.array([[routes[s][0][e].size for e in range(N)] for s in range(N)], dtype=np.int64)
+    blocks = [[None] * N for _ in range(N)]
+    for e in range(N):
+        off = 0
+        y = np.asarray(expert_out[e], dtype=np.float32)
+        for s in range(N):
+            k = int(counts[s, e])
+            blocks[e][s] = y[off:off + k].reshape(-1)
+            off += k
+    back = a2a_combine(blocks, bits, g, sr, intlog, theta)
+    outs = []
+    for s in range(N):
+        T = routes[s][1].shape[0]
+        acc = np.zeros((T, H), dtype=np.float32)
+        for e in range(N):
+            rows = back[s][e].reshape(-1, H)
+            sel = routes[s][0][e]
+            acc[sel] = acc[sel] + rows  # float32 + float32, rank order
+        outs.append(acc)
+    return outs
+
+
+# ---------------------------------------------------------------------------
 # synthetic inputs (synthetic.py:25-49) -- used to regenerate benchmark data
 # ---------------------------------------------------------------------------
 

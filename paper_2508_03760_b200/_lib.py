@@ -30,6 +30,7 @@ ERR_LOG2_TIE = 4
 ERR_TIMEOUT = 8
 ERR_CODE_RANGE = 16
 ERR_NEGATIVE = 32
+ERR_EXPERT_RANGE = 64
 
 BF16, F32, F64 = 0, 1, 2
 
@@ -87,6 +88,15 @@ SIGNATURES = {
     "fc2_a2a_q": (_I32, [_P, _PCFG, _P, _I32, _PI64, _P, _I32, _I64, _I64, _P, ctypes.c_double, _P]),
     "fc2_copy_check": (_I32, [_P, _I32, _P, _I32, _I64, _P, _P]),
     "fc2_copy_bytes": (_I32, [_P, _P, _I64, _I32, _P]),
+    "fc2_encode_batch_rows": (_I32, [_PCFG, _I32, _I32, _P, _PP, _I64, _PI64, _PI64, _PP, _P, _P]),
+    "fc2_moe_route": (_I32, [_P, _I32, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P]),
+    "fc2_gather_rows_check": (_I32, [_P, _I32, _P, _I64, _I64, _P, _I32, _P, _P]),
+    "fc2_moe_combine_sum": (_I32, [_I32, _PP, _P, _P, _P, _I64, _I64, _P, _I32, _P, _P]),
+    "fc2_comm_allgather_i32": (_I32, [_P, _P, _I32, _P, _P, ctypes.c_double, _P]),
+    "fc2_moe_dispatch": (_I32, [_P, _PCFG, _P, _I32, _I64, _I64, _P, _PI64, _P, _I32, _I64, _I64, _P,
+                                ctypes.c_double, _P]),
+    "fc2_moe_combine": (_I32, [_P, _PCFG, _P, _I32, _I64, _I64, _PI64, _P, _P, _P, _I32, _I64, _I64, _P,
+                               ctypes.c_double, _P]),
     "fc2_last_error": (ctypes.c_char_p, []),
     "fc2_launch_count": (_I64, []),
     "fc2_version": (_I32, []),
@@ -146,6 +156,8 @@ def raise_dev_err(bits: int, what: str = "") -> None:
         raise CodeRangeError(f"{what}codes out of range")
     if bits & ERR_SPIKE_INDEX:
         raise DecodeFormatError(f"{what}spike index out of range for group size")
+    if bits & ERR_EXPERT_RANGE:
+        raise ConfigError(f"{what}expert id out of range")
     if bits & ERR_TIMEOUT:
         raise RuntimeError(f"{what}cross-rank wait timed out")
 

@@ -387,9 +387,17 @@ static int64_t enc_unit(const fc2_config* cfg, int32_t x_dtype, const void* x, i
 // with a negative t0 so the kernels see absolute tile indices.
 static int encode_batch_impl(const fc2_config* cfg, int32_t x_dtype, int32_t njobs, const void* const* xs,
                              const int64_t* n_valid, const int64_t* n, void* const* payloads, int32_t* dev_err,
-                             void* stream, const int64_t* e_begin, const int64_t* e_end) {
+                             void* stream, const int64_t* e_begin, const int64_t* e_end,
+                             const int32_t* const* rows = nullptr, int64_t row_len = 0) {
   int rc = check_cfg(cfg);
   if (rc) return rc;
+  if (rows) {
+    if (row_len <= 0 || row_len % 8 || row_len > INT32_MAX)
+      return set_err(FC2_ECONFIG, "gathered rows need a row length that is a positive multiple of 8 (got %lld)",
+                     (long long)row_len);
+    for (int i = 0; i < njobs; ++i)
+      if (n[i] > INT32_MAX) return set_err(FC2_ECONFIG, "gathered chunk of %lld elements is too long", (long long)n[i]);
+  }
   if (njobs < 0 || njobs > FC2_MAX_JOBS) return set_err(FC2_ECONFIG, "njobs %d out of range", njobs);
   if ((e_begin || e_end) && njobs != 1) return set_err(FC2_ECONFIG, "sub-range encode takes one job");
   if (x_dtype < 0 || x_dtype > 2) return set_err(FC2_ECONFIG, "bad dtype %d", x_dtype);
@@ -408,7 +416,7 @@ static int encode_batch_impl(const fc2_config* cfg, int32_t x_dtype, int32_t njo
   EncBatch fast, gen;
   for (EncBatch* b : {&fast, &gen}) {
     b->nj = 0; b->B = B; b->G = G; b->sr = sr; b->intlog = cfg->scale_encoding; b->theta = cfg->theta;
-    b->lpg = lpg; b->total = 0; b->lut = lut; b->err = dev_err;
+    b->lpg = lpg; b->row_len = (int)row_len; b->total = 0; b->lut = lut; b->err = dev_err;
   }
   auto launch_gen = [&]() -> int {
     int64_t blocks = (gen.total + 7) / 8;
@@ -439,6 +447,7 @@ static int encode_batch_impl(const fc2_config* cfg, int32_t x_dtype, int32_t njo
     EncJob& j = b->j[b->nj++];
     j.x = xs[i] ? xs[i] : payloads[i];
     j.out = (uint8_t*)payloads[i];
+    j.rows = rows ? rows[i] : nullptr;
     j.n_valid = n_valid[i];
     j.n = n[i];
     // fast tiles: bf16 -> 32 / LPG groups per warp tile; f32 -> 1024 elements; generic: groups
@@ -465,6 +474,15 @@ int fc2_encode_batch(const fc2_config* cfg, int32_t x_dtype, int32_t njobs, cons
                      const int64_t* n_valid, const int64_t* n, void* const* payloads, int32_t* dev_err,
                      void* stream) {
   return encode_batch_impl(cfg, x_dtype, njobs, xs, n_valid, n, payloads, dev_err, stream, nullptr, nullptr);
+}
+
+int fc2_encode_batch_rows(const fc2_config* cfg, int32_t x_dtype, int32_t njobs, const void* x,
+                          const int32_t* const* rows, int64_t row_len, const int64_t* n_valid, const int64_t* n,
+                          void* const* payloads, int32_t* dev_err, void* stream) {
+  if (njobs < 0 || njobs > FC2_MAX_JOBS) return set_err(FC2_ECONFIG, "njobs %d out of range", njobs);
+  std::vector<const void*> xs(njobs > 0 ? njobs : 1, x);
+  return encode_batch_impl(cfg, x_dtype, njobs, xs.data(), n_valid, n, payloads, dev_err, stream, nullptr, nullptr,
+                           rows, row_len);
 }
 
 int fc2_encode(const fc2_config* cfg, const void* x, int32_t x_dtype, int64_t n_valid, int64_t n, void* payload,

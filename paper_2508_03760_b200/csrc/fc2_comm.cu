@@ -3,7 +3,8 @@
 // Every rank owns one symmetric device buffer (cudaMalloc, exported with
 // cudaIpcGetMemHandle, opened by every peer).  Layout of each buffer:
 //
-//   [0, 4096)                      barrier flags: uint32 arrive[FC2_COMM_MAX]
+//   [0, 4096)                      barrier flags: uint32 arrive[FC2_COMM_MAX];
+//                                  [1024, 3072): small all-gather area [parity][rank][16]
 //   [4096, 4096 + N*slot)          landing slots  land[src]   (stage 1, my shard)
 //   [.., + N*slot)                 gather slots   gath[owner] (stage 2)
 //   [.., + a2a_bytes)              All2All receive region
@@ -46,6 +47,7 @@ struct fc2_comm {
   bool opened[FC2_COMM_MAX];
   uint32_t epoch;
   uint32_t oneshot_calls;  // parity selects the one-shot landing buffer
+  uint32_t ag_calls;       // parity selects the small all-gather area
 };
 
 namespace {
@@ -296,16 +298,24 @@ int fc2_allreduce_oneshot(fc2_comm* c, const fc2_config* cfg, const void* x, int
   return fc2_gather_decode(cfg, N, gs.data(), S, y, y_dtype, n, dev_err, stream);
 }
 
+}  // extern "C"
+
+namespace {
+
 // Quantized All2All over the symmetric buffers (collectives.py:428-482 for
-// dispatch; combine = the same call with the transposed matrix).
-// matrix: host int64[N*N], m[src*N + dst] = elements rank src sends to dst.
-// x: this rank's payload, blocks for dst = 0..N-1 back to back.
+// dispatch; combine = the same exchange with the transposed matrix).
+// m: host int64[N*N], m[src*N + dst] = elements rank src sends to dst.
+// x: this rank's payload, blocks for dst = 0..N-1 back to back -- or, with
+//    rows != nullptr (MoE token dispatch), token rows: block dst is the
+//    rows rows[dst * rows_stride + i] of x (row_len elements each), gathered
+//    inside the encoder.
 // y: this rank's receive buffer, blocks from src = 0..N-1 back to back
-//    (y_dtype F32 or BF16); the diagonal block is NOT written here (exact copy,
-//    done by the caller).  region_off: byte offset of the All2All region.
-int fc2_a2a_q(fc2_comm* c, const fc2_config* cfg, const void* x, int32_t x_dtype, const int64_t* matrix,
-              void* y, int32_t y_dtype, int64_t region_off, int64_t region_bytes, int32_t* dev_err,
-              double timeout_s, void* stream) {
+//    (y_dtype F32 or BF16).  The diagonal block is an exact (gather-)copy when
+//    copy_diag, else left untouched.  region_off: byte offset of the All2All
+//    region.
+int a2a_core(fc2_comm* c, const fc2_config* cfg, const void* x, int32_t x_dtype, const int64_t* m,
+             const int32_t* rows, int64_t rows_stride, int64_t row_len, void* y, int32_t y_dtype, bool copy_diag,
+             int64_t region_off, int64_t region_bytes, int32_t* dev_err, double timeout_s, void* stream) {
   const int N = c->world, r = c->rank;
   int rc = fc2_check_config(cfg);
   if (rc) return rc;
@@ -316,9 +326,9 @@ int fc2_a2a_q(fc2_comm* c, const fc2_config* cfg, const void* x, int32_t x_dtype
   auto slot_off = [&](int dst, int src, int64_t* F_out) -> int64_t {
     int64_t off = 0;
     for (int s = 0; s <= src; ++s) {
-      const int64_t m = matrix[(int64_t)s * N + dst];
+      const int64_t v = m[(int64_t)s * N + dst];
       int64_t F = 0;
-      if (s != dst && m > 0) fc2_footprint(cfg, (m + G - 1) / G * G, &F);
+      if (s != dst && v > 0) fc2_footprint(cfg, (v + G - 1) / G * G, &F);
       if (s == src) { *F_out = F; return off; }
       off += (F + 15) / 16 * 16;
     }
@@ -335,25 +345,29 @@ int fc2_a2a_q(fc2_comm* c, const fc2_config* cfg, const void* x, int32_t x_dtype
                      (long long)end, (long long)region_bytes);
   }
   std::vector<const void*> xs;
+  std::vector<const int32_t*> rs;
   std::vector<int64_t> nv, ns;
   std::vector<void*> outs;
   int64_t soff = 0;
   for (int d = 0; d < N; ++d) {
-    const int64_t m = matrix[(int64_t)r * N + d];
-    if (d != r && m > 0) {
+    const int64_t v = m[(int64_t)r * N + d];
+    if (d != r && v > 0) {
       int64_t F = 0;
       const int64_t o = slot_off(d, r, &F);
       xs.push_back((const uint8_t*)x + soff * esz);
-      nv.push_back(m);
-      ns.push_back((m + G - 1) / G * G);
+      rs.push_back(rows ? rows + (int64_t)d * rows_stride : nullptr);
+      nv.push_back(v);
+      ns.push_back((v + G - 1) / G * G);
       outs.push_back(c->peer[d] + FC2_FLAG_BYTES + region_off + o);
     }
-    soff += m;
+    soff += v;
   }
   for (size_t i = 0; i < xs.size(); i += FC2_MAX_JOBS) {
     const int nj = (int)std::min<size_t>(FC2_MAX_JOBS, xs.size() - i);
-    rc = fc2_encode_batch(cfg, x_dtype, nj, xs.data() + i, nv.data() + i, ns.data() + i, outs.data() + i,
-                          dev_err, stream);
+    rc = rows ? fc2_encode_batch_rows(cfg, x_dtype, nj, x, rs.data() + i, row_len, nv.data() + i, ns.data() + i,
+                                      outs.data() + i, dev_err, stream)
+              : fc2_encode_batch(cfg, x_dtype, nj, xs.data() + i, nv.data() + i, ns.data() + i, outs.data() + i,
+                                 dev_err, stream);
     if (rc) return rc;
   }
   rc = fc2_comm_barrier(c, dev_err, timeout_s, stream);
@@ -363,16 +377,16 @@ int fc2_a2a_q(fc2_comm* c, const fc2_config* cfg, const void* x, int32_t x_dtype
   std::vector<void*> ys;
   int64_t roff = 0;
   for (int s = 0; s < N; ++s) {
-    const int64_t m = matrix[(int64_t)s * N + r];
-    if (s != r && m > 0) {
+    const int64_t v = m[(int64_t)s * N + r];
+    if (s != r && v > 0) {
       int64_t F = 0;
       const int64_t o = slot_off(r, s, &F);
       ps.push_back(c->local + FC2_FLAG_BYTES + region_off + o);
-      pn.push_back((m + G - 1) / G * G);
+      pn.push_back((v + G - 1) / G * G);
       ys.push_back((uint8_t*)y + roff * ysz);
-      po.push_back(m);
+      po.push_back(v);
     }
-    roff += m;
+    roff += v;
   }
   for (size_t i = 0; i < ps.size(); i += FC2_MAX_JOBS) {
     const int nj = (int)std::min<size_t>(FC2_MAX_JOBS, ps.size() - i);
@@ -381,18 +395,121 @@ int fc2_a2a_q(fc2_comm* c, const fc2_config* cfg, const void* x, int32_t x_dtype
     if (rc) return rc;
   }
   // diagonal block: exact copy, non-finite values flagged (collectives.py:152-164, 466-468)
-  {
+  if (copy_diag) {
     int64_t so = 0, ro = 0;
-    for (int d = 0; d < r; ++d) so += matrix[(int64_t)r * N + d];
-    for (int s = 0; s < r; ++s) ro += matrix[(int64_t)s * N + r];
-    const int64_t m = matrix[(int64_t)r * N + r];
-    if (m > 0) {
-      rc = fc2_copy_check((const uint8_t*)x + so * esz, x_dtype, (uint8_t*)y + ro * ysz, y_dtype, m, dev_err, stream);
+    for (int d = 0; d < r; ++d) so += m[(int64_t)r * N + d];
+    for (int s = 0; s < r; ++s) ro += m[(int64_t)s * N + r];
+    const int64_t v = m[(int64_t)r * N + r];
+    if (v > 0) {
+      rc = rows ? fc2_gather_rows_check(x, x_dtype, rows + (int64_t)r * rows_stride, v / row_len, row_len,
+                                        (uint8_t*)y + ro * ysz, y_dtype, dev_err, stream)
+                : fc2_copy_check((const uint8_t*)x + so * esz, x_dtype, (uint8_t*)y + ro * ysz, y_dtype, v, dev_err,
+                                 stream);
       if (rc) return rc;
     }
   }
   // everyone has consumed its region before anyone writes the next call's blocks
   return fc2_comm_barrier(c, dev_err, timeout_s, stream);
+}
+
+// plain stores of my n values into every peer's small all-gather area
+__global__ void k_put_small(const int32_t* __restrict__ mine, int n, int rank, int world,
+                            const __grid_constant__ BarrierArgs peers, int64_t area_off) {
+  const int i = (int)threadIdx.x;
+  if (i >= n * world) return;
+  const int p = i / n, k = i % n;
+  int32_t* dst = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(peers.peers[p]) + area_off) + rank * 16 + k;
+  *dst = mine[k];
+}
+
+}  // namespace
+
+extern "C" {
+
+int fc2_a2a_q(fc2_comm* c, const fc2_config* cfg, const void* x, int32_t x_dtype, const int64_t* matrix,
+              void* y, int32_t y_dtype, int64_t region_off, int64_t region_bytes, int32_t* dev_err,
+              double timeout_s, void* stream) {
+  return a2a_core(c, cfg, x, x_dtype, matrix, nullptr, 0, 0, y, y_dtype, true, region_off, region_bytes, dev_err,
+                  timeout_s, stream);
+}
+
+// Small all-gather through the flag page (the MoE token counts): rank r's n
+// (<= 16) int32 values land in every peer's area at [call parity][r]; after
+// the barrier all_out[p * n + k] = value k of rank p.  The parity double
+// buffer keeps a fast peer's next call from overwriting values not yet read.
+int fc2_comm_allgather_i32(fc2_comm* c, const int32_t* mine, int32_t n, int32_t* all_out, int32_t* dev_err,
+                           double timeout_s, void* stream) {
+  if (n < 1 || n > 16) return set_err(FC2_ECONFIG, "small all-gather takes 1..16 values");
+  const int N = c->world;
+  const int par = (int)(c->ag_calls++ & 1u);
+  const int64_t area = 1024 + (int64_t)par * FC2_COMM_MAX * 16 * 4;
+  BarrierArgs pa;
+  for (int p = 0; p < N; ++p) pa.peers[p] = (uint32_t*)c->peer[p];
+  k_put_small<<<1, 256, 0, (cudaStream_t)stream>>>(mine, n, c->rank, N, pa, area);
+  int rc = cuda_check("k_put_small");
+  if (rc) return rc;
+  rc = fc2_comm_barrier(c, dev_err, timeout_s, stream);
+  if (rc) return rc;
+  if (cudaMemcpy2DAsync(all_out, n * sizeof(int32_t), c->local + area, 16 * sizeof(int32_t), n * sizeof(int32_t),
+                        N, cudaMemcpyDeviceToDevice, (cudaStream_t)stream) != cudaSuccess)
+    return set_err(FC2_ECUDA, "cudaMemcpy2DAsync failed");
+  return FC2_OK;
+}
+
+// MoE token dispatch (BASELINE configs[3]): token_matrix[s*N + d] = rows rank
+// s sends to rank d (every rank knows it, e.g. from fc2_moe_route counts and
+// fc2_comm_allgather_i32); rows_dev: this rank's fc2_moe_route lists (dst d
+// at rows_dev + d * tokens).  y receives, per source rank in order, the
+// QDQ'd rows (exact on the diagonal).
+int fc2_moe_dispatch(fc2_comm* c, const fc2_config* cfg, const void* x, int32_t x_dtype, int64_t tokens,
+                     int64_t row_len, const int32_t* rows_dev, const int64_t* token_matrix, void* y, int32_t y_dtype,
+                     int64_t region_off, int64_t region_bytes, int32_t* dev_err, double timeout_s, void* stream) {
+  const int N = c->world;
+  if (row_len <= 0 || row_len % 8) return set_err(FC2_ECONFIG, "row length must be a positive multiple of 8");
+  std::vector<int64_t> m((size_t)N * N);
+  for (int i = 0; i < N * N; ++i) {
+    if (token_matrix[i] < 0 || token_matrix[i] > tokens) return set_err(FC2_ECONFIG, "token matrix entry out of range");
+    m[i] = token_matrix[i] * row_len;
+  }
+  return a2a_core(c, cfg, x, x_dtype, m.data(), rows_dev, tokens, row_len, y, y_dtype, true, region_off,
+                  region_bytes, dev_err, timeout_s, stream);
+}
+
+// MoE combine: the expert rank returns, to every source rank s, the rows it
+// received from s (y holds them in dispatch order), quantized like dispatch;
+// the source rank then sums, per token, the returned rows in destination-rank
+// order in fp32 (exact rows for its own rank): out[t] = sum_d block(d)[pos[t][d]].
+// scratch: float32 rows for every block this rank receives back (the sum of
+// token_matrix[rank][*] rows; the diagonal's share is left unused).
+int fc2_moe_combine(fc2_comm* c, const fc2_config* cfg, const void* y, int32_t y_dtype, int64_t tokens,
+                    int64_t row_len, const int64_t* token_matrix, const int32_t* pos_dev, float* scratch, void* out,
+                    int32_t out_dtype, int64_t region_off, int64_t region_bytes, int32_t* dev_err,
+                    double timeout_s, void* stream) {
+  const int N = c->world, r = c->rank;
+  if (row_len <= 0 || row_len % 8) return set_err(FC2_ECONFIG, "row length must be a positive multiple of 8");
+  std::vector<int64_t> mt((size_t)N * N);  // transposed: expert rank e returns token_matrix[s][e] rows to s
+  for (int s = 0; s < N; ++s)
+    for (int e = 0; e < N; ++e) mt[(size_t)e * N + s] = token_matrix[(size_t)s * N + e] * row_len;
+  int rc = a2a_core(c, cfg, y, y_dtype, mt.data(), nullptr, 0, 0, scratch, FC2_F32, false, region_off, region_bytes,
+                    dev_err, timeout_s, stream);
+  if (rc) return rc;
+  const void* srcs[FC2_COMM_MAX];
+  int32_t dts[FC2_COMM_MAX], chk[FC2_COMM_MAX];
+  int64_t off = 0, yoff = 0;
+  for (int s = 0; s < r; ++s) yoff += token_matrix[(size_t)s * N + r];  // my own tokens' rows inside y
+  for (int d = 0; d < N; ++d) {
+    if (d == r) {
+      srcs[d] = (const uint8_t*)y + yoff * row_len * (y_dtype == FC2_BF16 ? 2 : 4);
+      dts[d] = y_dtype;
+      chk[d] = 1;
+    } else {
+      srcs[d] = scratch + off * row_len;
+      dts[d] = FC2_F32;
+      chk[d] = 0;
+    }
+    off += token_matrix[(size_t)r * N + d];
+  }
+  return fc2_moe_combine_sum(N, srcs, dts, chk, pos_dev, tokens, row_len, out, out_dtype, dev_err, stream);
 }
 
 }  // extern "C"

@@ -47,11 +47,15 @@ inline void smem_attr(int bytes) {
 struct EncJob {
   const void* x;
   uint8_t* out;
+  // row gather (MoE token dispatch): element e of the chunk is x[rows[e / row_len] * row_len + e % row_len]
+  // (nullptr: x is the chunk itself)
+  const int32_t* rows;
   int64_t n_valid, n, t0;  // t0: first global tile (fast) / group (generic)
 };
 struct EncBatch {
   int nj, B, G, sr, intlog, theta;
   int lpg;  // lanes per group of the bf16 lane-per-group encoder (enc_lpg / enc_lpg_small)
+  int row_len;  // elements per gathered row (jobs with rows != nullptr; a multiple of 8)
   int64_t total;
   const double* lut;
   int32_t* err;
@@ -134,7 +138,12 @@ __device__ __forceinline__ void issue_tile(const EncBatch& b, int64_t t, uint8_t
     const int64_t e = e_base + (int64_t)c * S::EPC;
     int64_t valid = jb.n_valid - e;
     valid = valid < 0 ? 0 : (valid > S::EPC ? S::EPC : valid);
-    const void* src = valid > 0 ? (const void*)(x + e) : (const void*)x;
+    const T* p = x + e;
+    if (jb.rows && valid > 0) {  // gathered rows (row_len % 8 == 0: a chunk never straddles rows)
+      const uint32_t q = (uint32_t)e / (uint32_t)b.row_len;
+      p = x + (int64_t)__ldg(jb.rows + q) * b.row_len + ((uint32_t)e - q * (uint32_t)b.row_len);
+    }
+    const void* src = valid > 0 ? (const void*)p : (const void*)x;
     cp_async16(stage + S::pos(c) * 16, src, (int)(valid * sizeof(T)));
   }
 }
@@ -224,14 +233,29 @@ __global__ void __launch_bounds__(kEncWarps * 32) k_encode_fast(const __grid_con
 // ---------------------------------------------------------------------------
 
 template <int G, int LPG>
-__device__ __forceinline__ void issue_grp_tile(const EncJob& jb, int64_t t, uint8_t* stage) {
+__device__ __forceinline__ void issue_grp_tile(const EncJob& jb, int64_t t, uint8_t* stage, int row_len) {
   using IT = GTile<__nv_bfloat16, G, LPG>;
   constexpr int GPT = 32 / LPG;  // groups per warp tile
   const int64_t e0 = (t - jb.t0) * GPT * G;
   const int lane = (int)lane_id();
   const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(jb.x);
   constexpr int NJ = IT::CPG / LPG;  // 16-byte chunks per lane
-  if (e0 + GPT * G <= jb.n_valid) {  // whole tile present: plain 16-byte copies
+  if (jb.rows) {  // MoE dispatch: gathered token rows (a 16-byte chunk never straddles rows)
+    const uint32_t H = (uint32_t)row_len;
+    uint32_t e = (uint32_t)(e0 + 8 * lane);  // chunk lane + 32 j starts at element e + 256 j
+    uint32_t q = e / H, r = e - q * H;
+#pragma unroll 4
+    for (int j = 0; j < NJ; ++j) {
+      const int tc = lane + 32 * j;
+      const int64_t v = jb.n_valid - (int64_t)e;
+      const int valid = v <= 0 ? 0 : (v >= 8 ? 8 : (int)v);
+      const void* src = valid > 0 ? (const void*)(x + (int64_t)__ldg(jb.rows + q) * H + r) : (const void*)x;
+      cp_async16(stage + IT::in_pos(tc / IT::CPG, tc % IT::CPG) * 16, src, valid * 2);
+      e += 256;
+      r += 256;
+      while (r >= H) { r -= H; ++q; }
+    }
+  } else if (e0 + GPT * G <= jb.n_valid) {  // whole tile present: plain 16-byte copies
     const uint8_t* src = reinterpret_cast<const uint8_t*>(x + e0);
     if constexpr (IT::CPG <= 32 && 32 % IT::CPG == 0 && NJ > 8) {
       // chunk lane + 32 j: group g0 + K j, column c; the swizzle only sees
@@ -281,7 +305,7 @@ __device__ __forceinline__ void encode_grp_tile(const EncBatch& b, int64_t t, ui
   const int lane = (int)lane_id();
   const EncJob& jb = b.j[find_job(b, t)];  // one lookup per tile
   __syncwarp();  // previous tile fully consumed
-  issue_grp_tile<G, LPG>(jb, t, in0);
+  issue_grp_tile<G, LPG>(jb, t, in0, b.row_len);
   cp_async_commit();
   cp_async_wait<0>();
   __syncwarp();
@@ -357,6 +381,20 @@ struct PlainLoader {
   __device__ double operator()(int64_t i) const { return load_elem<T>(x, i, nv); }
 };
 
+// gathered rows (MoE token dispatch): element i of the chunk is
+// x[rows[i / H] * H + i % H]; zero past n_valid (the chunk's padding)
+template <typename T>
+struct RowLoader {
+  const T* x;
+  const int32_t* rows;
+  int64_t nv, H;
+  __device__ double operator()(int64_t i) const {
+    if (i >= nv) return 0.0;
+    const int64_t q = i / H;
+    return load_elem<T>(x, (int64_t)__ldg(rows + q) * H + (i - q * H), INT64_MAX);
+  }
+};
+
 template <typename T>
 __global__ void __launch_bounds__(256) k_encode_gen(const __grid_constant__ EncBatch b) {
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -373,8 +411,13 @@ __global__ void __launch_bounds__(256) k_encode_gen(const __grid_constant__ EncB
     OutList o;
     o.p[0] = jb.out;
     o.nd = 1;
-    PlainLoader<T> ld{reinterpret_cast<const T*>(jb.x), jb.n_valid};
-    generic_encode_group(ld, o, jb.n, g - jb.t0, b.B, b.G, b.sr != 0, cx);
+    if (jb.rows) {
+      RowLoader<T> ld{reinterpret_cast<const T*>(jb.x), jb.rows, jb.n_valid, b.row_len};
+      generic_encode_group(ld, o, jb.n, g - jb.t0, b.B, b.G, b.sr != 0, cx);
+    } else {
+      PlainLoader<T> ld{reinterpret_cast<const T*>(jb.x), jb.n_valid};
+      generic_encode_group(ld, o, jb.n, g - jb.t0, b.B, b.G, b.sr != 0, cx);
+    }
   }
 }
 

@@ -1,0 +1,261 @@
+// fc2_moe.cu -- MoE token routing around the quantized All2All (BASELINE
+// configs[3]; the codec fused into token dispatch/combine).
+//
+// The reference's All2All (collectives.py:428-482) moves block (src, dst) of a
+// flat payload: one chunk per block, zero-padded to a group multiple, QDQ'd,
+// the diagonal exact.  For MoE the block (src, dst) is the rows of the
+// tokens of rank src that route to at least one expert on rank dst (one copy
+// per distinct destination rank, token order).  This file holds the pieces
+// around the codec:
+//
+//   k_moe_route     top-k expert ids -> per-destination token lists (rows),
+//                   per-token positions in them (pos) and the counts; one
+//                   CTA, ballot + per-warp prefix, token order preserved
+//   k_gather_rows   the diagonal block: exact gather-copy of token rows with
+//                   the payload finiteness check (collectives.py:152-164)
+//   k_moe_combine   out[t] = sum over destination ranks d in rank order of
+//                   block(d -> me)[pos[t][d]] in fp32 from +0.0 (the QDQ'd
+//                   expert outputs, exact on the diagonal)
+//
+// The gather itself is fused into the encoders (EncJob.rows): the packed
+// block is produced straight from the token rows, no gathered copy in HBM.
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+#include <cstdint>
+
+#include "../../include/fc2.h"
+#include "fc2_common.cuh"
+
+namespace fc2 {
+int set_err(int code, const char* fmt, ...);
+int cuda_check(const char* what);
+int num_sms();
+}  // namespace fc2
+
+using namespace fc2;
+
+#define FC2_MOE_MAX_WORLD 16
+
+namespace {
+
+__device__ __forceinline__ uint32_t route_mask(const void* ids, int idx64, int64_t t, int K, int per,
+                                               int n_experts, int32_t* err) {
+  uint32_t m = 0;
+  for (int k = 0; k < K; ++k) {
+    const int64_t e = idx64 ? reinterpret_cast<const int64_t*>(ids)[t * K + k]
+                            : (int64_t) reinterpret_cast<const int32_t*>(ids)[t * K + k];
+    if (e < 0 || e >= n_experts) {
+      atomicOr(err, FC2_ERR_EXPERT_RANGE);
+      continue;
+    }
+    m |= 1u << (int)(e / per);
+  }
+  return m;
+}
+
+// One CTA of 1024 threads walks the tokens in rounds of 1024 (thread = token).
+// Positions inside a destination list follow token order: ballot rank inside
+// the warp + the warp's offset (scanned by thread d) + the running base.
+__global__ void __launch_bounds__(1024) k_moe_route(const void* ids, int idx64, int64_t T, int K, int per,
+                                                   int n_experts, int world, int32_t* counts, int32_t* rows,
+                                                   int32_t* pos, int32_t* err) {
+  __shared__ int32_t woff[32][FC2_MOE_MAX_WORLD];
+  __shared__ int32_t base[FC2_MOE_MAX_WORLD];
+  const int lane = (int)(threadIdx.x & 31), warp = (int)(threadIdx.x >> 5);
+  const uint32_t lt = (1u << lane) - 1u;
+  if (threadIdx.x < (unsigned)world) base[threadIdx.x] = 0;
+  __syncthreads();
+  for (int64_t t0 = 0; t0 < T; t0 += blockDim.x) {
+    const int64_t t = t0 + threadIdx.x;
+    const uint32_t m = t < T ? route_mask(ids, idx64, t, K, per, n_experts, err) : 0u;
+    for (int d = 0; d < world; ++d) {
+      const uint32_t bal = __ballot_sync(0xffffffffu, (m >> d) & 1u);
+      if (lane == 0) woff[warp][d] = __popc(bal);
+    }
+    __syncthreads();
+    if (threadIdx.x < (unsigned)world) {  // exclusive scan over the warps, per destination
+      const int d = (int)threadIdx.x;
+      int run = base[d];
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+        const int c = woff[w][d];
+        woff[w][d] = run;
+        run += c;
+      }
+      base[d] = run;
+    }
+    __syncthreads();
+    for (int d = 0; d < world; ++d) {
+      const uint32_t bal = __ballot_sync(0xffffffffu, (m >> d) & 1u);
+      if (t < T) {
+        if ((m >> d) & 1u) {
+          const int p = woff[warp][d] + __popc(bal & lt);
+          rows[(int64_t)d * T + p] = (int32_t)t;
+          pos[t * world + d] = p;
+        } else {
+          pos[t * world + d] = -1;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < (unsigned)world) counts[threadIdx.x] = base[threadIdx.x];
+}
+
+template <typename T>
+__device__ __forceinline__ void load8(const T* p, float* v);
+template <>
+__device__ __forceinline__ void load8<__nv_bfloat16>(const __nv_bfloat16* p, float* v) {
+  const uint4 q = *reinterpret_cast<const uint4*>(p);
+  const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    v[2 * i] = __uint_as_float(w[i] << 16);
+    v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+  }
+}
+template <>
+__device__ __forceinline__ void load8<float>(const float* p, float* v) {
+  const float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+
+__device__ __forceinline__ void load8_any(const void* p, int dt, int64_t i, float* v) {
+  if (dt == FC2_BF16) load8<__nv_bfloat16>(reinterpret_cast<const __nv_bfloat16*>(p) + i, v);
+  else load8<float>(reinterpret_cast<const float*>(p) + i, v);
+}
+
+__device__ __forceinline__ void store8_any(void* p, int dt, int64_t i, const float* v) {
+  if (dt == FC2_BF16) {
+    uint32_t w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) w[k] = bf16_bits(v[2 * k]) | (bf16_bits(v[2 * k + 1]) << 16);
+    *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p) + i) = make_uint4(w[0], w[1], w[2], w[3]);
+  } else {
+    float* q = reinterpret_cast<float*>(p) + i;
+    *reinterpret_cast<float4*>(q) = make_float4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<float4*>(q + 4) = make_float4(v[4], v[5], v[6], v[7]);
+  }
+}
+
+// y[r * H + h] = x[rows[r] * H + h], 8 elements per thread-iteration
+__global__ void k_gather_rows(const void* x, int xdt, const int32_t* rows, int64_t nrows, int64_t H, void* y,
+                              int ydt, int32_t* err) {
+  const int64_t n8 = nrows * H / 8;
+  bool bad = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = 8 * i, r = e / H, h = e - r * H;
+    float v[8];
+    load8_any(x, xdt, (int64_t)rows[r] * H + h, v);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) bad |= !isfinite(v[k]);
+    store8_any(y, ydt, e, v);
+  }
+  if (bad) atomicOr(err, FC2_ERR_NONFINITE);
+}
+
+struct CombineArgs {
+  const void* src[FC2_MOE_MAX_WORLD];  // block (d -> me), rows in pos order
+  int dt[FC2_MOE_MAX_WORLD];
+  int check[FC2_MOE_MAX_WORLD];        // exact (diagonal) blocks: flag non-finite values
+  const int32_t* pos;                  // [T][world], -1: token not routed to d
+  int64_t T, H;
+  int world, odt;
+  void* out;
+  int32_t* err;
+};
+
+__global__ void k_moe_combine(const __grid_constant__ CombineArgs a) {
+  const int64_t n8 = a.T * a.H / 8;
+  bool bad = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = 8 * i, t = e / a.H, h = e - t * a.H;
+    float acc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k] = 0.0f;  // fp32 from +0.0, destination ranks in order
+    for (int d = 0; d < a.world; ++d) {
+      const int p = __ldg(a.pos + t * a.world + d);
+      if (p < 0) continue;
+      float v[8];
+      load8_any(a.src[d], a.dt[d], (int64_t)p * a.H + h, v);
+      if (a.check[d]) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) bad |= !isfinite(v[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[k] = __fadd_rn(acc[k], v[k]);
+    }
+    store8_any(a.out, a.odt, e, acc);
+  }
+  if (bad) atomicOr(a.err, FC2_ERR_NONFINITE);
+}
+
+int grid_for(int64_t n8, int threads) {
+  int64_t blocks = (n8 + threads - 1) / threads;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  return (int)(blocks < 1 ? 1 : blocks);
+}
+
+}  // namespace
+
+extern "C" {
+
+int fc2_moe_route(const void* topk_ids, int32_t ids_are_int64, int64_t tokens, int32_t topk, int32_t n_experts,
+                  int32_t world, int32_t* counts, int32_t* rows, int32_t* pos, int32_t* dev_err, void* stream) {
+  if (world < 1 || world > FC2_MOE_MAX_WORLD) return set_err(FC2_ECONFIG, "world %d outside [1, 16]", world);
+  if (n_experts < world || n_experts % world)
+    return set_err(FC2_ECONFIG, "%d experts do not split evenly over %d ranks", n_experts, world);
+  if (topk < 1 || tokens < 0 || tokens > INT32_MAX) return set_err(FC2_ECONFIG, "bad routing shape");
+  if (tokens == 0) return cudaMemsetAsync(counts, 0, sizeof(int32_t) * world, (cudaStream_t)stream) == cudaSuccess
+                              ? FC2_OK
+                              : set_err(FC2_ECUDA, "cudaMemsetAsync failed");
+  k_moe_route<<<1, 1024, 0, (cudaStream_t)stream>>>(topk_ids, ids_are_int64 ? 1 : 0, tokens, topk,
+                                                   n_experts / world, n_experts, world, counts, rows, pos, dev_err);
+  return cuda_check("k_moe_route");
+}
+
+int fc2_gather_rows_check(const void* x, int32_t x_dtype, const int32_t* rows, int64_t nrows, int64_t row_len,
+                          void* y, int32_t y_dtype, int32_t* dev_err, void* stream) {
+  if (nrows <= 0) return FC2_OK;
+  if (row_len <= 0 || row_len % 8) return set_err(FC2_ECONFIG, "row length must be a positive multiple of 8");
+  if ((x_dtype != FC2_BF16 && x_dtype != FC2_F32) || (y_dtype != FC2_BF16 && y_dtype != FC2_F32))
+    return set_err(FC2_ECONFIG, "gather supports bf16 / f32");
+  if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15u)
+    return set_err(FC2_ECONFIG, "gather needs 16-byte aligned buffers");
+  const int64_t n8 = nrows * row_len / 8;
+  k_gather_rows<<<grid_for(n8, 256), 256, 0, (cudaStream_t)stream>>>(x, x_dtype, rows, nrows, row_len, y, y_dtype,
+                                                                   dev_err);
+  return cuda_check("k_gather_rows");
+}
+
+int fc2_moe_combine_sum(int32_t world, const void* const* srcs, const int32_t* src_dtypes,
+                        const int32_t* check_finite, const int32_t* pos, int64_t tokens, int64_t row_len, void* out,
+                        int32_t out_dtype, int32_t* dev_err, void* stream) {
+  if (world < 1 || world > FC2_MOE_MAX_WORLD) return set_err(FC2_ECONFIG, "world %d outside [1, 16]", world);
+  if (tokens <= 0) return FC2_OK;
+  if (row_len <= 0 || row_len % 8) return set_err(FC2_ECONFIG, "row length must be a positive multiple of 8");
+  if (out_dtype != FC2_BF16 && out_dtype != FC2_F32) return set_err(FC2_ECONFIG, "combine output is bf16 / f32");
+  CombineArgs a;
+  for (int d = 0; d < world; ++d) {
+    if (src_dtypes[d] != FC2_BF16 && src_dtypes[d] != FC2_F32) return set_err(FC2_ECONFIG, "combine source dtype");
+    if (reinterpret_cast<uintptr_t>(srcs[d]) & 15u) return set_err(FC2_ECONFIG, "combine sources must be 16-byte aligned");
+    a.src[d] = srcs[d];
+    a.dt[d] = src_dtypes[d];
+    a.check[d] = check_finite ? check_finite[d] : 0;
+  }
+  if (reinterpret_cast<uintptr_t>(out) & 15u) return set_err(FC2_ECONFIG, "combine output must be 16-byte aligned");
+  a.pos = pos;
+  a.T = tokens;
+  a.H = row_len;
+  a.world = world;
+  a.odt = out_dtype;
+  a.out = out;
+  a.err = dev_err;
+  const int64_t n8 = tokens * row_len / 8;
+  k_moe_combine<<<grid_for(n8, 256), 256, 0, (cudaStream_t)stream>>>(a);
+  return cuda_check("k_moe_combine");
+}
+
+}  // extern "C"

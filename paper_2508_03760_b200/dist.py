@@ -289,6 +289,69 @@ class QComm:
             self.check()
         return y
 
+    def moe_dispatch(self, x: torch.Tensor, topk_ids: torch.Tensor, n_experts: int = 256,
+                     out_dtype: torch.dtype = torch.bfloat16, check: bool = False):
+        """Quantized MoE token dispatch (BASELINE configs[3]; moe.moe_dispatch_q
+        is the simulated form).  ``x``: [T, H] bf16/f32 tokens of this rank,
+        ``topk_ids``: [T, K] expert ids (experts split contiguously over the
+        ranks).  Routing runs on the device (``fc2_moe_route``), the counts are
+        all-gathered through the communicator (one host read), and every
+        remote block is gather-encoded straight from the token rows into the
+        receiver's All2All region.  Returns ``(recv, handle)``: recv [R, H]
+        holds the rows from source ranks in order; ``handle`` feeds
+        :meth:`moe_combine`."""
+        from .moe import route
+
+        if self.transport != "ipc":
+            raise ConfigError("moe_dispatch is implemented on the ipc transport")
+        if x.dim() != 2:
+            raise ConfigError(f"tokens must be [tokens, hidden], got shape {tuple(x.shape)}")
+        x = x.contiguous()
+        T, H = x.shape
+        N, r = self.world, self.rank
+        counts, rows, pos = route(topk_ids.to(self.device), N, n_experts, self.err)
+        allc = torch.empty(N * N, dtype=torch.int32, device=self.device)
+        _lib.check(_lib.lib().fc2_comm_allgather_i32(self._c, counts.data_ptr(), N, allc.data_ptr(),
+                                                     self.err.data_ptr(), self.timeout_s, _device.stream_handle()))
+        tm = np.ascontiguousarray(allc.cpu().numpy().astype(np.int64).reshape(N, N))
+        if int(self.err.item()):
+            self.check()
+        y = torch.empty((int(tm[:, r].sum()), H), dtype=out_dtype, device=self.device)
+        c = self.cfg.c_struct()
+        _lib.check(_lib.lib().fc2_moe_dispatch(
+            self._c, ctypes.byref(c), x.data_ptr(), _device.dtype_code(x), T, H, rows.data_ptr(),
+            tm.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), y.data_ptr(), _device.dtype_code(y),
+            self.a2a_off, self.a2a_bytes, self.err.data_ptr(), self.timeout_s, _device.stream_handle()))
+        if check:
+            self.check()
+        return y, {"matrix": tm, "rows": rows, "pos": pos, "tokens": T, "hidden": H}
+
+    def moe_combine(self, y: torch.Tensor, handle: dict, out: torch.Tensor | None = None,
+                    out_dtype: torch.dtype = torch.bfloat16, check: bool = False) -> torch.Tensor:
+        """Quantized MoE combine: ``y`` = the expert outputs [R, H] in the
+        order :meth:`moe_dispatch` delivered the rows.  Each block returns to
+        its source rank with the same codec; the result [T, H] is, per token,
+        the fp32 sum of its returned rows in rank order (exact for this rank's
+        own experts)."""
+        if self.transport != "ipc":
+            raise ConfigError("moe_combine is implemented on the ipc transport")
+        tm, T, H = handle["matrix"], handle["tokens"], handle["hidden"]
+        N, r = self.world, self.rank
+        y = y.contiguous()
+        if y.dim() != 2 or y.shape[1] != H or y.shape[0] != int(tm[:, r].sum()):
+            raise ConfigError(f"expert outputs must be [{int(tm[:, r].sum())}, {H}], got {tuple(y.shape)}")
+        res = out if out is not None else torch.empty((T, H), dtype=out_dtype, device=self.device)
+        scratch = _device.workspace("moe_scratch", max(16, 4 * int(tm[r].sum()) * H), self.device)
+        c = self.cfg.c_struct()
+        _lib.check(_lib.lib().fc2_moe_combine(
+            self._c, ctypes.byref(c), y.data_ptr(), _device.dtype_code(y), T, H,
+            tm.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), handle["pos"].data_ptr(), scratch.data_ptr(),
+            res.data_ptr(), _device.dtype_code(res), self.a2a_off, self.a2a_bytes, self.err.data_ptr(),
+            self.timeout_s, _device.stream_handle()))
+        if check:
+            self.check()
+        return res
+
     def check(self) -> None:
         """Raise for any error bit the device set since the last check (the
         reference's DataError / DecodeFormatError, or a cross-rank timeout), then

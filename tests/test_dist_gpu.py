@@ -50,6 +50,25 @@ def _worker(rank, world, port, case, q):
                     y = comm.all_reduce(x.to(dt), check=True, algo=algo)
                     outs.append(y.float().cpu().numpy().tobytes())
             q.put((rank, outs))
+        elif kind == "moe":
+            # n = tokens per rank; hidden 512, top-4 of 16 experts; two rounds so
+            # the small all-gather's parity buffers and the region reuse run
+            from paper_2508_03760_b200.dist import moe_region_bytes
+
+            T, H, K, E = n, 512, 4, 16
+            ids = [np.argsort(np.random.default_rng(70 + s).random((T, E)), axis=1)[:, :K] for s in range(world)]
+            cap = moe_region_bytes(cfg, world, T, H, np.stack(ids), experts=E)
+            comm = QComm(max_elems=g * world, config=cfg, a2a_bytes=cap, timeout_s=120.0)
+            x = O.bf16_snap(O.spiky(T * H, seeds[rank])).astype(np.float32).reshape(T, H)
+            outs = []
+            for rnd in range(2):
+                recv, h = comm.moe_dispatch(torch.from_numpy(x).cuda().to(torch.bfloat16),
+                                            torch.from_numpy(ids[rank]).cuda(), n_experts=E,
+                                            out_dtype=torch.float32, check=True)
+                yo = (recv * 0.5 + 1.0).to(torch.bfloat16)
+                back = comm.moe_combine(yo, h, out_dtype=torch.float32, check=True)
+                outs.append((recv.cpu().numpy().tobytes(), back.cpu().numpy().tobytes()))
+            q.put((rank, outs))
         elif kind == "a2a_errors":
             # (1) blocks that do not fit the All2All region -> ConfigError (the
             # one-shot region behind it must never be overwritten); (2) NaN in
@@ -133,3 +152,19 @@ def test_ipc_all2all_region_bounds_and_error_reset():
     got = _run(2, ("a2a_errors", 0, 4, 128, True, 0))
     for r in range(2):
         assert got[r] == ["config", "data", True]
+
+
+@pytest.mark.parametrize("world,T,bits,g,sr", [(2, 96, 4, 128, True), (4, 50, 3, 32, False), (8, 64, 4, 128, True)])
+def test_ipc_moe_dispatch_combine_matches_oracle(world, T, bits, g, sr):
+    got = _run(world, ("moe", T, bits, g, sr, 13))
+    seeds = O.child_seeds(13, world)
+    H, K, E = 512, 4, 16
+    toks = [O.bf16_snap(O.spiky(T * H, seeds[s])).astype(np.float32).reshape(T, H) for s in range(world)]
+    ids = [np.argsort(np.random.default_rng(70 + s).random((T, E)), axis=1)[:, :K] for s in range(world)]
+    want, routes = O.moe_dispatch(toks, ids, bits, g, sr, E)
+    yo = [O.bf16_snap(w * 0.5 + 1.0).astype(np.float32) for w in want]
+    want_c = O.moe_combine(yo, routes, bits, g, sr)
+    for r in range(world):
+        for recv, back in got[r]:
+            assert np.array_equal(np.frombuffer(recv, dtype=np.float32).reshape(-1, H), want[r])
+            assert np.array_equal(np.frombuffer(back, dtype=np.float32).reshape(-1, H), want_c[r])
