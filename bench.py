@@ -350,6 +350,92 @@ def two_step_stage_times(fc, x, cfg, flush, steps, N=8):
     return out
 
 
+def moe_stage_times(fc, cfg, flush, steps, world=8, seed=4242):
+    """Per-rank kernels of the EP = 8 MoE dispatch + combine at the configs[3]
+    shape (4096 tokens x 7168, top-8 of 256), on one GPU: device routing,
+    gather-encode of the 7 remote token blocks straight from the token rows
+    (one launch), decode of 7 received blocks, decode of the 7 returned
+    blocks + the rank-order fp32 combine.  The received blocks are stand-ins
+    of the right sizes (this rank's own blocks), as in two_step_stage_times."""
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    from paper_2508_03760_b200 import moe as M
+    from paper_2508_03760_b200.collectives import _decode_jobs
+
+    dev = torch.device("cuda", 0)
+    T, H, E = MOE["tokens"], MOE["hidden"], MOE["experts"]
+    x = spiky_bf16(T * H, 11, dev).reshape(T, H)
+    ids = moe_routing(1, T, seed)[0].to(dev)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    counts, rows, pos = M.route(ids, world, E, err)
+    cnt = counts.cpu().numpy().astype(np.int64)
+    r = 0  # this rank
+    G = cfg.group_size
+    remote = [d for d in range(world) if d != r and cnt[d]]
+    Fs = {d: fc.footprint_bytes(cfg, -(-int(cnt[d]) * H // G) * G) for d in remote}
+    offs, tot = {}, 0
+    for d in remote:
+        offs[d] = tot
+        tot += (Fs[d] + 15) // 16 * 16
+    pay = torch.empty(tot, dtype=torch.uint8, device=dev)
+    recv = torch.empty((int(cnt.sum()), H), dtype=torch.float32, device=dev)
+    out = torch.empty((T, H), dtype=torch.bfloat16, device=dev)
+    c = cfg.c_struct()
+    lib = fc._lib.lib()
+    st = lambda: torch.cuda.current_stream().cuda_stream  # noqa: E731
+
+    def rte():
+        M.route(ids, world, E, err)
+
+    def enc():
+        fc._lib.check(lib.fc2_encode_batch_rows(
+            ctypes.byref(c), 0, len(remote), x.data_ptr(), fc._lib.ptr_array([rows.data_ptr() + 4 * d * T for d in remote]),
+            H, fc._lib.i64_array([int(cnt[d]) * H for d in remote]),
+            fc._lib.i64_array([-(-int(cnt[d]) * H // G) * G for d in remote]),
+            fc._lib.ptr_array([pay.data_ptr() + offs[d] for d in remote]), err.data_ptr(), st()))
+
+    roff = np.concatenate([[0], np.cumsum(cnt)])
+
+    def dec():
+        _decode_jobs(cfg, fc._lib.F32, [(pay.data_ptr() + offs[d], -(-int(cnt[d]) * H // G) * G,
+                                         recv[int(roff[d]):].data_ptr(), int(cnt[d]) * H) for d in remote], err)
+
+    pays = [pay.data_ptr() + offs[d] if d in offs else pay.data_ptr() for d in range(world)]
+    ns = [-(-int(cnt[d]) * H // G) * G for d in range(world)]
+    diag = x[:int(cnt[r])].contiguous()  # stand-in for this rank's own expert rows (exact)
+
+    def comb():  # fused: packed returned blocks + exact own rows -> rank-order fp32 sum
+        fc._lib.check(lib.fc2_moe_combine_q(
+            ctypes.byref(c), world, r, fc._lib.ptr_array(pays), fc._lib.i64_array(ns), diag.data_ptr(), 0,
+            pos.data_ptr(), T, H, out.data_ptr(), 0, err.data_ptr(), st()))
+
+    rows_out = int(cnt.sum() - cnt[r])
+    res = {"shape": f"{T} tok x {H}, top-{MOE['topk']} of {E}, EP={world} (rank 0 of a simulated EP group)",
+           "rows_sent_remote": rows_out, "copies_per_token": round(float(cnt.sum()) / T, 3)}
+    for name, fn, nbytes in (("route", rte, T * MOE["topk"] * 8 + T * world * 4),
+                             ("dispatch_gather_encode", enc, rows_out * H * 2 + tot),
+                             ("dispatch_decode", dec, tot + rows_out * H * 4),
+                             ("combine_fused", comb, tot + int(cnt[r]) * H * 2 + T * H * 2)):
+        for _ in range(2):
+            fn()
+        ts = []
+        for _ in range(steps):
+            flush_l2(flush)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        t = statistics.mean(ts)
+        res[name] = {"us": round(t * 1e3, 2), "bytes": int(nbytes), "GBps": round(nbytes / (t * 1e-3) / 1e9, 1)}
+    fc._device.check_err(err)
+    return res
+
+
 def time_e2e(fc, x_host, cfg, steps, warmup, serial=False):
     """Host-buffer round trip through the public API: pinned bf16 chunk in ->
     packed payload bytes and decoded bf16 values back in pinned host memory.
@@ -512,6 +598,7 @@ def run_codec(args):
                                         "decode_GBps": round((Fb + 2 * n) / (td * 1e-3) / 1e9, 1),
                                         "payload_bytes": Fb}
     stages = two_step_stage_times(fc, x, cfg, flush, max(3, args.steps // 2))
+    moe_stages = None if args.no_moe else moe_stage_times(fc, cfg, flush, max(3, args.steps // 2))
     # message-size sweep of the codec round trip (BASELINE configs[4] sizes,
     # 64 KB .. 1 GB of bf16 per call), same cfg, L2 flushed before each step
     size_sweep = {}
@@ -569,6 +656,7 @@ def run_codec(args):
                       f"{cpu_dt:.2f} s per round trip"},
         "sweep": sweep,
         "two_step_n8_per_rank_kernels": stages,
+        "moe_ep8_per_rank_kernels": moe_stages,
         "size_sweep": size_sweep,
         "gpu_launches": launches,
         "clocks": clk.summary(),

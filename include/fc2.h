@@ -256,6 +256,14 @@ int fc2_gather_rows_check(const void* x, int32_t x_dtype, const int32_t* rows, i
 int fc2_moe_combine_sum(int32_t world, const void* const* srcs, const int32_t* src_dtypes,
                         const int32_t* check_finite, const int32_t* pos, int64_t tokens, int64_t row_len, void* out,
                         int32_t out_dtype, int32_t* dev_err, void* stream);
+/* Fused combine straight from the packed returned blocks: payloads[d] holds
+ * block (d -> me) as one chunk of chunk_n[d] elements (d != me); exact: my own
+ * block's rows (dtype exact_dtype).  Same result as decoding every block to
+ * float32 and calling fc2_moe_combine_sum, without the float32 round trip.
+ * Needs group_size % 32 == 0 and row_len % 32 == 0 (else FC2_ENOTAPPLICABLE). */
+int fc2_moe_combine_q(const fc2_config* cfg, int32_t world, int32_t me, const void* const* payloads,
+                      const int64_t* chunk_n, const void* exact, int32_t exact_dtype, const int32_t* pos,
+                      int64_t tokens, int64_t row_len, void* out, int32_t out_dtype, int32_t* dev_err, void* stream);
 /* Small all-gather of n <= 16 int32 values per rank through the communicator
  * (the token counts): all_out[p * n + k] = value k of rank p (device). */
 int fc2_comm_allgather_i32(fc2_comm* c, const int32_t* mine, int32_t n, int32_t* all_out, int32_t* dev_err,

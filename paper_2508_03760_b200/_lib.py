@@ -92,6 +92,7 @@ SIGNATURES = {
     "fc2_moe_route": (_I32, [_P, _I32, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P]),
     "fc2_gather_rows_check": (_I32, [_P, _I32, _P, _I64, _I64, _P, _I32, _P, _P]),
     "fc2_moe_combine_sum": (_I32, [_I32, _PP, _P, _P, _P, _I64, _I64, _P, _I32, _P, _P]),
+    "fc2_moe_combine_q": (_I32, [_PCFG, _I32, _I32, _PP, _PI64, _P, _I32, _P, _I64, _I64, _P, _I32, _P, _P]),
     "fc2_comm_allgather_i32": (_I32, [_P, _P, _I32, _P, _P, ctypes.c_double, _P]),
     "fc2_moe_dispatch": (_I32, [_P, _PCFG, _P, _I32, _I64, _I64, _P, _PI64, _P, _I32, _I64, _I64, _P,
                                 ctypes.c_double, _P]),

@@ -319,6 +319,9 @@ static const double* lut_for(const fc2_config* c, int* rc) {
   return g_lut[dev] + (size_t)(c->theta - 1) * 256;
 }
 
+// for the other translation units (fc2_moe.cu)
+const double* lut_for_cfg(const fc2_config* c, int* rc) { return lut_for(c, rc); }
+
 static int64_t rec_nb(const fc2_config* c) { return rec_bytes(c->scheme == 1, c->scale_encoding == 1); }
 
 }  // namespace fc2

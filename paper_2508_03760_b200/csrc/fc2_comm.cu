@@ -313,27 +313,36 @@ namespace {
 //    (y_dtype F32 or BF16).  The diagonal block is an exact (gather-)copy when
 //    copy_diag, else left untouched.  region_off: byte offset of the All2All
 //    region.
+// byte offset of the block src -> dst inside dst's All2All region (blocks of
+// sources 0..N-1 back to back, 16-byte aligned slots; the diagonal and empty
+// blocks take no space); *F_out = the block's payload bytes
+int64_t a2a_slot(const fc2_config* cfg, const int64_t* m, int N, int dst, int src, int64_t* F_out) {
+  const int64_t G = cfg->group_size;
+  int64_t off = 0;
+  for (int s = 0; s <= src; ++s) {
+    const int64_t v = m[(int64_t)s * N + dst];
+    int64_t F = 0;
+    if (s != dst && v > 0) fc2_footprint(cfg, (v + G - 1) / G * G, &F);
+    if (s == src) { *F_out = F; return off; }
+    off += (F + 15) / 16 * 16;
+  }
+  return off;
+}
+
+// decode_recv = false: the received blocks stay packed in the region (the
+// fused MoE combine reads them there) and the trailing barrier is the
+// caller's, after it has consumed them.
 int a2a_core(fc2_comm* c, const fc2_config* cfg, const void* x, int32_t x_dtype, const int64_t* m,
              const int32_t* rows, int64_t rows_stride, int64_t row_len, void* y, int32_t y_dtype, bool copy_diag,
-             int64_t region_off, int64_t region_bytes, int32_t* dev_err, double timeout_s, void* stream) {
+             int64_t region_off, int64_t region_bytes, int32_t* dev_err, double timeout_s, void* stream,
+             bool decode_recv = true) {
   const int N = c->world, r = c->rank;
   int rc = fc2_check_config(cfg);
   if (rc) return rc;
   const int64_t G = cfg->group_size;
   const int esz = x_dtype == FC2_BF16 ? 2 : (x_dtype == FC2_F32 ? 4 : 8);
   const int ysz = y_dtype == FC2_BF16 ? 2 : (y_dtype == FC2_F32 ? 4 : 8);
-  // slot offset of the block src -> dst inside dst's region
-  auto slot_off = [&](int dst, int src, int64_t* F_out) -> int64_t {
-    int64_t off = 0;
-    for (int s = 0; s <= src; ++s) {
-      const int64_t v = m[(int64_t)s * N + dst];
-      int64_t F = 0;
-      if (s != dst && v > 0) fc2_footprint(cfg, (v + G - 1) / G * G, &F);
-      if (s == src) { *F_out = F; return off; }
-      off += (F + 15) / 16 * 16;
-    }
-    return off;
-  };
+  auto slot_off = [&](int dst, int src, int64_t* F_out) -> int64_t { return a2a_slot(cfg, m, N, dst, src, F_out); };
   if (region_off < 0 || region_bytes < 0 || region_off + region_bytes + FC2_FLAG_BYTES > c->bytes)
     return set_err(FC2_ECONFIG, "a2a region [%lld, +%lld) outside the communicator buffer", (long long)region_off,
                    (long long)region_bytes);
@@ -371,7 +380,7 @@ int a2a_core(fc2_comm* c, const fc2_config* cfg, const void* x, int32_t x_dtype,
     if (rc) return rc;
   }
   rc = fc2_comm_barrier(c, dev_err, timeout_s, stream);
-  if (rc) return rc;
+  if (rc || !decode_recv) return rc;
   std::vector<const void*> ps;
   std::vector<int64_t> pn, po;
   std::vector<void*> ys;
@@ -490,9 +499,27 @@ int fc2_moe_combine(fc2_comm* c, const fc2_config* cfg, const void* y, int32_t y
   std::vector<int64_t> mt((size_t)N * N);  // transposed: expert rank e returns token_matrix[s][e] rows to s
   for (int s = 0; s < N; ++s)
     for (int e = 0; e < N; ++e) mt[(size_t)e * N + s] = token_matrix[(size_t)s * N + e] * row_len;
+  const bool fused = cfg->group_size % 32 == 0 && row_len % 32 == 0;
   int rc = a2a_core(c, cfg, y, y_dtype, mt.data(), nullptr, 0, 0, scratch, FC2_F32, false, region_off, region_bytes,
-                    dev_err, timeout_s, stream);
+                    dev_err, timeout_s, stream, !fused);
   if (rc) return rc;
+  if (fused) {  // read the returned blocks packed, straight from the region
+    const void* pays[FC2_COMM_MAX];
+    int64_t ns[FC2_COMM_MAX];
+    int64_t yoff = 0;
+    for (int s = 0; s < r; ++s) yoff += token_matrix[(size_t)s * N + r];
+    for (int d = 0; d < N; ++d) {
+      int64_t F = 0;
+      const int64_t v = mt[(size_t)d * N + r];
+      pays[d] = c->local + FC2_FLAG_BYTES + region_off + a2a_slot(cfg, mt.data(), N, r, d, &F);
+      ns[d] = (v + cfg->group_size - 1) / cfg->group_size * cfg->group_size;
+    }
+    rc = fc2_moe_combine_q(cfg, N, r, pays, ns, (const uint8_t*)y + yoff * row_len * (y_dtype == FC2_BF16 ? 2 : 4),
+                           y_dtype, pos_dev, tokens, row_len, out, out_dtype, dev_err, stream);
+    if (rc) return rc;
+    // everyone has consumed its region before anyone writes the next call's blocks
+    return fc2_comm_barrier(c, dev_err, timeout_s, stream);
+  }
   const void* srcs[FC2_COMM_MAX];
   int32_t dts[FC2_COMM_MAX], chk[FC2_COMM_MAX];
   int64_t off = 0, yoff = 0;

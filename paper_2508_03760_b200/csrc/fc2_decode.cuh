@@ -135,6 +135,39 @@ __device__ __forceinline__ void dq_run32(const uint8_t* payload, int64_t n, int6
   }
 }
 
+// 32 code values (as 2^23 + code float bits) of one 32-element run from its plane words
+// (unit-major: w[O .. O + W) are unit u's words)
+template <int B>
+__device__ __forceinline__ void run_code_floats(const uint32_t* w, uint32_t* cf) {
+  if constexpr (B == 4) {
+#pragma unroll
+    for (int wd = 0; wd < 4; ++wd) {
+      const uint32_t ev = w[wd] & 0x0F0F0F0Fu, od = (w[wd] >> 4) & 0x0F0F0F0Fu;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        cf[8 * wd + 2 * k] = __byte_perm(ev, 0x4B000000u, 0x7650 + k);
+        cf[8 * wd + 2 * k + 1] = __byte_perm(od, 0x4B000000u, 0x7650 + k);
+      }
+    }
+  } else if constexpr (B == 8) {
+#pragma unroll
+    for (int wd = 0; wd < 8; ++wd)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) cf[4 * wd + k] = __byte_perm(w[wd], 0x4B000000u, 0x7650 + k);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      uint32_t c = 0;
+#pragma unroll
+      for (int u = 0; u < n_units(B); ++u) {
+        const int W = unit_w(B, u), O = unit_off(B, u);
+        c |= ((w[O + ((k * W) >> 5)] >> ((k * W) & 31)) & ((1u << W) - 1u)) << O;
+      }
+      cf[k] = 0x4B000000u | c;
+    }
+  }
+}
+
 // Code of one element (generic path, any alignment).
 __device__ __forceinline__ uint32_t load_code1(const uint8_t* payload, int64_t n, int64_t e, int B) {
   uint32_t c = 0;

@@ -26,11 +26,13 @@
 
 #include "../../include/fc2.h"
 #include "fc2_common.cuh"
+#include "fc2_decode.cuh"
 
 namespace fc2 {
 int set_err(int code, const char* fmt, ...);
 int cuda_check(const char* what);
 int num_sms();
+const double* lut_for_cfg(const fc2_config* c, int* rc);
 }  // namespace fc2
 
 using namespace fc2;
@@ -191,6 +193,126 @@ __global__ void k_moe_combine(const __grid_constant__ CombineArgs a) {
   if (bad) atomicOr(a.err, FC2_ERR_NONFINITE);
 }
 
+// Fused combine: the returned blocks are read in their packed form (no float32
+// round trip through HBM).  Warp = one 1024-element segment of one token,
+// lane = one 32-element run; per source rank d in order, the lane decodes
+// its run of row pos[t][d] of block d (codes + the group's record, reserved
+// spikes patched through a per-lane smem row) or reads the exact row of its
+// own block, and adds in fp32.  Needs G % 32 == 0 and H % 32 == 0.
+struct CombineQArgs {
+  const uint8_t* pay[FC2_MOE_MAX_WORLD];  // block (d -> me), packed; unused for d == me
+  int64_t n[FC2_MOE_MAX_WORLD];           // its chunk length (padded to a group multiple)
+  const void* exact;                      // my own block's rows (d == me), dtype edt
+  int edt;
+  int me, world, B, G, sr, intlog, theta;
+  const double* lut;
+  const int32_t* pos;                     // [T][world]
+  int64_t T, H;
+  void* out;
+  int odt;
+  int32_t* err;
+};
+
+template <int B>
+__global__ void __launch_bounds__(256, 2) k_moe_combine_q(const __grid_constant__ CombineQArgs a) {
+  __shared__ __align__(16) float spill_all[8][32][36];
+  const int warp = (int)(threadIdx.x >> 5), lane = (int)(threadIdx.x & 31);
+  float* spill = spill_all[warp][lane];
+  const int64_t segs = (a.H + 1023) / 1024;
+  const int64_t tasks = a.T * segs;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  bool bad = false;
+  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; w < tasks; w += nw) {
+    const int64_t t = w / segs;
+    const int64_t h = (w - t * segs) * 1024 + 32 * lane;
+    const bool on = h < a.H;
+    float acc[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) acc[k] = 0.0f;  // fp32 from +0.0, source ranks in order
+    for (int d = 0; d < a.world; ++d) {
+      const int p = __ldg(a.pos + t * a.world + d);
+      if (p < 0 || !on) continue;
+      const int64_t e0 = (int64_t)p * a.H + h;  // element of block d
+      float v[32];
+      if (d == a.me) {
+#pragma unroll
+        for (int k = 0; k < 32; k += 8) load8_any(a.exact, a.edt, e0 + k, v + k);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) bad |= !isfinite(v[k]);
+      } else {
+        // the run's plane words (unit-major), vector loads: slots are 16-byte
+        // aligned and chunk lengths multiples of 32, so unit u's 4W bytes are
+        // 4W-aligned
+        const uint8_t* P = a.pay[d];
+        const int64_t nd = a.n[d];
+        uint32_t w[B];
+#pragma unroll
+        for (int u = 0; u < n_units(B); ++u) {
+          const int W = unit_w(B, u), O = unit_off(B, u);
+          const uint8_t* q = P + nd * O / 8 + e0 * W / 8;
+          if (W == 8) {
+            const uint4 q0 = __ldg(reinterpret_cast<const uint4*>(q)), q1 = __ldg(reinterpret_cast<const uint4*>(q + 16));
+            w[O] = q0.x; w[O + 1] = q0.y; w[O + 2] = q0.z; w[O + 3] = q0.w;
+            w[O + 4] = q1.x; w[O + 5] = q1.y; w[O + 6] = q1.z; w[O + 7] = q1.w;
+          } else if (W == 4) {
+            const uint4 q0 = __ldg(reinterpret_cast<const uint4*>(q));
+            w[O] = q0.x; w[O + 1] = q0.y; w[O + 2] = q0.z; w[O + 3] = q0.w;
+          } else if (W == 2) {
+            const uint2 q0 = __ldg(reinterpret_cast<const uint2*>(q));
+            w[O] = q0.x; w[O + 1] = q0.y;
+          } else {
+            w[O] = __ldg(reinterpret_cast<const uint32_t*>(q));
+          }
+        }
+        DecCtx c;
+        c.n = nd;
+        c.meta_off = nd * B / 8;
+        c.B = B; c.G = a.G; c.sr = a.sr != 0; c.intlog = a.intlog != 0; c.theta = a.theta;
+        c.lut = a.lut; c.err = a.err;
+        const int64_t grp = e0 / a.G;
+        const GroupMeta m = read_meta(P, grp, c);
+        uint32_t cf[32];
+        run_code_floats<B>(w, cf);
+        if (!c.intlog) {
+#pragma unroll
+          for (int k = 0; k < 32; k += 2) {
+            float c0, c1;
+            add2(c0, c1, __uint_as_float(cf[k]), __uint_as_float(cf[k + 1]), -8388608.0f, -8388608.0f);
+            fma2(v[k], v[k + 1], c0, c1, m.s32, m.s32, m.z32, m.z32);
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 32; ++k)
+            v[k] = __double2float_rn(__dadd_rn(__dmul_rn((double)(cf[k] & 0xFFu), m.s64), m.o64));
+        }
+        if (c.sr) {  // reserved values, imin then imax (codec.py:559-561)
+          const int base = (int)(e0 - grp * a.G);
+          const int ka = m.imin - base, kz = m.imax - base;
+          const bool ha = m.imin >= 0 && (unsigned)ka < 32u, hz = m.imax >= 0 && (unsigned)kz < 32u;
+          if (ha || hz) {
+#pragma unroll
+            for (int k = 0; k < 32; k += 4) *reinterpret_cast<float4*>(spill + k) = make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]);
+            if (ha) spill[ka] = m.smin;
+            if (hz) spill[kz] = m.smax;
+#pragma unroll
+            for (int k = 0; k < 32; k += 4) {
+              const float4 q = *reinterpret_cast<const float4*>(spill + k);
+              v[k] = q.x; v[k + 1] = q.y; v[k + 2] = q.z; v[k + 3] = q.w;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 32; k += 2) add2(acc[k], acc[k + 1], acc[k], acc[k + 1], v[k], v[k + 1]);
+    }
+    if (on) {
+#pragma unroll
+      for (int k = 0; k < 32; k += 8) store8_any(a.out, a.odt, t * a.H + h + k, acc + k);
+    }
+  }
+  if (bad) atomicOr(a.err, FC2_ERR_NONFINITE);
+}
+
 int grid_for(int64_t n8, int threads) {
   int64_t blocks = (n8 + threads - 1) / threads;
   const int64_t cap = (int64_t)num_sms() * 8;
@@ -256,6 +378,53 @@ int fc2_moe_combine_sum(int32_t world, const void* const* srcs, const int32_t* s
   const int64_t n8 = tokens * row_len / 8;
   k_moe_combine<<<grid_for(n8, 256), 256, 0, (cudaStream_t)stream>>>(a);
   return cuda_check("k_moe_combine");
+}
+
+int fc2_moe_combine_q(const fc2_config* cfg, int32_t world, int32_t me, const void* const* payloads,
+                      const int64_t* chunk_n, const void* exact, int32_t exact_dtype, const int32_t* pos,
+                      int64_t tokens, int64_t row_len, void* out, int32_t out_dtype, int32_t* dev_err, void* stream) {
+  int rc = fc2_check_config(cfg);
+  if (rc) return rc;
+  if (world < 1 || world > FC2_MOE_MAX_WORLD || me < 0 || me >= world)
+    return set_err(FC2_ECONFIG, "bad rank %d / world %d", me, world);
+  if (tokens <= 0) return FC2_OK;
+  if (cfg->group_size % 32 || row_len <= 0 || row_len % 32)
+    return set_err(FC2_ENOTAPPLICABLE, "fused combine needs group_size and row length multiples of 32");
+  const double* lut = lut_for_cfg(cfg, &rc);
+  if (rc) return rc;
+  if ((exact_dtype != FC2_BF16 && exact_dtype != FC2_F32) || (out_dtype != FC2_BF16 && out_dtype != FC2_F32))
+    return set_err(FC2_ECONFIG, "combine rows are bf16 / f32");
+  if ((reinterpret_cast<uintptr_t>(exact) | reinterpret_cast<uintptr_t>(out)) & 15u)
+    return set_err(FC2_ECONFIG, "combine buffers must be 16-byte aligned");
+  CombineQArgs a;
+  for (int d = 0; d < world; ++d) {
+    a.pay[d] = (const uint8_t*)payloads[d];
+    a.n[d] = chunk_n[d];
+    if (d != me && payloads[d] && (reinterpret_cast<uintptr_t>(payloads[d]) & 3u))
+      return set_err(FC2_ECONFIG, "payloads must be 4-byte aligned");
+  }
+  a.exact = exact;
+  a.edt = exact_dtype;
+  a.me = me; a.world = world;
+  a.B = cfg->bitwidth; a.G = cfg->group_size; a.sr = cfg->scheme; a.intlog = cfg->scale_encoding; a.theta = cfg->theta;
+  a.lut = lut;
+  a.pos = pos; a.T = tokens; a.H = row_len; a.out = out; a.odt = out_dtype; a.err = dev_err;
+  const int64_t tasks = tokens * ((row_len + 1023) / 1024);
+  int64_t blocks = (tasks + 7) / 8;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (cfg->bitwidth) {
+    case 2: k_moe_combine_q<2><<<(unsigned)blocks, 256, 0, st>>>(a); break;
+    case 3: k_moe_combine_q<3><<<(unsigned)blocks, 256, 0, st>>>(a); break;
+    case 4: k_moe_combine_q<4><<<(unsigned)blocks, 256, 0, st>>>(a); break;
+    case 5: k_moe_combine_q<5><<<(unsigned)blocks, 256, 0, st>>>(a); break;
+    case 6: k_moe_combine_q<6><<<(unsigned)blocks, 256, 0, st>>>(a); break;
+    case 7: k_moe_combine_q<7><<<(unsigned)blocks, 256, 0, st>>>(a); break;
+    default: k_moe_combine_q<8><<<(unsigned)blocks, 256, 0, st>>>(a); break;
+  }
+  return cuda_check("k_moe_combine_q");
 }
 
 }  // extern "C"

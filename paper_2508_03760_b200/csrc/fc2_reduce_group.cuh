@@ -248,37 +248,6 @@ __device__ __forceinline__ void encode_tile_f32(const uint8_t* ist, uint8_t* ost
   __syncwarp();
 }
 
-// 32 code values (as 2^23 + code float bits) of run r of the lane's group
-template <int B>
-__device__ __forceinline__ void run_code_floats(const uint32_t* w, uint32_t* cf) {
-  if constexpr (B == 4) {
-#pragma unroll
-    for (int wd = 0; wd < 4; ++wd) {
-      const uint32_t ev = w[wd] & 0x0F0F0F0Fu, od = (w[wd] >> 4) & 0x0F0F0F0Fu;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        cf[8 * wd + 2 * k] = __byte_perm(ev, 0x4B000000u, 0x7650 + k);
-        cf[8 * wd + 2 * k + 1] = __byte_perm(od, 0x4B000000u, 0x7650 + k);
-      }
-    }
-  } else if constexpr (B == 8) {
-#pragma unroll
-    for (int wd = 0; wd < 8; ++wd)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) cf[4 * wd + k] = __byte_perm(w[wd], 0x4B000000u, 0x7650 + k);
-  } else {
-#pragma unroll
-    for (int k = 0; k < 32; ++k) {
-      uint32_t c = 0;
-#pragma unroll
-      for (int u = 0; u < n_units(B); ++u) {
-        const int W = unit_w(B, u), O = unit_off(B, u);
-        c |= ((w[O + ((k * W) >> 5)] >> ((k * W) & 31)) & ((1u << W) - 1u)) << O;
-      }
-      cf[k] = 0x4B000000u | c;
-    }
-  }
-}
 
 
 // ===========================================================================

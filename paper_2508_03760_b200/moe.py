@@ -221,22 +221,40 @@ def moe_combine_q(expert_out, layout: MoeLayout, topo: Topology, config: QuantCo
                 slots[(e, s)] = total
                 total += _round_up(footprint_bytes(config, _round_up(k, G)), _ALIGN)
     pay = torch.empty(max(total, 1), dtype=torch.uint8, device=dev)
-    scratch = [torch.empty((int(counts[s].sum()), H), dtype=torch.float32, device=dev) for s in range(N)]
+    # fused combine (fc2_moe_combine_q) reads the packed blocks directly; other
+    # shapes decode every block to float32 first (fc2_moe_combine_sum)
+    fused = G % 32 == 0 and H % 32 == 0
+    scratch = [] if fused else [torch.empty((int(counts[s].sum()), H), dtype=torch.float32, device=dev)
+                                for s in range(N)]
     for (e, s), off in slots.items():
         k = int(counts[s, e])
         r0 = int(counts[:s, e].sum())
         enc.setdefault(_device.dtype_code(ys[e]), []).append(
             (ys[e][r0:r0 + k].data_ptr(), k * H, _round_up(k * H, G), pay.data_ptr() + off))
-        so = int(counts[s, :e].sum())
-        dec.append((pay.data_ptr() + off, _round_up(k * H, G), scratch[s][so:so + k].data_ptr(), k * H))
+        if not fused:
+            so = int(counts[s, :e].sum())
+            dec.append((pay.data_ptr() + off, _round_up(k * H, G), scratch[s][so:so + k].data_ptr(), k * H))
     for code, jobs in enc.items():
         _encode_jobs(config, code, jobs, err)
     if dec:
         _decode_jobs(config, _lib.F32, dec, err)
     outs = []
+    c = config.c_struct()
     for s in range(N):
         T = layout.tokens[s]
         out = torch.empty((T, H), dtype=torch.float32, device=dev)
+        if fused:
+            r0 = int(counts[:s, s].sum())
+            pays = [pay.data_ptr() + slots[(e, s)] if (e, s) in slots else pay.data_ptr() for e in range(N)]
+            ns = [_round_up(int(counts[s, e]) * H, G) for e in range(N)]
+            if T:
+                _lib.check(_lib.lib().fc2_moe_combine_q(
+                    ctypes.byref(c), N, s, _lib.ptr_array(pays), _lib.i64_array(ns),
+                    ys[s].data_ptr() + r0 * H * ys[s].element_size(), _device.dtype_code(ys[s]),
+                    layout.pos[s].data_ptr(), T, H, out.data_ptr(), _lib.F32, err.data_ptr(),
+                    _device.stream_handle()))
+            outs.append(out)
+            continue
         srcs, dts, chk = [], [], []
         for e in range(N):
             if e == s:
