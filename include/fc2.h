@@ -225,6 +225,19 @@ int fc2_allreduce_oneshot(fc2_comm* c, const fc2_config* cfg, const void* x, int
                           int32_t y_dtype, int64_t n, int64_t slot_bytes, int64_t region_off,
                           int32_t* dev_err, double timeout_s, void* stream);
 
+/* Pipelined two-step (the NVSwitch form of the reference's microchunked
+ * schedule, scheduling.py:119-156 over collectives.py:263-315): the shard is
+ * cut into `chunks` (<= 16) microchunks of whole groups and encode/scatter,
+ * reduce/requantize and gather/decode of successive microchunks overlap on
+ * three streams, synchronised per chunk by release/acquire flags in peer
+ * memory (no device-wide barrier).  Same result as fc2_allreduce_2step bit for
+ * bit.  region_off / region_bytes: 4 * world * chunks * chunk_bytes bytes of
+ * the symmetric buffer (two parity sets of landing + gather slots);
+ * chunk_bytes >= footprint of one microchunk, a multiple of 16. */
+int fc2_allreduce_2step_pipe(fc2_comm* c, const fc2_config* cfg, const void* x, int32_t x_dtype, void* y,
+                             int32_t y_dtype, int64_t n, int32_t chunks, int64_t chunk_bytes, int64_t region_off,
+                             int64_t region_bytes, int32_t* dev_err, double timeout_s, void* stream);
+
 /* Quantized All2All (dispatch, collectives.py:428-482; combine = transposed
  * matrix).  matrix: host int64[world*world] element counts.  Remote blocks are
  * encoded straight into the receiver's All2All region [region_off,

@@ -85,6 +85,8 @@ SIGNATURES = {
     "fc2_comm_buffer": (_P, [_P, _I32]),
     "fc2_comm_barrier": (_I32, [_P, _P, ctypes.c_double, _P]),
     "fc2_allreduce_2step": (_I32, [_P, _PCFG, _P, _I32, _P, _I32, _I64, _I64, _P, ctypes.c_double, _P]),
+    "fc2_allreduce_2step_pipe": (_I32, [_P, _PCFG, _P, _I32, _P, _I32, _I64, _I32, _I64, _I64, _I64, _P,
+                                        ctypes.c_double, _P]),
     "fc2_a2a_q": (_I32, [_P, _PCFG, _P, _I32, _PI64, _P, _I32, _I64, _I64, _P, ctypes.c_double, _P]),
     "fc2_copy_check": (_I32, [_P, _I32, _P, _I32, _I64, _P, _P]),
     "fc2_copy_bytes": (_I32, [_P, _P, _I64, _I32, _P]),

@@ -915,3 +915,12 @@ int fc2_int_to_scale(const double* si, int64_t n, int32_t theta, double* out, vo
 }
 
 }  // extern "C"
+
+namespace fc2 {
+// batched decode whose float32 output is snapped to the bf16 grid (the
+// AllReduce output, collectives.py:185-186, 313-314), for fc2_comm.cu
+int decode_batch_grid(const fc2_config* cfg, int32_t y_dtype, int32_t njobs, const void* const* payloads,
+                      const int64_t* n, void* const* ys, const int64_t* n_out, int32_t* dev_err, void* stream) {
+  return decode_batch_impl(cfg, y_dtype, njobs, payloads, n, ys, n_out, dev_err, stream, 1);
+}
+}  // namespace fc2

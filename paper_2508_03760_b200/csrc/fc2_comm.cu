@@ -3,8 +3,9 @@
 // Every rank owns one symmetric device buffer (cudaMalloc, exported with
 // cudaIpcGetMemHandle, opened by every peer).  Layout of each buffer:
 //
-//   [0, 4096)                      barrier flags: uint32 arrive[FC2_COMM_MAX];
-//                                  [1024, 3072): small all-gather area [parity][rank][16]
+//   [0, 16384)                     flag page: uint32 arrive[FC2_COMM_MAX] at 0;
+//                                  [1024, 3072): small all-gather area [parity][rank][16];
+//                                  [4096, 6144): pipelined two-step flags [stage][src][chunk]
 //   [4096, 4096 + N*slot)          landing slots  land[src]   (stage 1, my shard)
 //   [.., + N*slot)                 gather slots   gath[owner] (stage 2)
 //   [.., + a2a_bytes)              All2All receive region
@@ -32,12 +33,16 @@
 namespace fc2 {
 int set_err(int code, const char* fmt, ...);
 int cuda_check(const char* what);
+int decode_batch_grid(const fc2_config* cfg, int32_t y_dtype, int32_t njobs, const void* const* payloads,
+                      const int64_t* n, void* const* ys, const int64_t* n_out, int32_t* dev_err, void* stream);
 }  // namespace fc2
 
 using namespace fc2;
 
 #define FC2_COMM_MAX 16
-#define FC2_FLAG_BYTES 4096
+#define FC2_FLAG_BYTES 16384
+#define FC2_PIPE_FLAGS 4096   // flag page: pipelined two-step flags [stage][src][chunk]
+#define FC2_PIPE_MAXK 16
 
 struct fc2_comm {
   int rank, world, device;
@@ -48,6 +53,9 @@ struct fc2_comm {
   uint32_t epoch;
   uint32_t oneshot_calls;  // parity selects the one-shot landing buffer
   uint32_t ag_calls;       // parity selects the small all-gather area
+  uint32_t pipe_epoch;     // pipelined two-step: flag value of the current call (parity: buffer set)
+  cudaStream_t s_red, s_gat;  // pipelined two-step: reduce / gather-decode streams (lazy)
+  cudaEvent_t ev_start, ev_red, ev_gat;
 };
 
 namespace {
@@ -85,6 +93,39 @@ __global__ void k_barrier(const __grid_constant__ BarrierArgs a) {
       break;
     }
     __nanosleep(256);
+  }
+  __threadfence_system();
+}
+
+// Pipelined two-step flags.  Signal: thread p publishes "my chunk is in
+// place" into peer p's flag word (fence.sys first, so the payload stores of
+// the kernels before it on this stream are ordered before the flag).  Wait:
+// thread s spins until source s's flag reaches the call's epoch.
+struct FlagArgs {
+  uint32_t* words[FC2_COMM_MAX];  // signal: flag word in peer p; wait: my flag word for source s
+  int world;
+  uint32_t epoch;
+  int32_t* err;
+  long long timeout_cycles;
+};
+
+__global__ void k_flag_signal(const __grid_constant__ FlagArgs a) {
+  const int p = threadIdx.x;
+  if (p >= a.world) return;
+  __threadfence_system();
+  st_release_sys(a.words[p], a.epoch);
+}
+
+__global__ void k_flag_wait(const __grid_constant__ FlagArgs a) {
+  const int s = threadIdx.x;
+  if (s >= a.world) return;
+  const long long t0 = clock64();
+  while ((int32_t)(ld_acquire_sys(a.words[s]) - a.epoch) < 0) {
+    if (clock64() - t0 > a.timeout_cycles) {
+      atomicOr(a.err, FC2_ERR_TIMEOUT);
+      break;
+    }
+    __nanosleep(128);
   }
   __threadfence_system();
 }
@@ -166,6 +207,13 @@ int fc2_comm_open_peers(fc2_comm* c, const void* handles) {
 int fc2_comm_destroy(fc2_comm* c) {
   if (!c) return FC2_OK;
   cudaDeviceSynchronize();
+  if (c->s_red) {
+    cudaStreamDestroy(c->s_red);
+    cudaStreamDestroy(c->s_gat);
+    cudaEventDestroy(c->ev_start);
+    cudaEventDestroy(c->ev_red);
+    cudaEventDestroy(c->ev_gat);
+  }
   for (int p = 0; p < c->world; ++p)
     if (c->opened[p]) cudaIpcCloseMemHandle(c->peer[p]);
   cudaFree(c->local);
@@ -296,6 +344,133 @@ int fc2_allreduce_oneshot(fc2_comm* c, const fc2_config* cfg, const void* x, int
   std::vector<const void*> gs(N);
   for (int o = 0; o < N; ++o) gs[o] = result + (int64_t)o * slot_bytes;
   return fc2_gather_decode(cfg, N, gs.data(), S, y, y_dtype, n, dev_err, stream);
+}
+
+// Pipelined two-step (the NVSwitch form of the reference's
+// microchunked HierPP schedule, scheduling.py:119-156): the shard is cut into
+// K microchunks of whole groups (groups are independent, so the result is the
+// two-step's bit for bit) and the three stages run on three streams,
+// synchronised per chunk by release/acquire flags in peer memory instead of
+// two device-wide barriers:
+//   caller stream   encode chunk k of my N shards -> peers' land[r][k]; signal F1[r][k]
+//   s_red           wait F1[*][k]; reduce + requantize chunk k -> peers' gath[r][k]; signal F2[r][k]
+//   s_gat           wait F2[*][k]; decode chunk k of the N shards into y
+// so chunk k + 1's encode overlaps chunk k's reduce and chunk k - 1's decode.
+// Buffers are double-buffered by call parity (region_off: 2 sets of land +
+// gath slots, chunk_bytes each), which with the flag waits makes back-to-back
+// calls safe without a trailing barrier.
+int fc2_allreduce_2step_pipe(fc2_comm* c, const fc2_config* cfg, const void* x, int32_t x_dtype, void* y,
+                             int32_t y_dtype, int64_t n, int32_t chunks, int64_t chunk_bytes, int64_t region_off,
+                             int64_t region_bytes, int32_t* dev_err, double timeout_s, void* stream) {
+  const int N = c->world, r = c->rank;
+  int rc = fc2_check_config(cfg);
+  if (rc) return rc;
+  if (chunks < 1 || chunks > FC2_PIPE_MAXK) return set_err(FC2_ECONFIG, "chunks must be in [1, %d]", FC2_PIPE_MAXK);
+  const int64_t G = cfg->group_size;
+  const int64_t mult = (int64_t)N * G;
+  const int64_t padded = (n + mult - 1) / mult * mult;
+  const int64_t S = padded / N;
+  // microchunk length: whole groups, a multiple of 1024 elements (aligned planes)
+  int64_t q = 1024;
+  while (q % G) q += 1024;
+  int64_t Sk = (S + chunks - 1) / chunks;
+  Sk = (Sk + q - 1) / q * q;
+  const int K = S == 0 ? 0 : (int)((S + Sk - 1) / Sk);
+  int64_t F = 0;
+  rc = fc2_footprint(cfg, Sk, &F);
+  if (rc) return rc;
+  if (F > chunk_bytes || (chunk_bytes & 15)) return set_err(FC2_ECONFIG, "chunk slot too small for the microchunk");
+  const int64_t set_bytes = (int64_t)2 * N * chunks * chunk_bytes;  // land + gath of one parity
+  if (region_off < 0 || (region_off & 15) || 2 * set_bytes > region_bytes ||
+      region_off + region_bytes + FC2_FLAG_BYTES > c->bytes)
+    return set_err(FC2_ECONFIG, "communicator buffer too small for the pipelined region");
+  if (n == 0) return FC2_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!c->s_red) {
+    if (cudaStreamCreateWithFlags(&c->s_red, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->s_gat, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_red, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_gat, cudaEventDisableTiming) != cudaSuccess)
+      return set_err(FC2_ECUDA, "stream/event creation failed");
+  }
+  const uint32_t epoch = ++c->pipe_epoch;
+  const int par = (int)(epoch & 1u);
+  const int esz = x_dtype == FC2_BF16 ? 2 : (x_dtype == FC2_F32 ? 4 : 8);
+  const int ysz = y_dtype == FC2_BF16 ? 2 : (y_dtype == FC2_F32 ? 4 : 8);
+  auto base = [&](int peer) { return c->peer[peer] + FC2_FLAG_BYTES + region_off + (int64_t)par * set_bytes; };
+  auto land = [&](int peer, int src, int k) { return (void*)(base(peer) + ((int64_t)src * chunks + k) * chunk_bytes); };
+  auto gath = [&](int peer, int own, int k) {
+    return (void*)(base(peer) + ((int64_t)(N + own) * chunks + k) * chunk_bytes);
+  };
+  auto flag = [&](int peer, int stage, int src, int k) {
+    return reinterpret_cast<uint32_t*>(c->peer[peer] + FC2_PIPE_FLAGS) + (stage * FC2_COMM_MAX + src) * FC2_PIPE_MAXK + k;
+  };
+  const long long tmo = (long long)(timeout_s * 2.0e9);
+  auto signal = [&](int stage, int k, cudaStream_t s) {
+    FlagArgs a;
+    for (int p = 0; p < N; ++p) a.words[p] = flag(p, stage, r, k);
+    a.world = N; a.epoch = epoch; a.err = dev_err; a.timeout_cycles = tmo;
+    k_flag_signal<<<1, 32, 0, s>>>(a);
+    return cuda_check("k_flag_signal");
+  };
+  auto wait = [&](int stage, int k, cudaStream_t s) {
+    FlagArgs a;
+    for (int p = 0; p < N; ++p) a.words[p] = flag(r, stage, p, k);
+    a.world = N; a.epoch = epoch; a.err = dev_err; a.timeout_cycles = tmo;
+    k_flag_wait<<<1, 32, 0, s>>>(a);
+    return cuda_check("k_flag_wait");
+  };
+  // the side streams start where the caller's stream is now
+  cudaEventRecord(c->ev_start, st);
+  cudaStreamWaitEvent(c->s_red, c->ev_start, 0);
+  cudaStreamWaitEvent(c->s_gat, c->ev_start, 0);
+  for (int k = 0; k < K; ++k) {
+    const int64_t e0 = (int64_t)k * Sk, len = std::min<int64_t>(Sk, S - e0);
+    // 1. encode chunk k of my N shards into the owners' landing slots
+    std::vector<const void*> xs(N);
+    std::vector<int64_t> nv(N), ns(N);
+    std::vector<void*> outs(N);
+    for (int j = 0; j < N; ++j) {
+      const int64_t at = (int64_t)j * S + e0;
+      const int64_t valid = n - at;
+      nv[j] = valid < 0 ? 0 : (valid > len ? len : valid);
+      ns[j] = len;
+      xs[j] = nv[j] ? (const uint8_t*)x + at * esz : x;
+      outs[j] = land(j, r, k);
+    }
+    if ((rc = fc2_encode_batch(cfg, x_dtype, N, xs.data(), nv.data(), ns.data(), outs.data(), dev_err, st))) return rc;
+    if ((rc = signal(0, k, st))) return rc;
+    // 2. reduce chunk k of my shard once every source has landed it
+    if ((rc = wait(0, k, c->s_red))) return rc;
+    std::vector<const void*> srcs(N);
+    std::vector<void*> dsts(N);
+    for (int s2 = 0; s2 < N; ++s2) srcs[s2] = land(r, s2, k);
+    for (int p = 0; p < N; ++p) dsts[p] = gath(p, r, k);
+    if ((rc = fc2_reduce_requant(cfg, N, srcs.data(), len, N, dsts.data(), dev_err, c->s_red))) return rc;
+    if ((rc = signal(1, k, c->s_red))) return rc;
+    // 3. decode chunk k of every owner's shard
+    if ((rc = wait(1, k, c->s_gat))) return rc;
+    std::vector<const void*> gs(N);
+    std::vector<int64_t> gn(N), go(N);
+    std::vector<void*> ys(N);
+    for (int o = 0; o < N; ++o) {
+      const int64_t at = (int64_t)o * S + e0;
+      const int64_t rem = n - at;
+      gs[o] = gath(r, o, k);
+      gn[o] = len;
+      go[o] = rem < 0 ? 0 : (rem > len ? len : rem);
+      ys[o] = (uint8_t*)y + (go[o] ? at : 0) * ysz;
+    }
+    if ((rc = decode_batch_grid(cfg, y_dtype, N, gs.data(), gn.data(), ys.data(), go.data(), dev_err, c->s_gat)))
+      return rc;
+  }
+  // the caller's stream continues after both side streams
+  cudaEventRecord(c->ev_red, c->s_red);
+  cudaEventRecord(c->ev_gat, c->s_gat);
+  cudaStreamWaitEvent(st, c->ev_red, 0);
+  cudaStreamWaitEvent(st, c->ev_gat, 0);
+  return cuda_check("pipelined two-step");
 }
 
 }  // extern "C"

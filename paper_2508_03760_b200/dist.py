@@ -75,6 +75,15 @@ class TwoStepLayout:
         return max(0, min(self.shard_len, self.n - shard * self.shard_len))
 
 
+def pipe_chunk_len(shard_len: int, chunks: int, group_size: int) -> int:
+    """Microchunk length of the pipelined two-step (fc2_allreduce_2step_pipe):
+    ceil(S / chunks) rounded up to whole groups and a multiple of 1024."""
+    q = 1024
+    while q % group_size:
+        q += 1024
+    return _round_up(-(-shard_len // max(1, chunks)), q)
+
+
 def a2a_slot_offsets(matrix: np.ndarray, config: QuantConfig, dst: int) -> list[int]:
     """Byte offset of each source's packed block inside rank dst's receive
     region (same rule as fc2_a2a_q)."""
@@ -161,7 +170,7 @@ class QComm:
 
     def __init__(self, group=None, max_elems: int = 1 << 25, config: QuantConfig | None = None,
                  transport: str = "ipc", a2a_bytes: int = 0, timeout_s: float = 60.0,
-                 oneshot_max_elems: int = 1 << 18):
+                 oneshot_max_elems: int = 1 << 18, pipe_chunks: int = 4):
         self.device = _device.require_cuda()
         self.group = group
         self.rank = dist.get_rank(group)
@@ -175,6 +184,12 @@ class QComm:
         self.os_lay = TwoStepLayout.make(min(int(oneshot_max_elems), max_elems), self.world, self.cfg)
         self.a2a_bytes = _round_up(int(a2a_bytes), _SLOT_ALIGN)
         self.os_off = self.a2a_off + self.a2a_bytes
+        # pipelined two-step region: 2 parity sets x (land + gath) x N x chunks slots
+        self.pipe_chunks = max(1, min(16, int(pipe_chunks)))
+        sk = pipe_chunk_len(self.max_lay.shard_len, self.pipe_chunks, self.cfg.group_size)
+        self.pipe_chunk_bytes = _round_up(max(footprint_bytes(self.cfg, sk), 1), _SLOT_ALIGN)
+        self.pipe_bytes = 4 * self.world * self.pipe_chunks * self.pipe_chunk_bytes
+        self.pipe_off = self.os_off + (2 * self.world * self.world + self.world) * self.os_lay.slot_bytes
         self.codec = CudaCodec(self.cfg, self.device)
         self.err = self.codec.err
         self._c = None
@@ -186,7 +201,7 @@ class QComm:
             hb = lib.fc2_comm_handle_bytes()
             handle = (ctypes.c_uint8 * hb)()
             ptr = ctypes.c_void_p()
-            nbytes = self.os_off + (2 * self.world * self.world + self.world) * self.os_lay.slot_bytes
+            nbytes = self.pipe_off + self.pipe_bytes
             self._nbytes = nbytes
             _lib.check(lib.fc2_comm_create(self.rank, self.world, nbytes, ctypes.byref(ptr),
                                            ctypes.cast(handle, ctypes.c_void_p)))
@@ -234,8 +249,19 @@ class QComm:
             raise DataError(f"payload of {n} elements exceeds the communicator's {self.max_lay.n}")
         y = out if out is not None else torch.empty(n, dtype=x.dtype, device=x.device)
         lay = TwoStepLayout.make(n, self.world, cfg)
-        if algo not in ("auto", "two_step", "one_shot"):
+        if algo not in ("auto", "two_step", "one_shot", "pipelined"):
             raise ConfigError(f"unknown allreduce algorithm {algo!r}")
+        if algo == "pipelined":
+            if self.transport != "ipc":
+                raise ConfigError("the pipelined two-step needs the ipc transport")
+            c = cfg.c_struct()
+            _lib.check(_lib.lib().fc2_allreduce_2step_pipe(
+                self._c, ctypes.byref(c), x.data_ptr(), _device.dtype_code(x), y.data_ptr(),
+                _device.dtype_code(y), n, self.pipe_chunks, self.pipe_chunk_bytes, self.pipe_off, self.pipe_bytes,
+                self.err.data_ptr(), self.timeout_s, _device.stream_handle()))
+            if check:
+                self.check()
+            return y
         one = self.transport == "ipc" and n <= self.os_lay.n and algo != "two_step"
         if algo == "one_shot" and not one:
             raise ConfigError("one_shot needs the ipc transport and n <= oneshot_max_elems")

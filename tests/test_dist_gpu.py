@@ -40,12 +40,12 @@ def _worker(rank, world, port, case, q):
                              chunk_size=g)
         seeds = O.child_seeds(seed, world)
         if kind == "allreduce":
-            comm = QComm(max_elems=n, config=cfg, timeout_s=120.0, oneshot_max_elems=n)
+            comm = QComm(max_elems=n, config=cfg, timeout_s=120.0, oneshot_max_elems=n, pipe_chunks=3)
             x = torch.from_numpy(O.bf16_snap(O.spiky(n, seeds[rank])).astype(np.float32)).cuda()
             outs = []
             # both algorithms, both output types; the one-shot runs three times
             # so both landing buffers (call parity) are exercised
-            for algo in ("two_step", "one_shot", "one_shot", "one_shot"):
+            for algo in ("two_step", "one_shot", "one_shot", "one_shot", "pipelined", "pipelined", "pipelined"):
                 for dt in (torch.float32, torch.bfloat16):
                     y = comm.all_reduce(x.to(dt), check=True, algo=algo)
                     outs.append(y.float().cpu().numpy().tobytes())
@@ -125,7 +125,8 @@ def _run(world, case):
 
 @pytest.mark.parametrize("world,n,bits,g,sr", [(2, 100003, 4, 128, True), (4, 1 << 16, 3, 128, True),
                                                (2, 8192, 2, 32, False), (8, 1 << 18, 4, 128, True),
-                                               (8, 100003, 3, 32, True)])
+                                               (8, 100003, 3, 32, True), (2, 1 << 21, 4, 128, True),
+                                               (3, 50000, 4, 24, True)])
 def test_ipc_two_step_matches_reference_algorithm(world, n, bits, g, sr):
     got = _run(world, ("allreduce", n, bits, g, sr, 5))
     payloads = [O.bf16_snap(O.spiky(n, s)).astype(np.float32) for s in O.child_seeds(5, world)]
