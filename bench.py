@@ -742,10 +742,23 @@ def run_multi(args, rank, world, local_rank):
         ts_main = timed(lambda: comm.all_reduce(x, out=y), args.steps, args.warmup)
     launches = (lib.fc2_launch_count() - l0) // max(1, args.steps + args.warmup)
     ms = statistics.mean(ts_main)
-    comm.check()
+
+    def stage_ok(name):
+        # every stage's device error word is checked (and cleared) before the
+        # next one starts, so a failure names the stage that produced it
+        try:
+            comm.check()
+        except Exception as e:
+            raise RuntimeError(f"rank {rank}: stage {name!r} set a device error: {e}") from e
+
+    stage_ok("two_step b4")
     # same size at 3 bits (configs[2] names 4-bit and 3-bit)
     cfg3 = fc.QuantConfig(3, group_size=args.group, chunk_size=args.group, scheme=scheme)
     ts_b3 = timed(lambda: comm.all_reduce(x, out=y, config=cfg3), args.steps, args.warmup)
+    stage_ok("two_step b3")
+    # the pipelined two-step (row f3): microchunked stages on three streams
+    ts_pipe = timed(lambda: comm.all_reduce(x, out=y, algo="pipelined"), args.steps, args.warmup)
+    stage_ok("pipelined b4")
     comm.all_reduce(x, out=y)  # leave the 4-bit result in y for the parity check
     # ---- bf16 NCCL AllReduce on the same box (NVLS default, then forced off)
     ts_nccl = ts_nccl_nonvls = None
@@ -771,6 +784,10 @@ def run_multi(args, rank, world, local_rank):
     nvl = None
     probe = min(256 << 20, comm.buffer_bytes // 2 // 16 * 16)
     if probe >= (16 << 20):
+        # the probe overwrites the peers' slots: every rank must be done with
+        # the collective above (its gather-decode still reads them) first
+        torch.cuda.synchronize()
+        dist.barrier()
         src = torch.empty(probe, dtype=torch.uint8, device=dev)
         peer = (rank + 1) % world
         dst_ptr = comm.buffer_ptr(peer)
@@ -780,6 +797,7 @@ def run_multi(args, rank, world, local_rank):
         nvl = probe / (statistics.median(ts_nvl) * 1e-3) / 1e9
         del src
         dist.barrier()
+        stage_ok("nvlink probe")
     # ---- e2e: pinned host in -> H2D -> all_reduce -> D2H, every step
     xh = x.cpu().pin_memory()
     yh = torch.empty_like(xh).pin_memory()
@@ -792,6 +810,7 @@ def run_multi(args, rank, world, local_rank):
 
     ts_e2e = timed(e2e, max(3, args.steps), 2)
     comm.all_reduce(x, out=y)
+    stage_ok("e2e")
     # ---- parity of the headline result (rank 0 regenerates every rank's input)
     parity = None
     if rank == 0:
@@ -822,6 +841,7 @@ def run_multi(args, rank, world, local_rank):
             t = statistics.mean(timed(lambda: comm.all_reduce(xm, out=ym, config=cb), k, 3))
             row[f"b{bits}_us"] = round(t * 1e3, 2)
             row[f"b{bits}_algbw_GBps"] = round(nb / (t * 1e-3) / 1e9, 2)
+            stage_ok(f"sweep {nb} B b{bits}")
         if backend == "nccl":
             xc = xm.clone()
             t = statistics.mean(timed(lambda: dist.all_reduce(xc), k, 3))
@@ -835,6 +855,7 @@ def run_multi(args, rank, world, local_rank):
     # ---- configs[3]: MoE token dispatch + combine (4096 tok x 7168, top-8 of 256, EP = world)
     moe = fcd.bench_moe(comm, cfg, routing, args.moe_tokens, MOE["hidden"], timed,
                         args.steps, args.warmup, backend == "nccl") if not args.no_moe else None
+    stage_ok("moe")
     if rank == 0:
         F = fc.footprint_bytes(cfg, comm.shard_len if n == comm.max_lay.n else
                                fcd.TwoStepLayout.make(n, world, cfg).shard_len)
@@ -862,6 +883,9 @@ def run_multi(args, rank, world, local_rank):
             "config": config_for(args, world),
             "b3": {"ms": round(statistics.mean(ts_b3), 5),
                    "algbw_GBps": round(2 * n / (statistics.mean(ts_b3) * 1e-3) / 1e9, 2), **pct(ts_b3)},
+            "pipelined": {"ms": round(statistics.mean(ts_pipe), 5), "chunks": comm.pipe_chunks,
+                          "algbw_GBps": round(2 * n / (statistics.mean(ts_pipe) * 1e-3) / 1e9, 2),
+                          **pct(ts_pipe)},
             "nccl_bf16": None if ts_nccl is None else {
                 "ms": round(statistics.mean(ts_nccl), 5), **pct(ts_nccl),
                 "algbw_GBps": round(2 * n / (statistics.mean(ts_nccl) * 1e-3) / 1e9, 2),

@@ -188,6 +188,30 @@ __device__ __forceinline__ uint32_t pair_tie_bits(uint32_t X0, uint32_t X1, int 
   }
 }
 
+// FB = 16 tie flags with the work on the FMA pipe (the ALU pipe is the
+// encoder's bottleneck).  y + kTieShift moves the tie window frac(y) in
+// [0, 16] ulp to [0x7BF0, 0x7C00], which is exactly the set of 16-bit
+// patterns an ordered f16 compare h >= 64512 accepts (0x7C00 = +inf, NaNs and
+// negatives compare false) -- so one PRMT + one HSET2 test a pair, with no
+// masking; exact-integer codes (frac = 0x8008) land on negative f16 and are
+// not flagged.  The 1.0 / 0.0 results are summed as r * 2^k into an f16 pair
+// that starts at 1024 (HFMA2): pair k of 8 sets bit k of the low byte of each
+// half (1024 + v, v < 256, is exact).  tie_bits16 merges the two
+// accumulators of a run into the split layout of pair_tie_bits.
+constexpr float kTieShift = 31728.0f / 65536.0f;  // 0x7BF0 ulp of 2^-16
+__device__ __forceinline__ void add2(float& r0, float& r1, float a0, float a1, float b0, float b1);
+__device__ __forceinline__ void tie_acc16(__half2& acc, float y0, float y1, int k) {
+  float z0, z1;  // exact: y in [128, 256) on the 2^-16 grid, y + shift < 256
+  add2(z0, z1, y0, y1, kTieShift, kTieShift);
+  const uint32_t h = __byte_perm(__float_as_uint(z0), __float_as_uint(z1), 0x5410);
+  const __half2 r = __hge2(*reinterpret_cast<const __half2*>(&h), __half2(__ushort_as_half(0x7BF0), __ushort_as_half(0x7BF0)));
+  acc = __hfma2(r, __float2half2_rn((float)(1 << k)), acc);
+}
+__device__ __forceinline__ uint32_t tie_bits16(const __half2 (&acc)[2]) {
+  return __byte_perm(*reinterpret_cast<const uint32_t*>(&acc[0]), *reinterpret_cast<const uint32_t*>(&acc[1]),
+                     0x6240);
+}
+
 // packed float32x2 arithmetic (sm_100: FFMA2 / FADD2)
 __device__ __forceinline__ void fma2(float& r0, float& r1, float a0, float a1, float b0, float b1, float c0,
                                      float c1) {

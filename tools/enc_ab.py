@@ -17,7 +17,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 import paper_2508_03760_b200 as fc  # noqa: E402
-from bench import spiky_bf16  # noqa: E402
+from bench import flush_l2, spiky_bf16  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--reps", type=int, default=30)
@@ -40,7 +40,7 @@ for mib in [int(v) for v in a.sizes.split(",")]:
         pay = torch.empty(F, dtype=torch.uint8, device=dev)
         ts = []
         for i in range(a.reps + 3):
-            flush.zero_()
+            flush_l2(flush)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             fc.encode_payload(x, cfg, n, out=pay, err=err, check=False)
