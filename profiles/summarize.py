@@ -83,7 +83,7 @@ def launches(path, out):
         if len(r) <= vi or r[mi] != "gpu__time_duration.sum":
             continue
         v = float(r[vi].replace(",", ""))
-        v = v / 1000.0 if r[ui] == "nsecond" else (v * 1000.0 if r[ui] == "msecond" else v)
+        v = v / 1000.0 if r[ui] in ("nsecond", "ns") else (v * 1000.0 if r[ui] in ("msecond", "ms") else v)
         name = re.sub(r"\(.*", "", r[ki])[:90]
         a = agg.setdefault(name, [0, 0.0])
         a[0] += 1

@@ -1,4 +1,5 @@
-"""One 64 MiB bf16 encode + decode (b4 SR g128 by default) for ncu captures (dev tool)."""
+"""One bf16 encode + decode (b4 SR g128 by default) for ncu captures (dev tool).
+KIB (default 65536 = 64 MiB), BITS, SCHEME."""
 import os
 import sys
 
@@ -10,9 +11,9 @@ from bench import spiky_bf16  # noqa: E402
 
 bits = int(os.environ.get("BITS", "4"))
 sr = os.environ.get("SCHEME", "sr") == "sr"
-mib = int(os.environ.get("MIB", "64"))
+kib = int(os.environ.get("KIB", str(64 * 1024)))
 dev = torch.device("cuda", 0)
-n = mib * (1 << 20) // 2
+n = kib * 1024 // 2
 x = spiky_bf16(n, 0, dev)
 cfg = fc.QuantConfig(bits, group_size=128, chunk_size=128,
                      scheme=fc.Scheme.SPIKE_RESERVING if sr else fc.Scheme.RTN)
