@@ -135,6 +135,44 @@ __device__ __forceinline__ void dq_run32(const uint8_t* payload, int64_t n, int6
   }
 }
 
+// Codes of elements 8q .. 8q+7 of a 32-element run, from its bit-split plane
+// words (unit-major, unit u at w[O .. O + W)), as bytes: byte i of E = code of
+// element 8q + 2i, byte i of Od = code of element 8q + 2i + 1.
+//   W = 4: the nibble word q, even / odd nibbles masked out;
+//   W = 2: the 16 bits of the 8 elements spread to one 2-bit field per nibble
+//          (PRMT, then two shift-or-mask steps), even / odd nibbles masked out;
+//   W = 1: byte q of the word; its even (odd) bits land on bit 0 (1) of bytes
+//          0..3 with one multiply by 1 + 2^6 + 2^12 + 2^18 (the partial
+//          products collide only on positions no target bit reads).
+// Unit u's bits are then added at bit offset O (no overlap, so + is |).
+template <int B>
+__device__ __forceinline__ void split_codes8(const uint32_t* w, int q, uint32_t& E, uint32_t& Od) {
+  E = 0u;
+  Od = 0u;
+#pragma unroll
+  for (int u = 0; u < n_units(B); ++u) {
+    const int W = unit_w(B, u), O = unit_off(B, u);
+    uint32_t ev, od;
+    if (W == 4) {
+      const uint32_t x = w[O + q];
+      ev = x & 0x0F0F0F0Fu;
+      od = (x >> 4) & 0x0F0F0F0Fu;
+    } else if (W == 2) {
+      uint32_t x = __byte_perm(w[O + (q >> 1)], 0u, (q & 1) ? 0x4342 : 0x4140);  // [0, t_hi, 0, t_lo]
+      x = (x | (x << 4)) & 0x0F0F0F0Fu;  // two elements per byte
+      x = (x | (x << 2)) & 0x33333333u;  // one element per nibble
+      ev = x & 0x03030303u;
+      od = (x >> 4) & 0x03030303u;
+    } else {  // W == 1
+      const uint32_t t = __byte_perm(w[O], 0u, 0x4440 | q);
+      ev = ((t & 0x55u) * 0x41041u) & 0x01010101u;
+      od = (((t & 0xAAu) * 0x41041u) & 0x02020202u) >> 1;
+    }
+    E += ev << O;
+    Od += od << O;
+  }
+}
+
 // 32 code values (as 2^23 + code float bits) of one 32-element run from its plane words
 // (unit-major: w[O .. O + W) are unit u's words)
 template <int B>
@@ -155,15 +193,18 @@ __device__ __forceinline__ void run_code_floats(const uint32_t* w, uint32_t* cf)
 #pragma unroll
       for (int k = 0; k < 4; ++k) cf[4 * wd + k] = __byte_perm(w[wd], 0x4B000000u, 0x7650 + k);
   } else {
+    // bit-split widths: per 8 elements, rebuild the even and odd elements'
+    // codes as bytes (SWAR, no per-element bit extraction), then one PRMT per
+    // element as for B = 4
 #pragma unroll
-    for (int k = 0; k < 32; ++k) {
-      uint32_t c = 0;
+    for (int q = 0; q < 4; ++q) {
+      uint32_t E, Od;
+      split_codes8<B>(w, q, E, Od);
 #pragma unroll
-      for (int u = 0; u < n_units(B); ++u) {
-        const int W = unit_w(B, u), O = unit_off(B, u);
-        c |= ((w[O + ((k * W) >> 5)] >> ((k * W) & 31)) & ((1u << W) - 1u)) << O;
+      for (int k = 0; k < 4; ++k) {
+        cf[8 * q + 2 * k] = __byte_perm(E, 0x4B000000u, 0x7650 + k);
+        cf[8 * q + 2 * k + 1] = __byte_perm(Od, 0x4B000000u, 0x7650 + k);
       }
-      cf[k] = 0x4B000000u | c;
     }
   }
 }

@@ -445,18 +445,6 @@ struct RunRegs {
   uint32_t r[3];   // metadata record
 };
 
-
-template <int B>
-__device__ __forceinline__ uint32_t code_of(const RunRegs<B>& rr, int k) {
-  uint32_t c = 0;
-#pragma unroll
-  for (int u = 0; u < n_units(B); ++u) {
-    const int W = unit_w(B, u), O = unit_off(B, u);
-    c |= ((rr.w[O + ((k * W) >> 5)] >> ((k * W) & 31)) & ((1u << W) - 1u)) << O;
-  }
-  return c;
-}
-
 // Decode v4: warp tile = 4096 elements, lane = 128 consecutive elements
 // (4 runs of 32).  The tile's code planes are cp.async-staged (2 stages,
 // XOR-swizzled per-lane words); the lane's metadata record(s) come straight
@@ -664,25 +652,7 @@ __global__ void __launch_bounds__(kDecWarps * 32) k_decode_fast(const __grid_con
         }
         // ---- codes -> exact floats (2^23 + code, as bit patterns)
         uint32_t cf[32];
-        if constexpr (B == 4) {  // nibbles: PRMT byte k of (w & 0x0F..) into 0x4B0000cc
-#pragma unroll
-          for (int wd = 0; wd < 4; ++wd) {
-            const uint32_t ev = rr.w[wd] & 0x0F0F0F0Fu, od = (rr.w[wd] >> 4) & 0x0F0F0F0Fu;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              cf[8 * wd + 2 * k] = __byte_perm(ev, 0x4B000000u, 0x7650 + k);
-              cf[8 * wd + 2 * k + 1] = __byte_perm(od, 0x4B000000u, 0x7650 + k);
-            }
-          }
-        } else if constexpr (B == 8) {
-#pragma unroll
-          for (int wd = 0; wd < 8; ++wd)
-#pragma unroll
-            for (int k = 0; k < 4; ++k) cf[4 * wd + k] = __byte_perm(rr.w[wd], 0x4B000000u, 0x7650 + k);
-        } else {
-#pragma unroll
-          for (int k = 0; k < 32; ++k) cf[k] = 0x4B000000u | code_of<B>(rr, k);
-        }
+        run_code_floats<B>(rr.w, cf);
         // ---- values
         float v[32];
         if (!b.intlog) {
