@@ -207,6 +207,18 @@ __device__ __forceinline__ void tie_acc16(__half2& acc, float y0, float y1, int 
   const __half2 r = __hge2(*reinterpret_cast<const __half2*>(&h), __half2(__ushort_as_half(0x7BF0), __ushort_as_half(0x7BF0)));
   acc = __hfma2(r, __float2half2_rn((float)(1 << k)), acc);
 }
+// FB = 15 (B = 8): bit 15 of the low half is the code's LSB, so the same
+// window is tested on |h| (the f16 abs ignores bit 15); y + shift carries into
+// the code bits harmlessly (y < 511.5 + 8u, the sum stays below 512, exact).
+constexpr float kTieShift15 = 31728.0f / 32768.0f;  // 0x7BF0 ulp of 2^-15
+__device__ __forceinline__ void tie_acc15(__half2& acc, float y0, float y1, int k) {
+  float z0, z1;
+  add2(z0, z1, y0, y1, kTieShift15, kTieShift15);
+  const uint32_t h = __byte_perm(__float_as_uint(z0), __float_as_uint(z1), 0x5410);
+  const __half2 r = __hge2(__habs2(*reinterpret_cast<const __half2*>(&h)),
+                           __half2(__ushort_as_half(0x7BF0), __ushort_as_half(0x7BF0)));
+  acc = __hfma2(r, __float2half2_rn((float)(1 << k)), acc);
+}
 __device__ __forceinline__ uint32_t tie_bits16(const __half2 (&acc)[2]) {
   return __byte_perm(*reinterpret_cast<const uint32_t*>(&acc[0]), *reinterpret_cast<const uint32_t*>(&acc[1]),
                      0x6240);

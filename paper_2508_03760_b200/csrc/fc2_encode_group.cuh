@@ -281,13 +281,11 @@ __device__ __forceinline__ void quant_runs(const uint8_t* ist, uint32_t* tms, co
     const uint8_t* rb = la.run(r);
     LaneWords<B> lw;
     lw.clear();
-    uint32_t tmj[2] = {0u, 0u};  // two accumulators: shorter dependency chains
-    // FB = 16: tie flags gathered as f16 sums on the FMA pipe (tie_acc16)
+    // tie flags gathered as f16 sums on the FMA pipe (tie_acc16 / tie_acc15)
     __half2 tacc[2] = {__float2half2_rn(1024.f), __float2half2_rn(1024.f)};
     uint32_t XR[32];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      uint32_t& tm = tmj[j & 1];
       const uint4 q = *reinterpret_cast<const uint4*>(rb + la.jx(j));
       const uint32_t ww[4] = {q.x, q.y, q.z, q.w};
       uint32_t X[8];
@@ -315,7 +313,7 @@ __device__ __forceinline__ void quant_runs(const uint8_t* ist, uint32_t* tms, co
         X[2 * pp] = __float_as_uint(y0);
         X[2 * pp + 1] = __float_as_uint(y1);
         if constexpr (FB == 16) tie_acc16(tacc[j >> 1], y0, y1, 4 * (j & 1) + pp);
-        else tm |= pair_tie_bits<FB>(X[2 * pp], X[2 * pp + 1], 4 * j + pp);
+        else tie_acc15(tacc[j >> 1], y0, y1, 4 * (j & 1) + pp);
       }
       if constexpr (FB == 16) {
 #pragma unroll
@@ -332,8 +330,7 @@ __device__ __forceinline__ void quant_runs(const uint8_t* ist, uint32_t* tms, co
     for (int i = 0; i < B; ++i) pw[q][i] = lw.w[i];
     // near-tie masks of this run, resolved after all runs (one divergent
     // pass per tile instead of one per run)
-    if constexpr (FB == 16) tms[32 * rr + (int)lane_id()] = tie_bits16(tacc);
-    else tms[32 * rr + (int)lane_id()] = tmj[0] | tmj[1];
+    tms[32 * rr + (int)lane_id()] = tie_bits16(tacc);
   }
   if (active) {  // the pair's bytes of every unit: [4W (r0 + rp), +4W PAIR) of the group
 #pragma unroll
