@@ -33,6 +33,41 @@ inline void smem_attr(int bytes) {
   }
 }
 
+// Programmatic dependent launch for the codec kernels: launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, a kernel's CTAs may be
+// scheduled while its stream predecessor is still draining its last wave;
+// each CTA first lets its own dependents go (launch_dependents) and then waits
+// for the predecessor's completion and memory flush (griddepcontrol.wait)
+// before touching global memory, so stream semantics are unchanged and only
+// the launch latency / ramp overlaps the predecessor's tail.
+#ifndef FC2_PDL
+#define FC2_PDL 1
+#endif
+__device__ __forceinline__ void pdl_enter() {
+#if FC2_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+template <typename K, typename... Args>
+inline void launch_pdl(K kern, unsigned grid, unsigned block, int smem, cudaStream_t st, Args... args) {
+#if FC2_PDL
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, args...);
+#else
+  kern<<<grid, block, smem, st>>>(args...);
+#endif
+}
+
 // ---------------------------------------------------------------------------
 // job tables (passed by value as __grid_constant__ kernel parameters)
 // ---------------------------------------------------------------------------
@@ -325,6 +360,7 @@ __device__ __forceinline__ void encode_grp_tile(const EncBatch& b, int64_t t, ui
 
 template <int B, bool SR, int G, int WARPS, int LPG>
 __global__ void __launch_bounds__(WARPS * 32, enc_min_ctas(B, WARPS)) k_encode_grp(const __grid_constant__ EncBatch b) {
+  pdl_enter();
   using IT = GTile<__nv_bfloat16, G, LPG>;
   constexpr int IN_BYTES = IT::IN_BYTES / LPG;
   constexpr int TIE_BYTES = G / LPG * 4;               // one 32-bit tie mask per run per lane
@@ -365,7 +401,7 @@ struct EncGrp {
     int64_t cap = (int64_t)num_sms() * FC2_ENC_CTAS_PER_SM;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
-    kern<<<(unsigned)blocks, WARPS * 32, SMEM, st>>>(b);
+    launch_pdl(kern, (unsigned)blocks, WARPS * 32, SMEM, st, b);
     return cuda_check("k_encode_grp");
   }
 };
@@ -481,6 +517,7 @@ struct DecIn {
 
 template <typename OT, int B>
 __global__ void __launch_bounds__(kDecWarps * 32) k_decode_fast(const __grid_constant__ DecBatch b) {
+  pdl_enter();
   constexpr int ESZ = (int)sizeof(OT);
   constexpr int OUT_BYTES = kDecTile / 2 * ESZ;  // half a tile: runs (0,1) then (2,3) of every lane
   constexpr int PER_WARP = kDecStages * DecIn<B>::BYTES + OUT_BYTES;
@@ -746,7 +783,7 @@ int launch_decode_fast(const DecBatch& b, cudaStream_t st) {
   const int64_t cap = (int64_t)num_sms() * 64;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  kern<<<(unsigned)blocks, kDecWarps * 32, SMEM, st>>>(b);
+  launch_pdl(kern, (unsigned)blocks, kDecWarps * 32, SMEM, st, b);
   return cuda_check("k_decode_fast");
 }
 
