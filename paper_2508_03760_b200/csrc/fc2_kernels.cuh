@@ -33,41 +33,6 @@ inline void smem_attr(int bytes) {
   }
 }
 
-// Programmatic dependent launch for the codec kernels: launched with
-// cudaLaunchAttributeProgrammaticStreamSerialization, a kernel's CTAs may be
-// scheduled while its stream predecessor is still draining its last wave;
-// each CTA first lets its own dependents go (launch_dependents) and then waits
-// for the predecessor's completion and memory flush (griddepcontrol.wait)
-// before touching global memory, so stream semantics are unchanged and only
-// the launch latency / ramp overlaps the predecessor's tail.
-#ifndef FC2_PDL
-#define FC2_PDL 1
-#endif
-__device__ __forceinline__ void pdl_enter() {
-#if FC2_PDL
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-#endif
-}
-template <typename K, typename... Args>
-inline void launch_pdl(K kern, unsigned grid, unsigned block, int smem, cudaStream_t st, Args... args) {
-#if FC2_PDL
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(block);
-  cfg.dynamicSmemBytes = (size_t)smem;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kern, args...);
-#else
-  kern<<<grid, block, smem, st>>>(args...);
-#endif
-}
-
 // ---------------------------------------------------------------------------
 // job tables (passed by value as __grid_constant__ kernel parameters)
 // ---------------------------------------------------------------------------

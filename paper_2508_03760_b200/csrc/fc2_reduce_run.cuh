@@ -56,6 +56,7 @@ struct RunTile {
 
 template <int B, bool SR, int G>
 __global__ void __launch_bounds__(32, FC2_RUN_MINB) k_reduce_run(const __grid_constant__ ReduceArgs a) {
+  pdl_enter();
   using RT = RunTile<B, SR, G>;
   constexpr int LPG = G / 32;  // lanes per group
   constexpr int NST = FC2_RUN_STAGES;
@@ -333,7 +334,7 @@ struct RedRun {
       blocks = (a.total + per - 1) / per;
     }
     if (blocks < 1) blocks = 1;
-    kern<<<(unsigned)blocks, 32, SMEM, st>>>(a);
+    launch_pdl(kern, (unsigned)blocks, 32, SMEM, st, a);
     return cuda_check("k_reduce_run");
   }
 };
