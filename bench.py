@@ -404,6 +404,32 @@ def two_step_stage_times(fc, x, cfg, flush, steps, N=8):
         t = statistics.mean(ts)
         out[name] = {"us": round(t * 1e3, 2), "bytes": nbytes, "GBps": round(nbytes / (t * 1e-3) / 1e9, 1)}
     out["sum_us"] = round(sum(v["us"] for v in out.values()), 2)
+    # the three stages back to back in one stream (region-timed, inputs rotating
+    # over 3 tensors): the per-rank kernel chain of the N = 8 two-step without
+    # the two barriers and the NVLink transfers
+    xr = [x] + [spiky_bf16(n, 500 + k, x.device) for k in range(1, ROTATE)]
+    jobs = [[(t.data_ptr() + s * S * 2, S, S, land.data_ptr() + s * slot) for s in range(N)] for t in xr]
+
+    def chain(i):
+        _encode_jobs(cfg, 0, jobs[i % ROTATE], err)
+        red()
+        gat()
+
+    for i in range(3):
+        chain(i)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda._sleep(int(steps * 150e-6 * 2.0e9))
+    a.record()
+    for i in range(steps):
+        chain(i)
+    b.record()
+    torch.cuda.synchronize()
+    out["chain_region_us"] = round(a.elapsed_time(b) / steps * 1e3, 2)
+    out["chain_note"] = ("encode 8 shards -> reduce+requant 1 shard -> gather-decode 8 shards, back to back in one "
+                         "stream (PDL launches), one CUDA-event region over the steps; the N = 8 two-step adds two "
+                         "device barriers and the NVLink stores")
+    del xr
     return out
 
 
