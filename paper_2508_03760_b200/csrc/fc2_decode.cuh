@@ -30,11 +30,9 @@ struct GroupMeta {
   int imin, imax;       // reserved indices (validated, else -1)
 };
 
-__device__ __forceinline__ GroupMeta read_meta(const uint8_t* payload, int64_t grp, const DecCtx& c) {
+// the group's metadata from its raw record words (load_record)
+__device__ __forceinline__ GroupMeta meta_from_record(const uint32_t (&r)[3], const DecCtx& c) {
   GroupMeta m;
-  const int rb = rec_bytes(c.sr, c.intlog);
-  uint32_t r[3] = {0, 0, 0};
-  load_record(payload + c.meta_off + grp * rb, r, rb);
   m.imin = m.imax = -1;
   m.smin = m.smax = 0.f;
   if (!c.intlog) {
@@ -64,6 +62,12 @@ __device__ __forceinline__ GroupMeta read_meta(const uint8_t* payload, int64_t g
     }
   }
   return m;
+}
+
+__device__ __forceinline__ GroupMeta read_meta(const uint8_t* payload, int64_t grp, const DecCtx& c) {
+  uint32_t r[3] = {0, 0, 0};
+  load_record(payload + c.meta_off + grp * rec_bytes(c.sr, c.intlog), r, rec_bytes(c.sr, c.intlog));
+  return meta_from_record(r, c);
 }
 
 __device__ __forceinline__ float code_f32(uint32_t c) {  // exact int -> float

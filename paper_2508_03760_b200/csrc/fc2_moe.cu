@@ -130,9 +130,13 @@ __device__ __forceinline__ void load8_any(const void* p, int dt, int64_t i, floa
 
 __device__ __forceinline__ void store8_any(void* p, int dt, int64_t i, const float* v) {
   if (dt == FC2_BF16) {
+    // RNE, as bf16_bits for every finite value (the sums here are finite or flagged)
     uint32_t w[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) w[k] = bf16_bits(v[2 * k]) | (bf16_bits(v[2 * k + 1]) << 16);
+    for (int k = 0; k < 4; ++k) {
+      const __nv_bfloat162 h2 = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
+      w[k] = *reinterpret_cast<const uint32_t*>(&h2);
+    }
     *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(p) + i) = make_uint4(w[0], w[1], w[2], w[3]);
   } else {
     float* q = reinterpret_cast<float*>(p) + i;
@@ -205,12 +209,45 @@ struct CombineQArgs {
   const void* exact;                      // my own block's rows (d == me), dtype edt
   int edt;
   int me, world, B, G, sr, intlog, theta;
+  int gshift;                             // log2(G) when G is a power of two, else -1
   const double* lut;
   const int32_t* pos;                     // [T][world]
   int64_t T, H;
   void* out;
   int odt;
   int32_t* err;
+};
+
+// the lane's 32-element run of a packed block: plane words (unit-major) with
+// vector loads -- slots are 16-byte aligned and chunk lengths multiples of 32,
+// so unit u's 4W bytes are 4W-aligned
+template <int B>
+__device__ __forceinline__ void load_run_words(const uint8_t* P, int64_t nd, int64_t e0, uint32_t (&w)[B]) {
+#pragma unroll
+  for (int u = 0; u < n_units(B); ++u) {
+    const int W = unit_w(B, u), O = unit_off(B, u);
+    const uint8_t* q = P + nd * O / 8 + e0 * W / 8;
+    if (W == 8) {
+      const uint4 q0 = __ldg(reinterpret_cast<const uint4*>(q)), q1 = __ldg(reinterpret_cast<const uint4*>(q + 16));
+      w[O] = q0.x; w[O + 1] = q0.y; w[O + 2] = q0.z; w[O + 3] = q0.w;
+      w[O + 4] = q1.x; w[O + 5] = q1.y; w[O + 6] = q1.z; w[O + 7] = q1.w;
+    } else if (W == 4) {
+      const uint4 q0 = __ldg(reinterpret_cast<const uint4*>(q));
+      w[O] = q0.x; w[O + 1] = q0.y; w[O + 2] = q0.z; w[O + 3] = q0.w;
+    } else if (W == 2) {
+      const uint2 q0 = __ldg(reinterpret_cast<const uint2*>(q));
+      w[O] = q0.x; w[O + 1] = q0.y;
+    } else {
+      w[O] = __ldg(reinterpret_cast<const uint32_t*>(q));
+    }
+  }
+}
+
+// operands of one source rank's run, loaded one source ahead of their use
+template <int B>
+struct CombineSrc {
+  uint32_t w[B];    // plane words (packed block)
+  uint32_t rec[3];  // the group's record (my own block's row is read at use)
 };
 
 template <int B>
@@ -221,58 +258,64 @@ __global__ void __launch_bounds__(256, 2) k_moe_combine_q(const __grid_constant_
   const int64_t segs = (a.H + 1023) / 1024;
   const int64_t tasks = a.T * segs;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int rb = rec_bytes(a.sr != 0, a.intlog != 0);
   bool bad = false;
   for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; w < tasks; w += nw) {
     const int64_t t = w / segs;
     const int64_t h = (w - t * segs) * 1024 + 32 * lane;
     const bool on = h < a.H;
+    // the token's row index in every source block: one load per lane, then shuffles
+    const int mypos = lane < a.world ? __ldg(a.pos + t * a.world + lane) : -1;
+    uint32_t todo = __ballot_sync(0xffffffffu, mypos >= 0);  // source ranks in order
     float acc[32];
 #pragma unroll
     for (int k = 0; k < 32; ++k) acc[k] = 0.0f;  // fp32 from +0.0, source ranks in order
-    for (int d = 0; d < a.world; ++d) {
-      const int p = __ldg(a.pos + t * a.world + d);
-      if (p < 0 || !on) continue;
-      const int64_t e0 = (int64_t)p * a.H + h;  // element of block d
+    auto load = [&](int d, int64_t e0, CombineSrc<B>& o) {
+      if (!on) return;
+      if (d != a.me) {
+        load_run_words<B>(a.pay[d], a.n[d], e0, o.w);
+        const int64_t grp = a.gshift >= 0 ? e0 >> a.gshift : e0 / a.G;  // no 64-bit division per run
+        load_record(a.pay[d] + a.n[d] * B / 8 + grp * rb, o.rec, rb);
+      }
+    };
+    CombineSrc<B> cur, nxt;
+    int dc = -1;
+    int64_t ec = 0;
+    if (todo) {
+      dc = __ffs(todo) - 1;
+      todo &= todo - 1;
+      ec = (int64_t)__shfl_sync(0xffffffffu, mypos, dc) * a.H + h;
+      load(dc, ec, cur);
+    }
+    while (dc >= 0) {  // warp-uniform
+      int dn = -1;
+      int64_t en = 0;
+      if (todo) {  // next source's loads go out before this one is decoded
+        dn = __ffs(todo) - 1;
+        todo &= todo - 1;
+        en = (int64_t)__shfl_sync(0xffffffffu, mypos, dn) * a.H + h;
+        load(dn, en, nxt);
+      }
       float v[32];
-      if (d == a.me) {
+      if (dc == a.me) {
+        if (on) {
 #pragma unroll
-        for (int k = 0; k < 32; k += 8) load8_any(a.exact, a.edt, e0 + k, v + k);
+          for (int k = 0; k < 32; k += 8) load8_any(a.exact, a.edt, ec + k, v + k);
 #pragma unroll
-        for (int k = 0; k < 32; ++k) bad |= !isfinite(v[k]);
-      } else {
-        // the run's plane words (unit-major), vector loads: slots are 16-byte
-        // aligned and chunk lengths multiples of 32, so unit u's 4W bytes are
-        // 4W-aligned
-        const uint8_t* P = a.pay[d];
-        const int64_t nd = a.n[d];
-        uint32_t w[B];
+          for (int k = 0; k < 32; ++k) bad |= !isfinite(v[k]);
+        } else {
 #pragma unroll
-        for (int u = 0; u < n_units(B); ++u) {
-          const int W = unit_w(B, u), O = unit_off(B, u);
-          const uint8_t* q = P + nd * O / 8 + e0 * W / 8;
-          if (W == 8) {
-            const uint4 q0 = __ldg(reinterpret_cast<const uint4*>(q)), q1 = __ldg(reinterpret_cast<const uint4*>(q + 16));
-            w[O] = q0.x; w[O + 1] = q0.y; w[O + 2] = q0.z; w[O + 3] = q0.w;
-            w[O + 4] = q1.x; w[O + 5] = q1.y; w[O + 6] = q1.z; w[O + 7] = q1.w;
-          } else if (W == 4) {
-            const uint4 q0 = __ldg(reinterpret_cast<const uint4*>(q));
-            w[O] = q0.x; w[O + 1] = q0.y; w[O + 2] = q0.z; w[O + 3] = q0.w;
-          } else if (W == 2) {
-            const uint2 q0 = __ldg(reinterpret_cast<const uint2*>(q));
-            w[O] = q0.x; w[O + 1] = q0.y;
-          } else {
-            w[O] = __ldg(reinterpret_cast<const uint32_t*>(q));
-          }
+          for (int k = 0; k < 32; ++k) v[k] = 0.f;
         }
+      } else {
         DecCtx c;
-        c.n = nd;
-        c.meta_off = nd * B / 8;
+        c.n = a.n[dc];
+        c.meta_off = a.n[dc] * B / 8;
         c.B = B; c.G = a.G; c.sr = a.sr != 0; c.intlog = a.intlog != 0; c.theta = a.theta;
-        c.lut = a.lut; c.err = a.err;
-        const int64_t grp = e0 / a.G;
-        const GroupMeta m = read_meta(P, grp, c);
+        c.lut = a.lut; c.err = on ? a.err : nullptr;
+        const GroupMeta m = meta_from_record(cur.rec, c);
         uint32_t cf[32];
-        run_code_floats<B>(w, cf);
+        run_code_floats<B>(cur.w, cf);
         if (!c.intlog) {
 #pragma unroll
           for (int k = 0; k < 32; k += 2) {
@@ -286,12 +329,13 @@ __global__ void __launch_bounds__(256, 2) k_moe_combine_q(const __grid_constant_
             v[k] = __double2float_rn(__dadd_rn(__dmul_rn((double)(cf[k] & 0xFFu), m.s64), m.o64));
         }
         if (c.sr) {  // reserved values, imin then imax (codec.py:559-561)
-          const int base = (int)(e0 - grp * a.G);
-          const int ka = m.imin - base, kz = m.imax - base;
-          const bool ha = m.imin >= 0 && (unsigned)ka < 32u, hz = m.imax >= 0 && (unsigned)kz < 32u;
+          const int base = (int)(ec & (a.G - 1));
+          const int ka = m.imin - (a.gshift >= 0 ? base : (int)(ec % a.G)), kz = m.imax - (a.gshift >= 0 ? base : (int)(ec % a.G));
+          const bool ha = on && m.imin >= 0 && (unsigned)ka < 32u, hz = on && m.imax >= 0 && (unsigned)kz < 32u;
           if (ha || hz) {
 #pragma unroll
-            for (int k = 0; k < 32; k += 4) *reinterpret_cast<float4*>(spill + k) = make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]);
+            for (int k = 0; k < 32; k += 4)
+              *reinterpret_cast<float4*>(spill + k) = make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]);
             if (ha) spill[ka] = m.smin;
             if (hz) spill[kz] = m.smax;
 #pragma unroll
@@ -304,6 +348,9 @@ __global__ void __launch_bounds__(256, 2) k_moe_combine_q(const __grid_constant_
       }
 #pragma unroll
       for (int k = 0; k < 32; k += 2) add2(acc[k], acc[k + 1], acc[k], acc[k + 1], v[k], v[k + 1]);
+      dc = dn;
+      ec = en;
+      cur = nxt;
     }
     if (on) {
 #pragma unroll
@@ -407,6 +454,9 @@ int fc2_moe_combine_q(const fc2_config* cfg, int32_t world, int32_t me, const vo
   a.edt = exact_dtype;
   a.me = me; a.world = world;
   a.B = cfg->bitwidth; a.G = cfg->group_size; a.sr = cfg->scheme; a.intlog = cfg->scale_encoding; a.theta = cfg->theta;
+  a.gshift = -1;
+  for (int sh = 0; sh < 16; ++sh)
+    if ((1 << sh) == a.G) a.gshift = sh;
   a.lut = lut;
   a.pos = pos; a.T = tokens; a.H = row_len; a.out = out; a.odt = out_dtype; a.err = dev_err;
   const int64_t tasks = tokens * ((row_len + 1023) / 1024);
