@@ -41,19 +41,39 @@ using namespace fc2;
 
 namespace {
 
+// destination-rank mask of token t (bit d: one of its experts lives on rank d);
+// the token's K ids are loaded before any is used (up to 16 in flight)
 __device__ __forceinline__ uint32_t route_mask(const void* ids, int idx64, int64_t t, int K, int per,
                                                int n_experts, int32_t* err) {
   uint32_t m = 0;
-  for (int k = 0; k < K; ++k) {
-    const int64_t e = idx64 ? reinterpret_cast<const int64_t*>(ids)[t * K + k]
-                            : (int64_t) reinterpret_cast<const int32_t*>(ids)[t * K + k];
-    if (e < 0 || e >= n_experts) {
-      atomicOr(err, FC2_ERR_EXPERT_RANGE);
-      continue;
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    int64_t e[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      e[k] = k0 + k >= K ? 0
+                         : (idx64 ? __ldg(reinterpret_cast<const long long*>(ids) + t * K + k0 + k)
+                                  : (int64_t)__ldg(reinterpret_cast<const int32_t*>(ids) + t * K + k0 + k));
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      if (k0 + k >= K) break;
+      if (e[k] < 0 || e[k] >= n_experts) {
+        atomicOr(err, FC2_ERR_EXPERT_RANGE);
+        continue;
+      }
+      m |= 1u << ((int)e[k] / per);  // 32-bit division: a validated expert id
     }
-    m |= 1u << (int)(e / per);
   }
   return m;
+}
+
+constexpr int kRouteChunk = 8192;  // tokens whose masks the routing CTA stages at once (32 KB of smem)
+
+// pass 1, all SMs: mask of every token, parked in pos[t * world] (pass 2
+// reads a chunk's masks into shared memory before it writes that chunk's pos)
+__global__ void k_moe_masks(const void* ids, int idx64, int64_t T, int K, int per, int n_experts, int world,
+                            int32_t* pos, int32_t* err) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < T) pos[t * world] = (int32_t)route_mask(ids, idx64, t, K, per, n_experts, err);
 }
 
 // One CTA of 1024 threads walks the tokens in rounds of 1024 (thread = token).
@@ -64,13 +84,27 @@ __global__ void __launch_bounds__(1024) k_moe_route(const void* ids, int idx64, 
                                                    int32_t* pos, int32_t* err) {
   __shared__ int32_t woff[32][FC2_MOE_MAX_WORLD];
   __shared__ int32_t base[FC2_MOE_MAX_WORLD];
+  pdl_enter();
+  __shared__ uint32_t masks[kRouteChunk];
   const int lane = (int)(threadIdx.x & 31), warp = (int)(threadIdx.x >> 5);
   const uint32_t lt = (1u << lane) - 1u;
   if (threadIdx.x < (unsigned)world) base[threadIdx.x] = 0;
   __syncthreads();
   for (int64_t t0 = 0; t0 < T; t0 += blockDim.x) {
+    if ((t0 % kRouteChunk) == 0) {  // the next chunk's masks (pass 1), all loads in flight together
+      __syncthreads();
+      uint32_t mk[kRouteChunk / 1024];
+#pragma unroll
+      for (int j = 0; j < kRouteChunk / 1024; ++j) {
+        const int64_t tt = t0 + threadIdx.x + 1024 * j;
+        mk[j] = tt < T ? (uint32_t)__ldcg(pos + tt * world) : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < kRouteChunk / 1024; ++j) masks[threadIdx.x + 1024 * j] = mk[j];
+      __syncthreads();
+    }
     const int64_t t = t0 + threadIdx.x;
-    const uint32_t m = t < T ? route_mask(ids, idx64, t, K, per, n_experts, err) : 0u;
+    const uint32_t m = masks[(t0 % kRouteChunk) + threadIdx.x];
     for (int d = 0; d < world; ++d) {
       const uint32_t bal = __ballot_sync(0xffffffffu, (m >> d) & 1u);
       if (lane == 0) woff[warp][d] = __popc(bal);
@@ -87,16 +121,29 @@ __global__ void __launch_bounds__(1024) k_moe_route(const void* ids, int idx64, 
       base[d] = run;
     }
     __syncthreads();
-    for (int d = 0; d < world; ++d) {
+    // the token's pos row is built in registers and stored with 16-byte
+    // stores (scattered 4-byte stores from one SM were the kernel's bottleneck)
+    int32_t pv[FC2_MOE_MAX_WORLD];
+#pragma unroll
+    for (int d = 0; d < FC2_MOE_MAX_WORLD; ++d) {
+      if (d >= world) break;
       const uint32_t bal = __ballot_sync(0xffffffffu, (m >> d) & 1u);
-      if (t < T) {
-        if ((m >> d) & 1u) {
-          const int p = woff[warp][d] + __popc(bal & lt);
-          rows[(int64_t)d * T + p] = (int32_t)t;
-          pos[t * world + d] = p;
-        } else {
-          pos[t * world + d] = -1;
-        }
+      pv[d] = -1;
+      if (t < T && ((m >> d) & 1u)) {
+        pv[d] = woff[warp][d] + __popc(bal & lt);
+        rows[(int64_t)d * T + pv[d]] = (int32_t)t;
+      }
+    }
+    if (t < T) {
+      int32_t* pr = pos + t * world;
+      if ((world & 3) == 0) {
+#pragma unroll
+        for (int d = 0; d < FC2_MOE_MAX_WORLD; d += 4)
+          if (d < world) *reinterpret_cast<int4*>(pr + d) = make_int4(pv[d], pv[d + 1], pv[d + 2], pv[d + 3]);
+      } else {
+#pragma unroll
+        for (int d = 0; d < FC2_MOE_MAX_WORLD; ++d)
+          if (d < world) pr[d] = pv[d];
       }
     }
     __syncthreads();
@@ -380,8 +427,13 @@ int fc2_moe_route(const void* topk_ids, int32_t ids_are_int64, int64_t tokens, i
   if (tokens == 0) return cudaMemsetAsync(counts, 0, sizeof(int32_t) * world, (cudaStream_t)stream) == cudaSuccess
                               ? FC2_OK
                               : set_err(FC2_ECUDA, "cudaMemsetAsync failed");
-  k_moe_route<<<1, 1024, 0, (cudaStream_t)stream>>>(topk_ids, ids_are_int64 ? 1 : 0, tokens, topk,
-                                                   n_experts / world, n_experts, world, counts, rows, pos, dev_err);
+  const int per = n_experts / world;
+  k_moe_masks<<<(unsigned)((tokens + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      topk_ids, ids_are_int64 ? 1 : 0, tokens, topk, per, n_experts, world, pos, dev_err);
+  int rc = cuda_check("k_moe_masks");
+  if (rc) return rc;
+  launch_pdl(k_moe_route, 1, 1024, 0, (cudaStream_t)stream, topk_ids, ids_are_int64 ? 1 : 0, tokens, topk, per,
+             n_experts, world, counts, rows, pos, dev_err);
   return cuda_check("k_moe_route");
 }
 
