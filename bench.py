@@ -704,6 +704,18 @@ def run_codec(args):
                 "encode_hbm_GBps": round((2 * m + Fm) / (te * 1e-3) / 1e9, 1),
                 "decode_hbm_GBps": round((Fm + 2 * m) / (td * 1e-3) / 1e9, 1)}
             del xs
+    # small-message latency (BASELINE configs[4] sizes, verdict item 7): round
+    # trips back to back in one CUDA-event region, inputs L2-resident (a
+    # communication kernel normally reads what a GEMM just wrote); the
+    # per-step flushed numbers above include ~3 us of event overhead per kernel
+    small_latency = {}
+    if not args.no_sweep:
+        for nb in (1 << 16, 1 << 18, 1 << 20, 1 << 22):
+            m = nb // 2
+            xs3 = [x[k * m:(k + 1) * m] for k in range(ROTATE)]
+            tr, te, td, _, _ = time_roundtrip_region(fc, xs3, cfg, 50, 5)
+            small_latency[f"{nb >> 10}KiB" if nb < (1 << 20) else f"{nb >> 20}MiB"] = {
+                "roundtrip_us": round(tr * 1e3, 2), "encode_us": round(te * 1e3, 2), "decode_us": round(td * 1e3, 2)}
     # end to end through host buffers
     x_host = x.cpu().pin_memory()
     e2e_ms, h2d, d2h = time_e2e(fc, x_host, cfg, max(3, args.steps), 2)
@@ -747,6 +759,8 @@ def run_codec(args):
         "two_step_n8_per_rank_kernels": stages,
         "moe_ep8_per_rank_kernels": moe_stages,
         "size_sweep": size_sweep,
+        "small_message_latency": {"method": "back-to-back round trips in one event region (PDL launches), "
+                                            "inputs L2-resident", **small_latency},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
