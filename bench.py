@@ -877,6 +877,8 @@ def run_multi(args, rank, world, local_rank):
             comm.check()
         except Exception as e:
             raise RuntimeError(f"rank {rank}: stage {name!r} set a device error: {e}") from e
+        if os.environ.get("FC2_BENCH_TRACE"):
+            print(f"[rank {rank}] stage done: {name}", file=sys.stderr, flush=True)
 
     stage_ok("two_step b4")
     # same size at 3 bits (configs[2] names 4-bit and 3-bit)

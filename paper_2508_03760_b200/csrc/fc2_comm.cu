@@ -82,7 +82,6 @@ struct BarrierArgs {
 // peer p's arrival in my array.  fence.sys first: every store this device made
 // before this kernel (earlier kernels on the stream) is ordered before the flag.
 __global__ void k_barrier(const __grid_constant__ BarrierArgs a) {
-  pdl_enter();
   const int p = threadIdx.x;
   if (p >= a.world) return;
   __threadfence_system();
@@ -111,7 +110,6 @@ struct FlagArgs {
 };
 
 __global__ void k_flag_signal(const __grid_constant__ FlagArgs a) {
-  pdl_enter();
   const int p = threadIdx.x;
   if (p >= a.world) return;
   __threadfence_system();
@@ -119,7 +117,6 @@ __global__ void k_flag_signal(const __grid_constant__ FlagArgs a) {
 }
 
 __global__ void k_flag_wait(const __grid_constant__ FlagArgs a) {
-  pdl_enter();
   const int s = threadIdx.x;
   if (s >= a.world) return;
   const long long t0 = clock64();
@@ -238,7 +235,7 @@ int fc2_comm_barrier(fc2_comm* c, int32_t* dev_err, double timeout_s, void* stre
   a.epoch = ++c->epoch;
   a.err = dev_err;
   a.timeout_cycles = (long long)(timeout_s * 2.0e9);
-  launch_pdl(k_barrier, 1, 32, 0, (cudaStream_t)stream, a);
+  k_barrier<<<1, 32, 0, (cudaStream_t)stream>>>(a);
   return cuda_check("k_barrier");
 }
 
@@ -414,14 +411,14 @@ int fc2_allreduce_2step_pipe(fc2_comm* c, const fc2_config* cfg, const void* x, 
     FlagArgs a;
     for (int p = 0; p < N; ++p) a.words[p] = flag(p, stage, r, k);
     a.world = N; a.epoch = epoch; a.err = dev_err; a.timeout_cycles = tmo;
-    launch_pdl(k_flag_signal, 1, 32, 0, s, a);
+    k_flag_signal<<<1, 32, 0, s>>>(a);
     return cuda_check("k_flag_signal");
   };
   auto wait = [&](int stage, int k, cudaStream_t s) {
     FlagArgs a;
     for (int p = 0; p < N; ++p) a.words[p] = flag(r, stage, p, k);
     a.world = N; a.epoch = epoch; a.err = dev_err; a.timeout_cycles = tmo;
-    launch_pdl(k_flag_wait, 1, 32, 0, s, a);
+    k_flag_wait<<<1, 32, 0, s>>>(a);
     return cuda_check("k_flag_wait");
   };
   // the side streams start where the caller's stream is now

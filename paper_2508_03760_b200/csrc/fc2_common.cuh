@@ -122,7 +122,13 @@ inline void launch_pdl(K kern, unsigned grid, unsigned block, int smem, cudaStre
 #endif
 }
 
-// (every kernel launched through launch_pdl must begin with pdl_enter)
+// (every kernel launched through launch_pdl must begin with pdl_enter).  The
+// communicator's spin-wait kernels (k_barrier, k_flag_wait / k_flag_signal)
+// are launched normally and never release their dependents early: a
+// dependent grid launched early parks its CTAs in griddepcontrol.wait, and
+// behind a kernel that waits for another stream or a peer those parked CTAs
+// can take the SM slots that stream / peer needs (a deadlock observed with
+// back-to-back pipelined AllReduce calls).
 
 // ---------------------------------------------------------------------------
 // fp32 code estimate with a 14-bit fixed-point fraction:
