@@ -69,6 +69,23 @@ def _worker(rank, world, port, case, q):
                 back = comm.moe_combine(yo, h, out_dtype=torch.float32, check=True)
                 outs.append((recv.cpu().numpy().tobytes(), back.cpu().numpy().tobytes()))
             q.put((rank, outs))
+        elif kind == "back_to_back":
+            # the bench's timed loop: many calls of every algorithm enqueued back
+            # to back on one stream with no host synchronization in between,
+            # inputs rotating over 3 tensors (catches cross-call buffer reuse
+            # races and launch-ordering deadlocks); the last result per
+            # algorithm is checked against the oracle
+            comm = QComm(max_elems=n, config=cfg, timeout_s=60.0, oneshot_max_elems=n, pipe_chunks=4)
+            xs = [torch.from_numpy(O.bf16_snap(O.spiky(n, s2)).astype(np.float32)).cuda().to(torch.bfloat16)
+                  for s2 in O.child_seeds(seed + rank, 3)]
+            outs = []
+            for algo in ("two_step", "pipelined", "one_shot"):
+                y = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+                for i in range(12):
+                    comm.all_reduce(xs[i % 3], out=y, algo=algo)
+                comm.check()
+                outs.append(y.float().cpu().numpy().tobytes())
+            q.put((rank, outs))
         elif kind == "a2a_errors":
             # (1) blocks that do not fit the All2All region -> ConfigError (the
             # one-shot region behind it must never be overwritten); (2) NaN in
@@ -133,6 +150,20 @@ def test_ipc_two_step_matches_reference_algorithm(world, n, bits, g, sr):
     want, _ = O.two_step(payloads, bits, g, sr)
     for r in range(world):
         for blob in got[r]:  # float32 and bf16 outputs
+            assert np.array_equal(np.frombuffer(blob, dtype=np.float32), want[0])
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("world,n", [(2, 1 << 20), (4, 3 << 16)])
+def test_ipc_back_to_back_calls(world, n):
+    got = _run(world, ("back_to_back", n, 4, 128, True, 31))
+    # call 11 used input set 11 % 3 = 2 on every rank
+    payloads = []
+    for r in range(world):
+        payloads.append(O.bf16_snap(O.spiky(n, O.child_seeds(31 + r, 3)[2])).astype(np.float32))
+    want, _ = O.two_step(payloads, 4, 128, True)
+    for r in range(world):
+        for blob in got[r]:
             assert np.array_equal(np.frombuffer(blob, dtype=np.float32), want[0])
 
 
