@@ -685,6 +685,7 @@ static int host_pipeline(int mode, const fc2_config* cfg, const void* x_host, in
   slice = (slice + unit - 1) / unit * unit;
   HostPipe* hp = host_pipe(&rc);
   if (rc) return rc;
+  NoPdl no_pdl;  // kernels here follow cross-stream event waits
   cudaStream_t st = (cudaStream_t)stream;
   if (cudaEventRecord(hp->fork, st) != cudaSuccess) return set_err(FC2_ECUDA, "fork event failed");
   for (int i = 0; i < kPipeStreams; ++i) cudaStreamWaitEvent(hp->s[i], hp->fork, 0);

@@ -362,6 +362,7 @@ int fc2_allreduce_oneshot(fc2_comm* c, const fc2_config* cfg, const void* x, int
 int fc2_allreduce_2step_pipe(fc2_comm* c, const fc2_config* cfg, const void* x, int32_t x_dtype, void* y,
                              int32_t y_dtype, int64_t n, int32_t chunks, int64_t chunk_bytes, int64_t region_off,
                              int64_t region_bytes, int32_t* dev_err, double timeout_s, void* stream) {
+  NoPdl no_pdl;  // three streams joined by events: plain launches
   const int N = c->world, r = c->rank;
   int rc = fc2_check_config(cfg);
   if (rc) return rc;

@@ -103,9 +103,24 @@ __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
 #endif
 }
+// Host paths that schedule kernels on several streams with event waits (the
+// host-resident pipeline, the pipelined two-step) hold a NoPdl guard: their
+// launches are plain, so no kernel can start ahead of an event it waits on.
+inline int& pdl_off_depth() {
+  static thread_local int d = 0;
+  return d;
+}
+struct NoPdl {
+  NoPdl() { ++pdl_off_depth(); }
+  ~NoPdl() { --pdl_off_depth(); }
+};
 template <typename K, typename... Args>
 inline void launch_pdl(K kern, unsigned grid, unsigned block, int smem, cudaStream_t st, Args... args) {
 #if FC2_PDL
+  if (pdl_off_depth() > 0) {
+    kern<<<grid, block, smem, st>>>(args...);
+    return;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
