@@ -315,17 +315,15 @@ __device__ __forceinline__ void quant_runs(const uint8_t* ist, uint32_t* tms, co
         if constexpr (FB == 16) tie_acc16(tacc[j >> 1], y0, y1, 4 * (j & 1) + pp);
         else tie_acc15(tacc[j >> 1], y0, y1, 4 * (j & 1) + pp);
       }
-      if constexpr (FB == 16) {
+      // FB = 15 (8-bit codes in bits [15, 23)): one shift (IMAD on the FMA
+      // pipe) puts the code in byte 2 as for FB = 16, so the same byte-permute
+      // packing applies
 #pragma unroll
-        for (int e = 0; e < 8; ++e) XR[8 * j + e] = X[e];
-      } else {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) lw.template put_fixb<FB>(8 * j + e, X[e], 0);
-      }
+      for (int e = 0; e < 8; ++e) XR[8 * j + e] = FB == 16 ? X[e] : X[e] << 1;
     }
     // spike slots hold an in-range stand-in (encode_tile_bf16), so every code
     // fits its width and no masking is needed when the unit is the whole code
-    if constexpr (FB == 16) pack_run_fb16<B, false>(XR, lw.w);
+    pack_run_fb16<B, false>(XR, lw.w);
 #pragma unroll
     for (int i = 0; i < B; ++i) pw[q][i] = lw.w[i];
     // near-tie masks of this run, resolved after all runs (one divergent
