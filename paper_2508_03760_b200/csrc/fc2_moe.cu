@@ -302,17 +302,20 @@ __global__ void __launch_bounds__(256, 2) k_moe_combine_q(const __grid_constant_
   __shared__ __align__(16) float spill_all[8][32][36];
   const int warp = (int)(threadIdx.x >> 5), lane = (int)(threadIdx.x & 31);
   float* spill = spill_all[warp][lane];
-  const int64_t segs = (a.H + 1023) / 1024;
-  const int64_t tasks = a.T * segs;
-  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  // 32-bit task / position arithmetic (the launcher checks T * segments and
+  // H against INT32_MAX): no 64-bit division per task
+  const int H = (int)a.H;
+  const int segs = (H + 1023) / 1024;
+  const int tasks = (int)a.T * segs;
+  const int nw = (int)gridDim.x * (int)(blockDim.x >> 5);
   const int rb = rec_bytes(a.sr != 0, a.intlog != 0);
   bool bad = false;
-  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; w < tasks; w += nw) {
-    const int64_t t = w / segs;
-    const int64_t h = (w - t * segs) * 1024 + 32 * lane;
-    const bool on = h < a.H;
+  for (int w = (int)blockIdx.x * (int)(blockDim.x >> 5) + warp; w < tasks; w += nw) {
+    const int t = w / segs;
+    const int h = (w - t * segs) * 1024 + 32 * lane;
+    const bool on = h < H;
     // the token's row index in every source block: one load per lane, then shuffles
-    const int mypos = lane < a.world ? __ldg(a.pos + t * a.world + lane) : -1;
+    const int mypos = lane < a.world ? __ldg(a.pos + (int64_t)t * a.world + lane) : -1;
     uint32_t todo = __ballot_sync(0xffffffffu, mypos >= 0);  // source ranks in order
     float acc[32];
 #pragma unroll
@@ -331,7 +334,7 @@ __global__ void __launch_bounds__(256, 2) k_moe_combine_q(const __grid_constant_
     if (todo) {
       dc = __ffs(todo) - 1;
       todo &= todo - 1;
-      ec = (int64_t)__shfl_sync(0xffffffffu, mypos, dc) * a.H + h;
+      ec = (int64_t)__shfl_sync(0xffffffffu, mypos, dc) * H + h;
       load(dc, ec, cur);
     }
     while (dc >= 0) {  // warp-uniform
@@ -340,7 +343,7 @@ __global__ void __launch_bounds__(256, 2) k_moe_combine_q(const __grid_constant_
       if (todo) {  // next source's loads go out before this one is decoded
         dn = __ffs(todo) - 1;
         todo &= todo - 1;
-        en = (int64_t)__shfl_sync(0xffffffffu, mypos, dn) * a.H + h;
+        en = (int64_t)__shfl_sync(0xffffffffu, mypos, dn) * H + h;
         load(dn, en, nxt);
       }
       float v[32];
@@ -401,7 +404,7 @@ __global__ void __launch_bounds__(256, 2) k_moe_combine_q(const __grid_constant_
     }
     if (on) {
 #pragma unroll
-      for (int k = 0; k < 32; k += 8) store8_any(a.out, a.odt, t * a.H + h + k, acc + k);
+      for (int k = 0; k < 32; k += 8) store8_any(a.out, a.odt, (int64_t)t * H + h + k, acc + k);
     }
   }
   if (bad) atomicOr(a.err, FC2_ERR_NONFINITE);
@@ -512,6 +515,8 @@ int fc2_moe_combine_q(const fc2_config* cfg, int32_t world, int32_t me, const vo
   a.lut = lut;
   a.pos = pos; a.T = tokens; a.H = row_len; a.out = out; a.odt = out_dtype; a.err = dev_err;
   const int64_t tasks = tokens * ((row_len + 1023) / 1024);
+  if (tasks > INT32_MAX || row_len > INT32_MAX - 1024)
+    return set_err(FC2_ECONFIG, "combine of %lld tokens x %lld is too large", (long long)tokens, (long long)row_len);
   int64_t blocks = (tasks + 7) / 8;
   const int64_t cap = (int64_t)num_sms() * 8;
   if (blocks > cap) blocks = cap;
