@@ -975,6 +975,10 @@ def run_multi(args, rank, world, local_rank):
             row[f"b{bits}_us"] = round(t * 1e3, 2)
             row[f"b{bits}_algbw_GBps"] = round(nb / (t * 1e-3) / 1e9, 2)
             stage_ok(f"sweep {nb} B b{bits}")
+            if bits == 4 and m <= comm.os_lay.n:  # the fused single-kernel one-shot (row f1)
+                t = statistics.mean(timed(lambda: comm.all_reduce(xm, out=ym, config=cb, algo="fused"), k, 3))
+                row["b4_fused_us"] = round(t * 1e3, 2)
+                stage_ok(f"sweep {nb} B b4 fused")
         if backend == "nccl":
             xc = xm.clone()
             t = statistics.mean(timed(lambda: dist.all_reduce(xc), k, 3))

@@ -224,6 +224,14 @@ int fc2_allreduce_2step(fc2_comm* c, const fc2_config* cfg, const void* x, int32
 int fc2_allreduce_oneshot(fc2_comm* c, const fc2_config* cfg, const void* x, int32_t x_dtype, void* y,
                           int32_t y_dtype, int64_t n, int64_t slot_bytes, int64_t region_off,
                           int32_t* dev_err, double timeout_s, void* stream);
+/* Fused one-shot AllReduce ("a fused single-kernel two-step
+ * with in-kernel flags"): the result of fc2_allreduce_oneshot -- same region,
+ * same bits -- from one cooperative kernel: pack + peer stores, an in-kernel
+ * grid barrier and cross-rank flags, then reduce + requantize + decode of every
+ * shard.  bf16 / f32 tensors; float64-exact generic codec (latency regime). */
+int fc2_allreduce_fused(fc2_comm* c, const fc2_config* cfg, const void* x, int32_t x_dtype, void* y,
+                        int32_t y_dtype, int64_t n, int64_t slot_bytes, int64_t region_off, int32_t* dev_err,
+                        double timeout_s, void* stream);
 
 /* Pipelined two-step (the NVSwitch form of the reference's microchunked
  * schedule, scheduling.py:119-156 over collectives.py:263-315): the shard is

@@ -69,6 +69,7 @@ SIGNATURES = {
     "fc2_reduce_requant": (_I32, [_PCFG, _I32, _PP, _I64, _I32, _PP, _P, _P]),
     "fc2_reduce_requant_batch": (_I32, [_PCFG, _I32, _PP, _I64, _I32, _I64, _I32, _PP, _I64, _P, _P]),
     "fc2_allreduce_oneshot": (_I32, [_P, _PCFG, _P, _I32, _P, _I32, _I64, _I64, _I64, _P, ctypes.c_double, _P]),
+    "fc2_allreduce_fused": (_I32, [_P, _PCFG, _P, _I32, _P, _I32, _I64, _I64, _I64, _P, ctypes.c_double, _P]),
     "fc2_gather_decode": (_I32, [_PCFG, _I32, _PP, _I64, _P, _I32, _I64, _P, _P]),
     "fc2_pack_codes": (_I32, [_P, _I64, _I32, _P, _P, _P]),
     "fc2_unpack_codes": (_I32, [_P, _I64, _I32, _P, _P]),

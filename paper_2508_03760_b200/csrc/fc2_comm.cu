@@ -29,12 +29,16 @@
 
 #include "../../include/fc2.h"
 #include "fc2_common.cuh"
+#include "fc2_decode.cuh"
+#include "fc2_encode.cuh"
 
 namespace fc2 {
 int set_err(int code, const char* fmt, ...);
 int cuda_check(const char* what);
 int decode_batch_grid(const fc2_config* cfg, int32_t y_dtype, int32_t njobs, const void* const* payloads,
                       const int64_t* n, void* const* ys, const int64_t* n_out, int32_t* dev_err, void* stream);
+const double* lut_for_cfg(const fc2_config* c, int* rc);
+int num_sms();
 }  // namespace fc2
 
 using namespace fc2;
@@ -43,6 +47,7 @@ using namespace fc2;
 #define FC2_FLAG_BYTES 16384
 #define FC2_PIPE_FLAGS 4096   // flag page: pipelined two-step flags [stage][src][chunk]
 #define FC2_PIPE_MAXK 16
+#define FC2_FUSED_CTR 8192    // flag page: the fused one-shot's grid-barrier counter (local)
 
 struct fc2_comm {
   int rank, world, device;
@@ -52,6 +57,7 @@ struct fc2_comm {
   bool opened[FC2_COMM_MAX];
   uint32_t epoch;
   uint32_t oneshot_calls;  // parity selects the one-shot landing buffer
+  uint32_t fused_arrivals; // fused one-shot: CTAs that have reached its grid barrier so far
   uint32_t ag_calls;       // parity selects the small all-gather area
   uint32_t pipe_epoch;     // pipelined two-step: flag value of the current call (parity: buffer set)
   cudaStream_t s_red, s_gat;  // pipelined two-step: reduce / gather-decode streams (lazy)
@@ -141,6 +147,154 @@ __global__ void __launch_bounds__(512) k_copy_bytes(uint8_t* __restrict__ dst, c
     reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
   const int64_t tail = nbytes & 15;
   if (blockIdx.x == 0 && (int64_t)threadIdx.x < tail) dst[(n16 << 4) + threadIdx.x] = src[(n16 << 4) + threadIdx.x];
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Fused one-shot AllReduce ("a fused single-kernel two-step
+// with in-kernel flags"): one cooperative launch does what
+// fc2_allreduce_oneshot does in four (encode -> barrier -> reduce+requant ->
+// decode).  Warp = one group, float64-exact generic codec throughout (the
+// same bits as the fast kernels; this path is for latency-bound sizes):
+//   phase 1  group g of shard j of x -> packed, stored once per peer into
+//            landing[par][me][j] of every rank (up to 8 destinations per store);
+//   barrier  every CTA bumps a local counter; CTA 0 waits for all of them,
+//            then publishes "rank r reached epoch" to every peer (the
+//            k_barrier protocol) and every CTA waits for all peers' flags;
+//   phase 2  group g of shard j: the N landed sources decoded and summed in
+//            fp32 in rank order from +0.0, requantized into the local result
+//            slot, decoded back to the bf16 grid straight into y.
+// The landing parity alternates with fc2_allreduce_oneshot's, so mixed calls
+// stay safe without a trailing barrier.
+// ---------------------------------------------------------------------------
+namespace {
+
+struct FusedArgs {
+  const void* x;
+  int xdt;
+  void* y;
+  int ydt;
+  int64_t n, S;             // elements, shard length (padded / N)
+  int N, r, par;
+  uint8_t* base[FC2_COMM_MAX];  // every rank's symmetric buffer (this process' mapping) + flag page
+  int64_t region_off, slot;
+  uint32_t* arrive_mine;
+  uint32_t* arrive_peer[FC2_COMM_MAX];
+  uint32_t epoch;
+  uint32_t* gctr;
+  uint32_t gtarget;
+  int B, G, sr, intlog, theta;
+  const double* lut;
+  int32_t* err;
+  long long timeout_cycles;
+};
+
+struct LandedSum {  // element i of shard j: fp32 rank-order sum of the N landed sources
+  const uint8_t* src[FC2_COMM_MAX];
+  int N;
+  DecCtx c;
+  __device__ double operator()(int64_t i) const {
+    float s = 0.0f;
+    for (int k = 0; k < N; ++k) s = __fadd_rn(s, decode_elem32(src[k], i, c));
+    return (double)s;
+  }
+};
+
+template <typename T>
+struct ShardLoader {
+  const T* x;
+  int64_t nv;
+  __device__ double operator()(int64_t i) const {
+    if (i >= nv) return 0.0;
+    if constexpr (sizeof(T) == 2) return (double)__bfloat162float(x[i]);
+    else return (double)x[i];
+  }
+};
+
+__device__ __forceinline__ uint8_t* fused_land(const FusedArgs& a, int dst, int src, int shard) {
+  return a.base[dst] + a.region_off + ((int64_t)a.par * a.N * a.N + (int64_t)src * a.N + shard) * a.slot;
+}
+
+__device__ bool spin_until(const uint32_t* p, uint32_t target, const FusedArgs& a) {
+  const long long t0 = clock64();
+  while ((int32_t)(ld_acquire_sys(p) - target) < 0) {
+    if (clock64() - t0 > a.timeout_cycles) {
+      atomicOr(a.err, FC2_ERR_TIMEOUT);
+      return false;
+    }
+    __nanosleep(128);
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(256) k_allreduce_fused(const __grid_constant__ FusedArgs a) {
+  const int warp = (int)(threadIdx.x >> 5), lane = (int)(threadIdx.x & 31);
+  const int64_t gps = a.S / a.G;            // groups per shard
+  const int64_t total = gps * a.N;          // groups of the padded tensor
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  EncCtx cx;
+  cx.n = a.S; cx.meta_off = a.S * a.B / 8; cx.intlog = a.intlog; cx.theta = a.theta; cx.lut = a.lut;
+  cx.err = a.err;
+  // ---- phase 1: my shards, packed, into every rank's landing row for me
+  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; w < total; w += nw) {
+    const int j = (int)(w / gps);
+    const int64_t gl = w - (int64_t)j * gps;
+    int64_t nv = a.n - (int64_t)j * a.S;
+    nv = nv < 0 ? 0 : (nv > a.S ? a.S : nv);
+    for (int d0 = 0; d0 < a.N; d0 += 8) {  // OutList carries up to 8 destinations
+      OutList o;
+      o.nd = a.N - d0 < 8 ? a.N - d0 : 8;
+      for (int d = 0; d < o.nd; ++d) o.p[d] = fused_land(a, d0 + d, a.r, j);
+      if (a.xdt == FC2_BF16) {
+        ShardLoader<__nv_bfloat16> ld{reinterpret_cast<const __nv_bfloat16*>(a.x) + (int64_t)j * a.S, nv};
+        generic_encode_group(ld, o, a.S, gl, a.B, a.G, a.sr != 0, cx);
+      } else {
+        ShardLoader<float> ld{reinterpret_cast<const float*>(a.x) + (int64_t)j * a.S, nv};
+        generic_encode_group(ld, o, a.S, gl, a.B, a.G, a.sr != 0, cx);
+      }
+    }
+  }
+  // ---- grid barrier (co-resident CTAs: cooperative launch), then the peers
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    atomicAdd(a.gctr, 1u);
+    if (blockIdx.x == 0 && spin_until(a.gctr, a.gtarget, a)) {
+      __threadfence_system();
+      for (int p = 0; p < a.N; ++p) st_release_sys(a.arrive_peer[p] + a.r, a.epoch);
+    }
+    for (int p = 0; p < a.N; ++p)
+      if (!spin_until(a.arrive_mine + p, a.epoch, a)) break;
+    __threadfence_system();
+  }
+  __syncthreads();
+  // ---- phase 2: every shard reduced, requantized and decoded locally
+  uint8_t* result = a.base[a.r] + a.region_off + (int64_t)2 * a.N * a.N * a.slot;
+  DecCtx dc;
+  dc.n = a.S; dc.meta_off = a.S * a.B / 8; dc.B = a.B; dc.G = a.G; dc.sr = a.sr != 0; dc.intlog = a.intlog != 0;
+  dc.theta = a.theta; dc.lut = a.lut; dc.err = a.err;
+  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; w < total; w += nw) {
+    const int j = (int)(w / gps);
+    const int64_t gl = w - (int64_t)j * gps;
+    LandedSum sum;
+    sum.N = a.N;
+    sum.c = dc;
+    for (int s2 = 0; s2 < a.N; ++s2) sum.src[s2] = fused_land(a, a.r, s2, j);
+    OutList o;
+    o.nd = 1;
+    o.p[0] = result + (int64_t)j * a.slot;
+    generic_encode_group(sum, o, a.S, gl, a.B, a.G, a.sr != 0, cx);
+    __syncwarp();  // the group's planes and record, written by the warp, before the warp reads them back
+    for (int e = lane; e < a.G; e += 32) {
+      const int64_t idx = (int64_t)j * a.S + gl * a.G + e;
+      if (idx >= a.n) break;
+      const uint32_t bits = bf16_bits(decode_elem32(o.p[0], gl * a.G + e, dc));  // bf16 grid (collectives.py:185-186)
+      if (a.ydt == FC2_BF16) reinterpret_cast<uint16_t*>(a.y)[idx] = (uint16_t)bits;
+      else reinterpret_cast<float*>(a.y)[idx] = bf16_val(bits);
+    }
+    __syncwarp();
+  }
 }
 
 }  // namespace
@@ -344,6 +498,63 @@ int fc2_allreduce_oneshot(fc2_comm* c, const fc2_config* cfg, const void* x, int
   std::vector<const void*> gs(N);
   for (int o = 0; o < N; ++o) gs[o] = result + (int64_t)o * slot_bytes;
   return fc2_gather_decode(cfg, N, gs.data(), S, y, y_dtype, n, dev_err, stream);
+}
+
+// Fused one-shot AllReduce: same region, same result bits as
+// fc2_allreduce_oneshot, one cooperative kernel (see k_allreduce_fused).
+int fc2_allreduce_fused(fc2_comm* c, const fc2_config* cfg, const void* x, int32_t x_dtype, void* y,
+                        int32_t y_dtype, int64_t n, int64_t slot_bytes, int64_t region_off, int32_t* dev_err,
+                        double timeout_s, void* stream) {
+  const int N = c->world, r = c->rank;
+  int rc = fc2_check_config(cfg);
+  if (rc) return rc;
+  if ((x_dtype != FC2_BF16 && x_dtype != FC2_F32) || (y_dtype != FC2_BF16 && y_dtype != FC2_F32))
+    return set_err(FC2_ECONFIG, "the fused one-shot takes bf16 / f32 tensors");
+  const int64_t mult = (int64_t)N * cfg->group_size;
+  const int64_t padded = (n + mult - 1) / mult * mult;
+  const int64_t S = padded / N;
+  int64_t F = 0;
+  rc = fc2_footprint(cfg, S, &F);
+  if (rc) return rc;
+  if (F > slot_bytes || (slot_bytes & 15)) return set_err(FC2_ECONFIG, "slot too small for shard footprint");
+  if (region_off < 0 || (region_off & 15) ||
+      region_off + (int64_t)(2 * N * N + N) * slot_bytes > c->bytes - FC2_FLAG_BYTES)
+    return set_err(FC2_ECONFIG, "communicator buffer too small for the one-shot region");
+  const double* lut = lut_for_cfg(cfg, &rc);
+  if (rc) return rc;
+  if (n == 0) return FC2_OK;
+  FusedArgs a;
+  memset(&a, 0, sizeof(a));
+  a.x = x; a.xdt = x_dtype; a.y = y; a.ydt = y_dtype; a.n = n; a.S = S; a.N = N; a.r = r;
+  a.par = (int)(c->oneshot_calls++ & 1u);
+  for (int p = 0; p < N; ++p) {
+    a.base[p] = c->peer[p] + FC2_FLAG_BYTES;
+    a.arrive_peer[p] = (uint32_t*)c->peer[p];
+  }
+  a.region_off = region_off; a.slot = slot_bytes;
+  a.arrive_mine = (uint32_t*)c->local;
+  a.epoch = ++c->epoch;
+  a.gctr = (uint32_t*)(c->local + FC2_FUSED_CTR);
+  a.B = cfg->bitwidth; a.G = cfg->group_size; a.sr = cfg->scheme; a.intlog = cfg->scale_encoding;
+  a.theta = cfg->theta; a.lut = lut; a.err = dev_err;
+  a.timeout_cycles = (long long)(timeout_s * 2.0e9);
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_allreduce_fused, 256, 0);
+    if (per_sm < 1) per_sm = 1;
+  }
+  const int64_t groups = padded / cfg->group_size;
+  int64_t grid = (groups + 7) / 8;
+  const int64_t cap = (int64_t)per_sm * num_sms();
+  if (grid > cap) grid = cap;
+  if (grid < 1) grid = 1;
+  c->fused_arrivals += (uint32_t)grid;
+  a.gtarget = c->fused_arrivals;
+  void* args[] = {&a};
+  if (cudaLaunchCooperativeKernel((const void*)k_allreduce_fused, dim3((unsigned)grid), dim3(256), args, 0,
+                                  (cudaStream_t)stream) != cudaSuccess)
+    return cuda_check("k_allreduce_fused (cooperative launch)");
+  return cuda_check("k_allreduce_fused");
 }
 
 // Pipelined two-step (the NVSwitch form of the reference's

@@ -234,8 +234,11 @@ class QComm:
 
         ``algo``: ``"two_step"`` (two packed exchanges), ``"one_shot"`` (one
         all-gather of packed shards, every rank reduces every shard: fewer
-        barriers for latency-bound sizes, same bits), or ``"auto"`` (one-shot
-        up to ``oneshot_max_elems`` on the ipc transport).  ``config``
+        barriers for latency-bound sizes, same bits), ``"fused"`` (the
+        one-shot as one cooperative kernel with in-kernel flags),
+        ``"pipelined"`` (microchunked two-step on three streams), or
+        ``"auto"`` (one-shot up to ``oneshot_max_elems`` on the ipc
+        transport, else two-step).  ``config``
         overrides the communicator's codec for this call when its packed
         shards fit the communicator's slots (e.g. fewer bits)."""
         cfg = self.cfg if config is None else config
@@ -249,8 +252,22 @@ class QComm:
             raise DataError(f"payload of {n} elements exceeds the communicator's {self.max_lay.n}")
         y = out if out is not None else torch.empty(n, dtype=x.dtype, device=x.device)
         lay = TwoStepLayout.make(n, self.world, cfg)
-        if algo not in ("auto", "two_step", "one_shot", "pipelined"):
+        if algo not in ("auto", "two_step", "one_shot", "pipelined", "fused"):
             raise ConfigError(f"unknown allreduce algorithm {algo!r}")
+        if algo == "fused":
+            # the one-shot's result from one cooperative kernel (row f1)
+            if self.transport != "ipc" or n > self.os_lay.n:
+                raise ConfigError("fused needs the ipc transport and n <= oneshot_max_elems")
+            if x.dtype not in (torch.bfloat16, torch.float32) or y.dtype not in (torch.bfloat16, torch.float32):
+                raise ConfigError("fused takes bf16 / float32 tensors")
+            c = cfg.c_struct()
+            _lib.check(_lib.lib().fc2_allreduce_fused(
+                self._c, ctypes.byref(c), x.data_ptr(), _device.dtype_code(x), y.data_ptr(),
+                _device.dtype_code(y), n, self.os_lay.slot_bytes, self.os_off, self.err.data_ptr(),
+                self.timeout_s, _device.stream_handle()))
+            if check:
+                self.check()
+            return y
         if algo == "pipelined":
             if self.transport != "ipc":
                 raise ConfigError("the pipelined two-step needs the ipc transport")

@@ -45,7 +45,8 @@ def _worker(rank, world, port, case, q):
             outs = []
             # both algorithms, both output types; the one-shot runs three times
             # so both landing buffers (call parity) are exercised
-            for algo in ("two_step", "one_shot", "one_shot", "one_shot", "pipelined", "pipelined", "pipelined"):
+            for algo in ("two_step", "one_shot", "one_shot", "one_shot", "pipelined", "pipelined", "pipelined",
+                         "fused", "one_shot", "fused", "fused"):
                 for dt in (torch.float32, torch.bfloat16):
                     y = comm.all_reduce(x.to(dt), check=True, algo=algo)
                     outs.append(y.float().cpu().numpy().tobytes())
@@ -79,7 +80,7 @@ def _worker(rank, world, port, case, q):
             xs = [torch.from_numpy(O.bf16_snap(O.spiky(n, s2)).astype(np.float32)).cuda().to(torch.bfloat16)
                   for s2 in O.child_seeds(seed + rank, 3)]
             outs = []
-            for algo in ("two_step", "pipelined", "one_shot"):
+            for algo in ("two_step", "pipelined", "one_shot", "fused"):
                 y = torch.empty(n, dtype=torch.bfloat16, device="cuda")
                 for i in range(12):
                     comm.all_reduce(xs[i % 3], out=y, algo=algo)
