@@ -88,6 +88,7 @@ struct BarrierArgs {
 // peer p's arrival in my array.  fence.sys first: every store this device made
 // before this kernel (earlier kernels on the stream) is ordered before the flag.
 __global__ void k_barrier(const __grid_constant__ BarrierArgs a) {
+  pdl_wait_only();
   const int p = threadIdx.x;
   if (p >= a.world) return;
   __threadfence_system();
@@ -116,6 +117,7 @@ struct FlagArgs {
 };
 
 __global__ void k_flag_signal(const __grid_constant__ FlagArgs a) {
+  pdl_wait_only();
   const int p = threadIdx.x;
   if (p >= a.world) return;
   __threadfence_system();
@@ -123,6 +125,7 @@ __global__ void k_flag_signal(const __grid_constant__ FlagArgs a) {
 }
 
 __global__ void k_flag_wait(const __grid_constant__ FlagArgs a) {
+  pdl_wait_only();
   const int s = threadIdx.x;
   if (s >= a.world) return;
   const long long t0 = clock64();
@@ -190,26 +193,14 @@ struct FusedArgs {
   long long timeout_cycles;
 };
 
-struct LandedSum {  // element i of shard j: fp32 rank-order sum of the N landed sources
-  const uint8_t* src[FC2_COMM_MAX];
-  int N;
-  DecCtx c;
-  __device__ double operator()(int64_t i) const {
-    float s = 0.0f;
-    for (int k = 0; k < N; ++k) s = __fadd_rn(s, decode_elem32(src[k], i, c));
-    return (double)s;
-  }
-};
+constexpr int kFusedMaxG = 256;  // largest group the fused kernel stages (8 warps x 1 KB of smem)
 
-template <typename T>
-struct ShardLoader {
-  const T* x;
-  int64_t nv;
-  __device__ double operator()(int64_t i) const {
-    if (i >= nv) return 0.0;
-    if constexpr (sizeof(T) == 2) return (double)__bfloat162float(x[i]);
-    else return (double)x[i];
-  }
+// element i of the chunk from the warp's staged group (floats, exact for bf16 /
+// f32 input and for fp32 sums); g0 = first element of the group
+struct StagedGroup {
+  const float* v;
+  int64_t g0;
+  __device__ double operator()(int64_t i) const { return (double)v[i - g0]; }
 };
 
 __device__ __forceinline__ uint8_t* fused_land(const FusedArgs& a, int dst, int src, int shard) {
@@ -236,24 +227,32 @@ __global__ void __launch_bounds__(256) k_allreduce_fused(const __grid_constant__
   EncCtx cx;
   cx.n = a.S; cx.meta_off = a.S * a.B / 8; cx.intlog = a.intlog; cx.theta = a.theta; cx.lut = a.lut;
   cx.err = a.err;
-  // ---- phase 1: my shards, packed, into every rank's landing row for me
+  // ---- phase 1: my shards, packed, into every rank's landing row for me.
+  // The group is staged in shared memory first (coalesced loads, one round
+  // trip) so the float64 encoder's two passes over it never touch global memory.
+  __shared__ float stage[8][kFusedMaxG];
+  float* sg = stage[warp];
   for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; w < total; w += nw) {
     const int j = (int)(w / gps);
     const int64_t gl = w - (int64_t)j * gps;
-    int64_t nv = a.n - (int64_t)j * a.S;
-    nv = nv < 0 ? 0 : (nv > a.S ? a.S : nv);
+    const int64_t e0 = (int64_t)j * a.S + gl * a.G;  // element of x
+    for (int e = lane; e < a.G; e += 32) {
+      const int64_t idx = e0 + e;
+      float v = 0.0f;  // zero padding past n (collectives.py:167-172)
+      if (idx < a.n && (int64_t)gl * a.G + e < a.S)
+        v = a.xdt == FC2_BF16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(a.x)[idx])
+                              : reinterpret_cast<const float*>(a.x)[idx];
+      sg[e] = v;
+    }
+    __syncwarp();
+    const StagedGroup ld{sg, gl * a.G};
     for (int d0 = 0; d0 < a.N; d0 += 8) {  // OutList carries up to 8 destinations
       OutList o;
       o.nd = a.N - d0 < 8 ? a.N - d0 : 8;
       for (int d = 0; d < o.nd; ++d) o.p[d] = fused_land(a, d0 + d, a.r, j);
-      if (a.xdt == FC2_BF16) {
-        ShardLoader<__nv_bfloat16> ld{reinterpret_cast<const __nv_bfloat16*>(a.x) + (int64_t)j * a.S, nv};
-        generic_encode_group(ld, o, a.S, gl, a.B, a.G, a.sr != 0, cx);
-      } else {
-        ShardLoader<float> ld{reinterpret_cast<const float*>(a.x) + (int64_t)j * a.S, nv};
-        generic_encode_group(ld, o, a.S, gl, a.B, a.G, a.sr != 0, cx);
-      }
+      generic_encode_group(ld, o, a.S, gl, a.B, a.G, a.sr != 0, cx, true);
     }
+    __syncwarp();
   }
   // ---- grid barrier (co-resident CTAs: cooperative launch), then the peers
   __syncthreads();
@@ -277,19 +276,52 @@ __global__ void __launch_bounds__(256) k_allreduce_fused(const __grid_constant__
   for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; w < total; w += nw) {
     const int j = (int)(w / gps);
     const int64_t gl = w - (int64_t)j * gps;
-    LandedSum sum;
-    sum.N = a.N;
-    sum.c = dc;
-    for (int s2 = 0; s2 < a.N; ++s2) sum.src[s2] = fused_land(a, a.r, s2, j);
+    const int64_t g0 = gl * a.G;  // group start inside the shard
+    // every source's record first (independent loads), then its codes: sums in
+    // fp32 from +0.0 in rank order, lane = elements lane, lane + 32, ...
+    float acc[kFusedMaxG / 32];
+#pragma unroll
+    for (int k = 0; k < kFusedMaxG / 32; ++k) acc[k] = 0.0f;
+    for (int s0 = 0; s0 < a.N; s0 += 8) {
+      const int ns = a.N - s0 < 8 ? a.N - s0 : 8;
+      GroupMeta m[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q < ns) m[q] = read_meta(fused_land(a, a.r, s0 + q, j), gl, dc);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (q >= ns) break;
+        const uint8_t* P = fused_land(a, a.r, s0 + q, j);
+#pragma unroll
+        for (int k = 0; k < kFusedMaxG / 32; ++k) {
+          const int e = lane + 32 * k;
+          if (e >= a.G) break;
+          float v;
+          if (dc.sr && e == m[q].imax) v = m[q].smax;  // imax written last (codec.py:559-561)
+          else if (dc.sr && e == m[q].imin) v = m[q].smin;
+          else v = dq32(load_code1(P, a.S, g0 + e, a.B), m[q], dc.intlog);
+          acc[k] = __fadd_rn(acc[k], v);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kFusedMaxG / 32; ++k)
+      if (lane + 32 * k < a.G) sg[lane + 32 * k] = acc[k];
+    __syncwarp();
     OutList o;
     o.nd = 1;
     o.p[0] = result + (int64_t)j * a.slot;
-    generic_encode_group(sum, o, a.S, gl, a.B, a.G, a.sr != 0, cx);
+    generic_encode_group(StagedGroup{sg, g0}, o, a.S, gl, a.B, a.G, a.sr != 0, cx, true);
     __syncwarp();  // the group's planes and record, written by the warp, before the warp reads them back
+    const GroupMeta mr = read_meta(o.p[0], gl, dc);
     for (int e = lane; e < a.G; e += 32) {
-      const int64_t idx = (int64_t)j * a.S + gl * a.G + e;
+      const int64_t idx = (int64_t)j * a.S + g0 + e;
       if (idx >= a.n) break;
-      const uint32_t bits = bf16_bits(decode_elem32(o.p[0], gl * a.G + e, dc));  // bf16 grid (collectives.py:185-186)
+      float v;
+      if (dc.sr && e == mr.imax) v = mr.smax;
+      else if (dc.sr && e == mr.imin) v = mr.smin;
+      else v = dq32(load_code1(o.p[0], a.S, g0 + e, a.B), mr, dc.intlog);
+      const uint32_t bits = bf16_bits(v);  // the bf16 grid (collectives.py:185-186)
       if (a.ydt == FC2_BF16) reinterpret_cast<uint16_t*>(a.y)[idx] = (uint16_t)bits;
       else reinterpret_cast<float*>(a.y)[idx] = bf16_val(bits);
     }
@@ -389,7 +421,7 @@ int fc2_comm_barrier(fc2_comm* c, int32_t* dev_err, double timeout_s, void* stre
   a.epoch = ++c->epoch;
   a.err = dev_err;
   a.timeout_cycles = (long long)(timeout_s * 2.0e9);
-  k_barrier<<<1, 32, 0, (cudaStream_t)stream>>>(a);
+  launch_pdl(k_barrier, 1, 32, 0, (cudaStream_t)stream, a);
   return cuda_check("k_barrier");
 }
 
@@ -510,6 +542,8 @@ int fc2_allreduce_fused(fc2_comm* c, const fc2_config* cfg, const void* x, int32
   if (rc) return rc;
   if ((x_dtype != FC2_BF16 && x_dtype != FC2_F32) || (y_dtype != FC2_BF16 && y_dtype != FC2_F32))
     return set_err(FC2_ECONFIG, "the fused one-shot takes bf16 / f32 tensors");
+  if (cfg->group_size > kFusedMaxG)
+    return set_err(FC2_ECONFIG, "the fused one-shot stages groups of at most %d elements", kFusedMaxG);
   const int64_t mult = (int64_t)N * cfg->group_size;
   const int64_t padded = (n + mult - 1) / mult * mult;
   const int64_t S = padded / N;
@@ -623,14 +657,14 @@ int fc2_allreduce_2step_pipe(fc2_comm* c, const fc2_config* cfg, const void* x, 
     FlagArgs a;
     for (int p = 0; p < N; ++p) a.words[p] = flag(p, stage, r, k);
     a.world = N; a.epoch = epoch; a.err = dev_err; a.timeout_cycles = tmo;
-    k_flag_signal<<<1, 32, 0, s>>>(a);
+    launch_pdl(k_flag_signal, 1, 32, 0, s, a);
     return cuda_check("k_flag_signal");
   };
   auto wait = [&](int stage, int k, cudaStream_t s) {
     FlagArgs a;
     for (int p = 0; p < N; ++p) a.words[p] = flag(r, stage, p, k);
     a.world = N; a.epoch = epoch; a.err = dev_err; a.timeout_cycles = tmo;
-    k_flag_wait<<<1, 32, 0, s>>>(a);
+    launch_pdl(k_flag_wait, 1, 32, 0, s, a);
     return cuda_check("k_flag_wait");
   };
   // the side streams start where the caller's stream is now

@@ -97,6 +97,13 @@ __device__ __forceinline__ double rha(double x) {
 #ifndef FC2_PDL
 #define FC2_PDL 1
 #endif
+// spin-wait kernels: may start early (one CTA parks behind the predecessor)
+// but never release their own dependents early
+__device__ __forceinline__ void pdl_wait_only() {
+#if FC2_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
 __device__ __forceinline__ void pdl_enter() {
 #if FC2_PDL
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -137,9 +144,10 @@ inline void launch_pdl(K kern, unsigned grid, unsigned block, int smem, cudaStre
 #endif
 }
 
-// (every kernel launched through launch_pdl must begin with pdl_enter).  The
-// communicator's spin-wait kernels (k_barrier, k_flag_wait / k_flag_signal)
-// are launched normally and never release their dependents early: a
+// (every kernel launched through launch_pdl must begin with pdl_enter or
+// pdl_wait_only).  The communicator's spin-wait kernels (k_barrier,
+// k_flag_wait / k_flag_signal) use pdl_wait_only: they never release their
+// dependents early: a
 // dependent grid launched early parks its CTAs in griddepcontrol.wait, and
 // behind a kernel that waits for another stream or a peer those parked CTAs
 // can take the SM slots that stream / peer needs (a deadlock observed with

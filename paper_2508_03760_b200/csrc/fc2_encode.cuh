@@ -422,9 +422,20 @@ __device__ __forceinline__ void out_record(const OutList& o, int64_t off, const 
 
 // Encode group `gi` of a chunk with one full warp.  `ld(i)` returns element i
 // of the chunk as a double (zero padding included).
+// est: codes from the fp32 fixed-point estimate with the exact float64
+// recompute only for near ties (the fast kernels' contract, same bits); off:
+// every code in float64.
+template <class Loader>
+__device__ void generic_encode_group(const Loader& ld, const OutList& out, int64_t n, int64_t gi,
+                                     int B, int G, bool sr, const EncCtx& cx, bool est);
 template <class Loader>
 __device__ void generic_encode_group(const Loader& ld, const OutList& out, int64_t n, int64_t gi,
                                      int B, int G, bool sr, const EncCtx& cx) {
+  generic_encode_group(ld, out, n, gi, B, G, sr, cx, false);
+}
+template <class Loader>
+__device__ void generic_encode_group(const Loader& ld, const OutList& out, int64_t n, int64_t gi,
+                                     int B, int G, bool sr, const EncCtx& cx, bool est) {
   const int lane = (int)lane_id();
   const int L = (1 << B) - 1;
   const int64_t g0 = gi * (int64_t)G;
@@ -466,6 +477,8 @@ __device__ void generic_encode_group(const Loader& ld, const OutList& out, int64
   }
   GroupParams p = group_params(zero, vmax, L, cx.intlog != 0, cx.theta, cx.lut, lane == 0 ? cx.err : nullptr);
   const int sc = sr ? exact_code(0.0, p.off, p.div, L) : 0;
+  const bool fast = est && !p.exact;
+  const float Lh = (float)L + 0.5f;
   // codes: lane handles runs of 8 consecutive elements -> W bytes per unit
   const int nu = n_units(B);
   for (int e = lane * 8; e < G; e += 256) {
@@ -473,7 +486,17 @@ __device__ void generic_encode_group(const Loader& ld, const OutList& out, int64
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int idx = e + j;
-      c[j] = (sr && (idx == imin || idx == imax)) ? sc : exact_code(ld(g0 + idx), p.off, p.div, L);
+      if (sr && (idx == imin || idx == imax)) {
+        c[j] = sc;
+      } else {
+        const double v = ld(g0 + idx);
+        if (fast) {  // estimate within 2.5 ulp of 2^-14; near ties go float64
+          const uint32_t X = fix_est_clamped((float)v, p.off32, p.inv32, Lh);
+          c[j] = fix_is_tie(X) ? exact_code(v, p.off, p.div, L) : (int)((X >> kFixBits) & 0xFFu);
+        } else {
+          c[j] = exact_code(v, p.off, p.div, L);
+        }
+      }
     }
     for (int u = 0; u < nu; ++u) {
       const int W = unit_w(B, u), O = unit_off(B, u);
