@@ -1020,6 +1020,7 @@ def run_multi(args, rank, world, local_rank):
             "data": "synthetic spiky bf16 per rank (N(0,1), 1/64 at +-50)",
             "config": config_for(args, world),
             "b3": {"ms": round(ms_b3, 5), "algbw_GBps": round(2 * n / (ms_b3 * 1e-3) / 1e9, 2)},
+            "auto_algorithm": {f"n={k[0]} b{k[1]}": v for k, v in comm._tuned.items()},
             "pipelined": {"ms": round(ms_pipe, 5), "chunks": comm.pipe_chunks,
                           "algbw_GBps": round(2 * n / (ms_pipe * 1e-3) / 1e9, 2)},
             "nccl_bf16": None if ts_nccl is None else {

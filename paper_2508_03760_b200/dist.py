@@ -186,6 +186,11 @@ class QComm:
         self.os_off = self.a2a_off + self.a2a_bytes
         # pipelined two-step region: 2 parity sets x (land + gath) x N x chunks slots
         self.pipe_chunks = max(1, min(16, int(pipe_chunks)))
+        # algo="auto" above the one-shot size: two-step or pipelined, whichever
+        # the first call of a (size, codec) measured faster on this box (max
+        # over ranks, so every rank picks the same one)
+        self.autotune = True
+        self._tuned: dict = {}
         sk = pipe_chunk_len(self.max_lay.shard_len, self.pipe_chunks, self.cfg.group_size)
         self.pipe_chunk_bytes = _round_up(max(footprint_bytes(self.cfg, sk), 1), _SLOT_ALIGN)
         self.pipe_bytes = 4 * self.world * self.pipe_chunks * self.pipe_chunk_bytes
@@ -238,7 +243,8 @@ class QComm:
         one-shot as one cooperative kernel with in-kernel flags),
         ``"pipelined"`` (microchunked two-step on three streams), or
         ``"auto"`` (one-shot up to ``oneshot_max_elems`` on the ipc
-        transport, else two-step).  ``config``
+        transport; above it two-step or pipelined, whichever the first call
+        of that size measured faster, agreed over the ranks).  ``config``
         overrides the communicator's codec for this call when its packed
         shards fit the communicator's slots (e.g. fewer bits)."""
         cfg = self.cfg if config is None else config
@@ -279,6 +285,14 @@ class QComm:
             if check:
                 self.check()
             return y
+        if (algo == "auto" and self.autotune and self.transport == "ipc" and self.world > 1
+                and n > self.os_lay.n):
+            key = (n, cfg.bitwidth, cfg.group_size, cfg.scheme, cfg.scale_encoding, cfg.theta, x.dtype, y.dtype)
+            if key not in self._tuned:
+                self._tuned[key] = self._tune(x, y, cfg)
+            algo = self._tuned[key]
+            if algo == "pipelined":
+                return self.all_reduce(x, out=y, check=check, algo="pipelined", config=config)
         one = self.transport == "ipc" and n <= self.os_lay.n and algo != "two_step"
         if algo == "one_shot" and not one:
             raise ConfigError("one_shot needs the ipc transport and n <= oneshot_max_elems")
@@ -300,6 +314,26 @@ class QComm:
         if check:
             self.check()
         return y
+
+    def _tune(self, x: torch.Tensor, y: torch.Tensor, cfg: QuantConfig) -> str:
+        """Time the two large-message algorithms on this call's own buffers (each
+        result is the same bits, so the caller's output is valid whichever ran
+        last) and agree on the faster one across ranks."""
+        algos = ("two_step", "pipelined")
+        ts = []
+        for a in algos:
+            self.all_reduce(x, out=y, algo=a, config=cfg)  # warm
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            self.all_reduce(x, out=y, algo=a, config=cfg)
+            e.record()
+            e.synchronize()
+            ts.append(s.elapsed_time(e))
+        dev = self.device if dist.get_backend(self.group) == "nccl" else torch.device("cpu")
+        t = torch.tensor(ts, dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        t = t.cpu().tolist()
+        return algos[int(t[1] < t[0])]
 
     def all2all(self, x: torch.Tensor, matrix, out: torch.Tensor | None = None,
                 out_dtype: torch.dtype = torch.float32, check: bool = False) -> torch.Tensor:

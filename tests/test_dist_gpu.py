@@ -86,7 +86,16 @@ def _worker(rank, world, port, case, q):
                     comm.all_reduce(xs[i % 3], out=y, algo=algo)
                 comm.check()
                 outs.append(y.float().cpu().numpy().tobytes())
-            q.put((rank, outs))
+            comm.close()
+            # algo="auto" above the one-shot size: the first call of the size
+            # times two-step and pipelined and every rank adopts the same one
+            comm = QComm(max_elems=n, config=cfg, timeout_s=60.0, oneshot_max_elems=1024, pipe_chunks=4)
+            y = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+            for i in range(12):
+                comm.all_reduce(xs[i % 3], out=y)
+            comm.check()
+            outs.append(y.float().cpu().numpy().tobytes())
+            q.put((rank, outs + [list(comm._tuned.values())]))
         elif kind == "a2a_errors":
             # (1) blocks that do not fit the All2All region -> ConfigError (the
             # one-shot region behind it must never be overwritten); (2) NaN in
@@ -164,8 +173,10 @@ def test_ipc_back_to_back_calls(world, n):
         payloads.append(O.bf16_snap(O.spiky(n, O.child_seeds(31 + r, 3)[2])).astype(np.float32))
     want, _ = O.two_step(payloads, 4, 128, True)
     for r in range(world):
-        for blob in got[r]:
+        *blobs, chosen = got[r]
+        for blob in blobs:
             assert np.array_equal(np.frombuffer(blob, dtype=np.float32), want[0])
+        assert len(chosen) == 1 and chosen[0] in ("two_step", "pipelined") and chosen == got[0][-1]
 
 
 @pytest.mark.parametrize("world", [2, 3, 8])
