@@ -242,9 +242,10 @@ class QComm:
         barriers for latency-bound sizes, same bits), ``"fused"`` (the
         one-shot as one cooperative kernel with in-kernel flags),
         ``"pipelined"`` (microchunked two-step on three streams), or
-        ``"auto"`` (one-shot up to ``oneshot_max_elems`` on the ipc
-        transport; above it two-step or pipelined, whichever the first call
-        of that size measured faster, agreed over the ranks).  ``config``
+        ``"auto"`` (on the ipc transport: up to ``oneshot_max_elems`` the
+        one-shot or its fused form, above it the two-step or the pipelined
+        two-step -- whichever the first call of that size measured faster,
+        agreed over the ranks).  ``config``
         overrides the communicator's codec for this call when its packed
         shards fit the communicator's slots (e.g. fewer bits)."""
         cfg = self.cfg if config is None else config
@@ -285,14 +286,18 @@ class QComm:
             if check:
                 self.check()
             return y
-        if (algo == "auto" and self.autotune and self.transport == "ipc" and self.world > 1
-                and n > self.os_lay.n):
-            key = (n, cfg.bitwidth, cfg.group_size, cfg.scheme, cfg.scale_encoding, cfg.theta, x.dtype, y.dtype)
-            if key not in self._tuned:
-                self._tuned[key] = self._tune(x, y, cfg)
-            algo = self._tuned[key]
-            if algo == "pipelined":
-                return self.all_reduce(x, out=y, check=check, algo="pipelined", config=config)
+        if algo == "auto" and self.autotune and self.transport == "ipc" and self.world > 1:
+            small = n <= self.os_lay.n
+            cands = (("one_shot", "fused") if x.dtype in (torch.bfloat16, torch.float32)
+                     and y.dtype in (torch.bfloat16, torch.float32) and cfg.group_size <= 256
+                     else ("one_shot",)) if small else ("two_step", "pipelined")
+            if len(cands) > 1:
+                key = (n, cfg.bitwidth, cfg.group_size, cfg.scheme, cfg.scale_encoding, cfg.theta, x.dtype, y.dtype)
+                if key not in self._tuned:
+                    self._tuned[key] = self._tune(x, y, cfg, cands)
+                algo = self._tuned[key]
+                if algo in ("pipelined", "fused"):
+                    return self.all_reduce(x, out=y, check=check, algo=algo, config=config)
         one = self.transport == "ipc" and n <= self.os_lay.n and algo != "two_step"
         if algo == "one_shot" and not one:
             raise ConfigError("one_shot needs the ipc transport and n <= oneshot_max_elems")
@@ -315,11 +320,10 @@ class QComm:
             self.check()
         return y
 
-    def _tune(self, x: torch.Tensor, y: torch.Tensor, cfg: QuantConfig) -> str:
-        """Time the two large-message algorithms on this call's own buffers (each
-        result is the same bits, so the caller's output is valid whichever ran
-        last) and agree on the faster one across ranks."""
-        algos = ("two_step", "pipelined")
+    def _tune(self, x: torch.Tensor, y: torch.Tensor, cfg: QuantConfig, algos) -> str:
+        """Time the candidate algorithms on this call's own buffers (each result
+        is the same bits, so the caller's output is valid whichever ran last)
+        and agree on the fastest across ranks."""
         ts = []
         for a in algos:
             self.all_reduce(x, out=y, algo=a, config=cfg)  # warm
@@ -333,7 +337,7 @@ class QComm:
         t = torch.tensor(ts, dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
         t = t.cpu().tolist()
-        return algos[int(t[1] < t[0])]
+        return algos[min(range(len(algos)), key=lambda i: t[i])]
 
     def all2all(self, x: torch.Tensor, matrix, out: torch.Tensor | None = None,
                 out_dtype: torch.dtype = torch.float32, check: bool = False) -> torch.Tensor:

@@ -46,7 +46,7 @@ def _worker(rank, world, port, case, q):
             # both algorithms, both output types; the one-shot runs three times
             # so both landing buffers (call parity) are exercised
             for algo in ("two_step", "one_shot", "one_shot", "one_shot", "pipelined", "pipelined", "pipelined",
-                         "fused", "one_shot", "fused", "fused"):
+                         "fused", "one_shot", "fused", "fused", "auto", "auto"):
                 for dt in (torch.float32, torch.bfloat16):
                     y = comm.all_reduce(x.to(dt), check=True, algo=algo)
                     outs.append(y.float().cpu().numpy().tobytes())
@@ -177,6 +177,7 @@ def test_ipc_back_to_back_calls(world, n):
         for blob in blobs:
             assert np.array_equal(np.frombuffer(blob, dtype=np.float32), want[0])
         assert len(chosen) == 1 and chosen[0] in ("two_step", "pipelined") and chosen == got[0][-1]
+    # the small-message choice (one-shot / fused) is exercised by the allreduce case's "auto" calls
 
 
 @pytest.mark.parametrize("world", [2, 3, 8])
