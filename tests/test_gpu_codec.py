@@ -68,10 +68,37 @@ def tie_heavy(n, seed):
     return (rng.integers(-64, 64, n) / 8.0).astype(np.float32)
 
 
+def stress(n, seed, g=32):
+    """Every group of g (the smallest group size of a test: coarser groups mix
+    regimes) drawn from a different regime that exercises a separate branch
+    of the fast kernels: large offsets (explicit v - off form), tiny and huge
+    ranges (the all-float64 path), constant groups (scale 0), many copies of
+    both extremes (spike occurrence counting), one-signed groups (the
+    reserved-slot stand-in), subnormals, exact-integer grids (near ties)."""
+    rng = np.random.default_rng(seed)
+    out = np.empty(n, dtype=np.float64)
+    regimes = [
+        lambda k: rng.normal(0, 1, k),
+        lambda k: 1000.0 + rng.normal(0, 1, k),
+        lambda k: rng.normal(0, 1e-33, k),
+        lambda k: rng.normal(0, 1e30, k),
+        lambda k: np.full(k, rng.normal()),
+        lambda k: rng.choice([-3.0, 3.0, 0.5], size=k, p=[0.3, 0.3, 0.4]),
+        lambda k: np.abs(rng.normal(5, 1, k)) + 1.0,
+        lambda k: -np.abs(rng.normal(5, 1, k)) - 1.0,
+        lambda k: rng.normal(0, 1e-39, k),
+        lambda k: rng.integers(-40, 40, k) / 4.0,
+    ]
+    for i in range(0, n, g):
+        out[i:i + g] = regimes[rng.integers(len(regimes))](min(g, n - i))
+    return O.bf16_snap(out.astype(np.float32)).astype(np.float32)
+
+
 INPUTS = {
     "spiky": lambda n, s: O.bf16_snap(O.spiky(n, s)).astype(np.float32),
     "ties": tie_heavy,
     "gauss_f32": lambda n, s: np.random.default_rng(s).normal(0, 1, n).astype(np.float32),
+    "stress": stress,
 }
 
 
@@ -93,7 +120,7 @@ def test_codec_matches_oracle_random(bits, sr, g, kind):
 @pytest.mark.parametrize("bits", range(2, 9))
 @pytest.mark.parametrize("sr", [False, True])
 @pytest.mark.parametrize("g", [32, 64, 128, 256])
-@pytest.mark.parametrize("kind", ["spiky", "ties"])
+@pytest.mark.parametrize("kind", ["spiky", "ties", "stress"])
 def test_codec_bf16_device_matches_oracle(bits, sr, g, kind):
     """The bf16 lane-per-group encoder (k_encode_grp) in its small-chunk
     shape (one 32-element run per lane) against the oracle, every g."""
@@ -145,6 +172,22 @@ def test_codec_intlog_matches_oracle(bits, sr):
     planes, meta = O.encode(x, bits, 128, sr, intlog=True)
     assert chunk.planes == planes and chunk.meta == meta
     assert np.array_equal(fc.decode_chunk(chunk), O.decode(planes, meta, n, bits, 128, sr, intlog=True))
+
+
+@pytest.mark.parametrize("bits,sr,g", [(4, True, 128), (3, True, 128), (8, True, 128), (2, False, 128),
+                                        (5, True, 64), (4, True, 256), (6, False, 32)])
+def test_codec_bf16_bandwidth_shape_stress(bits, sr, g):
+    """The bandwidth shape of k_encode_grp (and k_decode_fast) on the stress
+    mix, whole payload and decoded values against the oracle."""
+    n = 1 << 22  # above the small-chunk crossover: bandwidth tiles
+    x = stress(n, 97 + bits + g, g)
+    cfg = cfg_of(bits, g, sr, False, n)
+    xd = torch.from_numpy(x).cuda().to(torch.bfloat16)
+    pay = fc.encode_payload(xd, cfg, n)
+    planes, meta = O.encode(x, bits, g, sr)
+    assert np.array_equal(pay.cpu().numpy(), np.frombuffer(b"".join(planes) + meta, dtype=np.uint8))
+    dec = fc.decode_payload(pay, cfg, n, out_dtype=torch.float32).cpu().numpy()
+    assert np.array_equal(dec, O.decode(planes, meta, n, bits, g, sr).astype(np.float32))
 
 
 def test_codec_f64_inputs_are_exact():
