@@ -55,6 +55,19 @@ def test_two_step_matches_oracle(N, n, bits, g, sr):
     assert np.array_equal(res.outputs[0], want[0])
 
 
+@pytest.mark.parametrize("N,bits,g,sr", [(8, 4, 128, True), (4, 3, 64, True), (8, 8, 128, True), (2, 2, 32, False)])
+def test_two_step_stress_matches_oracle(N, bits, g, sr):
+    """The stage-2 reducer on the stress mix (tests/test_gpu_codec.py): sums of
+    groups from different regimes across ranks, requantized."""
+    from tests.test_gpu_codec import stress
+
+    n = N * g * 2048  # the fast stage-2 shape (1024-element tiles, 16-byte aligned slots)
+    payloads = [stress(n, 500 + r, g) for r in range(N)]
+    res = fc.two_step_allreduce_q(payloads, fc.preset("B200", N), cfg(bits, g, sr))
+    want, _ = O.two_step(payloads, bits, g, sr)
+    assert np.array_equal(res.outputs[0], want[0])
+
+
 def test_two_step_nonfinite_raises():
     payloads = [np.ones(4096, np.float32) for _ in range(4)]
     payloads[2][100] = np.nan
