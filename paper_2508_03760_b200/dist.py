@@ -325,6 +325,12 @@ class QComm:
         is the same bits, so the caller's output is valid whichever ran last)
         and agree on the fastest across ranks."""
         ts = []
+        # in-place calls (out aliases x): the timed runs write a private output,
+        # so the caller's input is intact for the call that follows
+        xs, xe = x.data_ptr(), x.data_ptr() + x.numel() * x.element_size()
+        ys, ye = y.data_ptr(), y.data_ptr() + y.numel() * y.element_size()
+        if xs < ye and ys < xe:
+            y = torch.empty_like(y)
         for a in algos:
             self.all_reduce(x, out=y, algo=a, config=cfg)  # warm
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -95,6 +95,12 @@ def _worker(rank, world, port, case, q):
                 comm.all_reduce(xs[i % 3], out=y)
             comm.check()
             outs.append(y.float().cpu().numpy().tobytes())
+            # in place (NCCL's default form): the first call of a new size tunes
+            # on a private copy, so the result is still one reduction of the input
+            xin = xs[2][: n // 2].clone()
+            half = comm.all_reduce(xin, out=xin)
+            comm.check()
+            outs.append(half.float().cpu().numpy().tobytes())
             q.put((rank, outs + [list(comm._tuned.values())]))
         elif kind == "a2a_errors":
             # (1) blocks that do not fit the All2All region -> ConfigError (the
@@ -172,11 +178,14 @@ def test_ipc_back_to_back_calls(world, n):
     for r in range(world):
         payloads.append(O.bf16_snap(O.spiky(n, O.child_seeds(31 + r, 3)[2])).astype(np.float32))
     want, _ = O.two_step(payloads, 4, 128, True)
+    want_half, _ = O.two_step([p[: n // 2] for p in payloads], 4, 128, True)
     for r in range(world):
-        *blobs, chosen = got[r]
+        *blobs, inplace, chosen = got[r]
         for blob in blobs:
             assert np.array_equal(np.frombuffer(blob, dtype=np.float32), want[0])
-        assert len(chosen) == 1 and chosen[0] in ("two_step", "pipelined") and chosen == got[0][-1]
+        assert np.array_equal(np.frombuffer(inplace, dtype=np.float32), want_half[0])
+        # one choice per tuned size (n, n / 2), the same on every rank
+        assert len(chosen) == 2 and set(chosen) <= {"two_step", "pipelined"} and chosen == got[0][-1]
     # the small-message choice (one-shot / fused) is exercised by the allreduce case's "auto" calls
 
 
