@@ -257,7 +257,11 @@ class QComm:
         n = x.numel()
         if n > self.max_lay.n:
             raise DataError(f"payload of {n} elements exceeds the communicator's {self.max_lay.n}")
-        y = out if out is not None else torch.empty(n, dtype=x.dtype, device=x.device)
+        if x.device != self.device:
+            raise ConfigError(f"input on {x.device}, communicator on {self.device}")
+        if out is not None and (out.device != self.device or not out.is_contiguous() or out.numel() != n):
+            raise ConfigError(f"out must be a contiguous {n}-element tensor on {self.device}")
+        y = out.reshape(-1) if out is not None else torch.empty(n, dtype=x.dtype, device=x.device)
         lay = TwoStepLayout.make(n, self.world, cfg)
         if algo not in ("auto", "two_step", "one_shot", "pipelined", "fused"):
             raise ConfigError(f"unknown allreduce algorithm {algo!r}")
