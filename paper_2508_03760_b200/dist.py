@@ -366,6 +366,8 @@ class QComm:
         if int(m[r].sum()) != x.numel():
             raise ConfigError("dispatch row does not match the payload size")
         n_out = int(m[:, r].sum())
+        if out is not None and (out.device != self.device or not out.is_contiguous() or out.numel() != n_out):
+            raise ConfigError(f"out must be a contiguous {n_out}-element tensor on {self.device}")
         y = out if out is not None else torch.empty(n_out, dtype=out_dtype, device=x.device)
         x = x.reshape(-1).contiguous()
         c = self.cfg.c_struct()
@@ -431,6 +433,8 @@ class QComm:
         y = y.contiguous()
         if y.dim() != 2 or y.shape[1] != H or y.shape[0] != int(tm[:, r].sum()):
             raise ConfigError(f"expert outputs must be [{int(tm[:, r].sum())}, {H}], got {tuple(y.shape)}")
+        if out is not None and (out.device != self.device or not out.is_contiguous() or out.numel() != T * H):
+            raise ConfigError(f"out must be a contiguous [{T}, {H}] tensor on {self.device}")
         res = out if out is not None else torch.empty((T, H), dtype=out_dtype, device=self.device)
         scratch = _device.workspace("moe_scratch", max(16, 4 * int(tm[r].sum()) * H), self.device)
         c = self.cfg.c_struct()
