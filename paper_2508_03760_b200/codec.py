@@ -189,8 +189,13 @@ def encode_payload(x: torch.Tensor, config: QuantConfig, n: int | None = None,
     nv = x.numel()
     n = nv if n is None else int(n)
     nbytes = footprint_bytes(config, n)
+    if n < nv:
+        raise ConfigError(f"chunk of {n} elements cannot hold {nv} values")
     if out is None:
         out = torch.empty(nbytes, dtype=torch.uint8, device=x.device)
+    elif (out.device != x.device or out.dtype != torch.uint8 or not out.is_contiguous()
+          or out.numel() < nbytes):
+        raise ConfigError(f"payload buffer must be a contiguous uint8 tensor of >= {nbytes} bytes on {x.device}")
     own_err = err is None
     if own_err:
         err = _device.new_err(x.device)
@@ -212,8 +217,15 @@ def decode_payload(payload: torch.Tensor, config: QuantConfig, n: int,
     if config.int_log:
         _device.ensure_intlog(config.theta, dev)
     n_out = n if n_out is None else int(n_out)
+    need = footprint_bytes(config, n)
+    if payload.dtype != torch.uint8 or not payload.is_contiguous() or payload.numel() < need:
+        raise ConfigError(f"payload must be a contiguous uint8 tensor of >= {need} bytes")
+    if n_out > n:
+        raise ConfigError(f"n_out {n_out} exceeds the chunk's {n} elements")
     if out is None:
         out = torch.empty(n_out, dtype=out_dtype, device=payload.device)
+    elif out.device != payload.device or not out.is_contiguous() or out.numel() < n_out:
+        raise ConfigError(f"out must be a contiguous tensor of >= {n_out} elements on {payload.device}")
     own_err = err is None
     if own_err:
         err = _device.new_err(payload.device)

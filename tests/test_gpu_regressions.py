@@ -87,3 +87,24 @@ def test_all2all_nonfinite_anywhere_raises(where):
     blocks[src][dst][3] = np.inf
     with pytest.raises(fc.DataError):
         fc.all2all_combine_q(blocks, fc.preset("B200", N), cfg(4, 128, True))
+
+
+def test_payload_buffer_validation():
+    """Caller-provided buffers that are too small, of the wrong dtype or
+    non-contiguous raise ConfigError instead of being overrun."""
+    cfg = fc.QuantConfig(4, group_size=128, chunk_size=128)
+    x = torch.zeros(1024, dtype=torch.bfloat16, device="cuda")
+    F = fc.footprint_bytes(cfg, 1024)
+    with pytest.raises(fc.ConfigError):
+        fc.encode_payload(x, cfg, 1024, out=torch.empty(F - 1, dtype=torch.uint8, device="cuda"))
+    with pytest.raises(fc.ConfigError):
+        fc.encode_payload(x, cfg, 1024, out=torch.empty(F, dtype=torch.int32, device="cuda"))
+    with pytest.raises(fc.ConfigError):
+        fc.encode_payload(x, cfg, 512)
+    pay = fc.encode_payload(x, cfg, 1024)
+    with pytest.raises(fc.ConfigError):
+        fc.decode_payload(pay[:-1], cfg, 1024)
+    with pytest.raises(fc.ConfigError):
+        fc.decode_payload(pay, cfg, 1024, out=torch.empty(1023, device="cuda"))
+    with pytest.raises(fc.ConfigError):
+        fc.decode_payload(pay, cfg, 1024, out=torch.empty(2048, device="cuda")[::2])
