@@ -66,6 +66,9 @@ __device__ __forceinline__ uint32_t route_mask(const void* ids, int idx64, int64
   return m;
 }
 
+#ifndef FC2_COMBINE_MINB
+#define FC2_COMBINE_MINB 2
+#endif
 constexpr int kRouteChunk = 8192;  // tokens whose masks the routing CTA stages at once (32 KB of smem)
 
 // pass 1, all SMs: mask of every token, parked in pos[t * world] (pass 2
@@ -298,7 +301,7 @@ struct CombineSrc {
 };
 
 template <int B>
-__global__ void __launch_bounds__(256, 2) k_moe_combine_q(const __grid_constant__ CombineQArgs a) {
+__global__ void __launch_bounds__(256, FC2_COMBINE_MINB) k_moe_combine_q(const __grid_constant__ CombineQArgs a) {
   __shared__ __align__(16) float spill_all[8][32][36];
   const int warp = (int)(threadIdx.x >> 5), lane = (int)(threadIdx.x & 31);
   float* spill = spill_all[warp][lane];
