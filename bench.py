@@ -842,6 +842,9 @@ def run_multi(args, rank, world, local_rank):
     # (64 MiB in + 64 MiB out per step already exceed L2)
     xr = [x] + [spiky_bf16(n, 1000 + 97 * k + rank, dev) for k in range(1, ROTATE)]
 
+    lib = fc._lib.lib()
+    region_launches = [0]
+
     def region(fn, steps, warmup):
         """The contract's form: warm-up, then exactly `steps` calls bracketed by
         barrier + synchronize and one CUDA-event pair; per-step ms = region /
@@ -852,22 +855,22 @@ def run_multi(args, rank, world, local_rank):
         dist.barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda._sleep(int(steps * 200e-6 * 2.0e9))  # GPU busy while the host enqueues the region
+        l_start = lib.fc2_launch_count()
         a.record()
         for i in range(steps):
             fn(i)
         b.record()
+        region_launches[0] = lib.fc2_launch_count() - l_start  # this library's kernels in the region
         torch.cuda.synchronize()
         t = torch.tensor([a.elapsed_time(b) / steps], device=tdev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.barrier()
         return float(t.item())
 
-    lib = fc._lib.lib()
     # ---- headline: configs[2] two-step AllReduce through the public API
-    l0 = lib.fc2_launch_count()
     with ClockSampler(dev.index) as clk:
         ms = region(lambda i: comm.all_reduce(xr[i % ROTATE], out=y), args.steps, args.warmup)
-    launches = (lib.fc2_launch_count() - l0) // max(1, args.steps + args.warmup)
+    launches = region_launches[0]
     ts_main = timed(lambda: comm.all_reduce(x, out=y), args.steps, args.warmup)  # per-step view
 
     def stage_ok(name):
