@@ -582,12 +582,12 @@ int fc2_allreduce_fused(fc2_comm* c, const fc2_config* cfg, const void* x, int32
   const int64_t cap = (int64_t)per_sm * num_sms();
   if (grid > cap) grid = cap;
   if (grid < 1) grid = 1;
-  c->fused_arrivals += (uint32_t)grid;
-  a.gtarget = c->fused_arrivals;
+  a.gtarget = c->fused_arrivals + (uint32_t)grid;  // committed only once the launch is accepted
   void* args[] = {&a};
   if (cudaLaunchCooperativeKernel((const void*)k_allreduce_fused, dim3((unsigned)grid), dim3(256), args, 0,
                                   (cudaStream_t)stream) != cudaSuccess)
     return cuda_check("k_allreduce_fused (cooperative launch)");
+  c->fused_arrivals = a.gtarget;
   return cuda_check("k_allreduce_fused");
 }
 
