@@ -170,7 +170,7 @@ def test_ipc_two_step_matches_reference_algorithm(world, n, bits, g, sr):
 
 
 @pytest.mark.timeout(900)
-@pytest.mark.parametrize("world,n", [(2, 1 << 20), (4, 3 << 16)])
+@pytest.mark.parametrize("world,n", [(2, 1 << 20), (4, 3 << 16), (8, 1 << 16)])
 def test_ipc_back_to_back_calls(world, n):
     got = _run(world, ("back_to_back", n, 4, 128, True, 31))
     # call 11 used input set 11 % 3 = 2 on every rank
