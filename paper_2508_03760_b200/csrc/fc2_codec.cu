@@ -686,6 +686,10 @@ static int host_pipeline(int mode, const fc2_config* cfg, const void* x_host, in
   HostPipe* hp = host_pipe(&rc);
   if (rc) return rc;
   NoPdl no_pdl;  // kernels here follow cross-stream event waits
+  // the per-device pipeline streams and events are shared: one host thread
+  // enqueues a pipeline at a time (the enqueue is short; the work stays async)
+  static std::mutex pipe_mu;
+  std::lock_guard<std::mutex> pipe_lk(pipe_mu);
   cudaStream_t st = (cudaStream_t)stream;
   if (cudaEventRecord(hp->fork, st) != cudaSuccess) return set_err(FC2_ECUDA, "fork event failed");
   for (int i = 0; i < kPipeStreams; ++i) cudaStreamWaitEvent(hp->s[i], hp->fork, 0);
