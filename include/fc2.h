@@ -7,6 +7,12 @@
  * report data-dependent errors through a caller-owned device int32 word
  * (`dev_err`, bit mask FC2_ERR_*) that the host checks when it wants to.
  *
+ * Threading: the codec entry points may be called from several host threads
+ * (the host-resident pipelines serialize their enqueues internally).  A
+ * communicator (fc2_comm) is driven by one host thread, and every rank must
+ * issue the same sequence of collective calls on it (ranks synchronize through
+ * flags in each other's buffers).
+ *
  * Each entry point names the reference interface it replaces (paths relative
  * to /root/reference/pkg/src/qcomm).  The reference is a pure Python+numpy
  * package with no FFI; the binding a maintainer would add is the ctypes stub
