@@ -19,6 +19,7 @@
 //                   278-392, bfloat16.py:16-36.
 // Host-resident chunks (fc2_*_host) are sliced and pipelined over internal
 // streams (see host_pipeline below).
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <utility>
@@ -603,6 +604,33 @@ constexpr int kPipeEvents = 8;
 #ifndef FC2_PIPE_PAYLOAD_LAST
 #define FC2_PIPE_PAYLOAD_LAST 1
 #endif
+#ifndef FC2_PIPE_TRACE
+#define FC2_PIPE_TRACE 0  // dev builds: print a timing-event timeline of every host pipeline call
+#endif
+struct PipeTrace {
+  std::vector<std::pair<cudaEvent_t, std::string>> ev;
+  std::vector<double> host_us;
+  void mark(cudaStream_t s, const char* what, int64_t k) {
+    if (!FC2_PIPE_TRACE) return;
+    host_us.push_back(std::chrono::duration<double, std::micro>(
+        std::chrono::steady_clock::now().time_since_epoch()).count());
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    ev.emplace_back(e, std::string(what) + " " + std::to_string(k));
+  }
+  void dump(cudaStream_t st) {
+    if (!FC2_PIPE_TRACE || ev.empty()) return;
+    cudaStreamSynchronize(st);
+    for (size_t i = 0; i < ev.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[0].first, ev[i].first);
+      fprintf(stderr, "[pipe] gpu %8.1f us  host %8.1f us  %s\n", ms * 1e3f, host_us[i] - host_us[0],
+              ev[i].second.c_str());
+    }
+    for (auto& x : ev) cudaEventDestroy(x.first);
+  }
+};
 struct HostPipe {
   cudaStream_t s[kPipeStreams];
   cudaEvent_t fork, join[kPipeStreams], up[kPipeEvents], dn[kPipeEvents];
@@ -691,6 +719,8 @@ static int host_pipeline(int mode, const fc2_config* cfg, const void* x_host, in
   static std::mutex pipe_mu;
   std::lock_guard<std::mutex> pipe_lk(pipe_mu);
   cudaStream_t st = (cudaStream_t)stream;
+  PipeTrace tr;
+  tr.mark(st, "fork", 0);
   if (cudaEventRecord(hp->fork, st) != cudaSuccess) return set_err(FC2_ECUDA, "fork event failed");
   for (int i = 0; i < kPipeStreams; ++i) cudaStreamWaitEvent(hp->s[i], hp->fork, 0);
   const int xs = esize(x_dtype), ys = esize(y_dtype);
@@ -711,13 +741,16 @@ static int host_pipeline(int mode, const fc2_config* cfg, const void* x_host, in
         rc = copy_payload_slice(cfg, n, e0, e1, pay_dev, pay_host, cudaMemcpyHostToDevice, up);
         if (rc) return rc;
       }
+      tr.mark(up, "up_done", k);
       cudaEvent_t ev = hp->up[k % kPipeEvents];
       if (cudaEventRecord(ev, up) != cudaSuccess || cudaStreamWaitEvent(s, ev, 0) != cudaSuccess)
         return set_err(FC2_ECUDA, "upload event failed");
     }
+    tr.mark(s, "kern_start", k);
     if (mode & 1) {
       rc = encode_batch_impl(cfg, x_dtype, 1, &x_dev, &n, &n, &pay_dev, dev_err, s, &e0, &e1);
       if (rc) return rc;
+      tr.mark(s, "enc_done", k);
     }
     if (mode & 8) {
       const void* pd = pay_dev;
@@ -725,6 +758,7 @@ static int host_pipeline(int mode, const fc2_config* cfg, const void* x_host, in
       if (rc) return rc;
     }
     if (mode & 10) {
+      tr.mark(s, "kern_done", k);
       cudaEvent_t ev = hp->dn[k % kPipeEvents];
       if (cudaEventRecord(ev, s) != cudaSuccess || cudaStreamWaitEvent(down, ev, 0) != cudaSuccess)
         return set_err(FC2_ECUDA, "download event failed");
@@ -735,6 +769,7 @@ static int host_pipeline(int mode, const fc2_config* cfg, const void* x_host, in
       if ((mode & 8) && cudaMemcpyAsync((uint8_t*)y_host + e0 * ys, (const uint8_t*)y_dev + e0 * ys,
                                         (e1 - e0) * ys, cudaMemcpyDeviceToHost, down) != cudaSuccess)
         return set_err(FC2_ECUDA, "y slice copy failed");
+      tr.mark(down, "down_done", k);
     }
   }
   // round trip: the payload comes back in one copy per plane + one for the
@@ -742,11 +777,14 @@ static int host_pipeline(int mode, const fc2_config* cfg, const void* x_host, in
   if (FC2_PIPE_PAYLOAD_LAST && (mode & 2) && (mode & 8)) {
     rc = copy_payload_slice(cfg, n, 0, n, pay_dev, pay_host, cudaMemcpyDeviceToHost, down);
     if (rc) return rc;
+    tr.mark(down, "payload_done", 0);
   }
   for (int i = 0; i < kPipeStreams; ++i) {
     cudaEventRecord(hp->join[i], hp->s[i]);
     cudaStreamWaitEvent(st, hp->join[i], 0);
   }
+  tr.mark(st, "join", 0);
+  tr.dump(st);
   return cuda_check("host pipeline");
 }
 

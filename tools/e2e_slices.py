@@ -14,7 +14,8 @@ xh = spiky_bf16(n, 0, torch.device("cuda")).cpu().pin_memory()
 F = fc.footprint_bytes(cfg, n)
 pay_h = torch.empty(F, dtype=torch.uint8).pin_memory()
 y_h = torch.empty(n, dtype=torch.bfloat16).pin_memory()
-for sl in [1 << 20, 1 << 21, 3 << 20, 1 << 22, 6 << 20, 1 << 23]:
+SL = os.environ.get("SLICES")
+for sl in ([int(v) << 20 for v in SL.split(",")] if SL else [1 << 20, 1 << 21, 3 << 20, 1 << 22, 6 << 20, 1 << 23]):
     for _ in range(3):
         fc.roundtrip_host(xh, cfg, payload=pay_h, out=y_h, slice_elems=sl, check=False)
     torch.cuda.synchronize()
