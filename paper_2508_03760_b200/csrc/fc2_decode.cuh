@@ -213,6 +213,31 @@ __device__ __forceinline__ void run_code_floats(const uint32_t* w, uint32_t* cf)
   }
 }
 
+// Substitute the reserved values (imin first, then imax: codec.py:559-561) into
+// a lane's 32 decoded run values.  ha / hz: the slot lies in this run (ka, kz
+// run-relative).  Registers cannot be indexed by a data-dependent position, so
+// the run round-trips through the lane's 16-byte-aligned smem spill row (32
+// floats).  QUAD: only the float4 quads holding a slot make the trip, each
+// predicated on its own, so a hit lane moves 32 B each way instead of 128 B.
+template <bool QUAD>
+__device__ __forceinline__ void subst_reserved(float (&v)[32], float* spill, bool ha, int ka, float smin, bool hz,
+                                               int kz, float smax) {
+  const int qa = ha ? ka >> 2 : -1, qz = hz ? kz >> 2 : -1;
+#pragma unroll
+  for (int k = 0; k < 32; k += 4)
+    if (!QUAD || qa == k / 4 || qz == k / 4)
+      *reinterpret_cast<float4*>(spill + k) = make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]);
+  if (ha) spill[ka] = smin;
+  if (hz) spill[kz] = smax;
+#pragma unroll
+  for (int k = 0; k < 32; k += 4) {
+    if (!QUAD || qa == k / 4 || qz == k / 4) {
+      const float4 q = *reinterpret_cast<const float4*>(spill + k);
+      v[k] = q.x; v[k + 1] = q.y; v[k + 2] = q.z; v[k + 3] = q.w;
+    }
+  }
+}
+
 // Code of one element (generic path, any alignment).
 __device__ __forceinline__ uint32_t load_code1(const uint8_t* payload, int64_t n, int64_t e, int B) {
   uint32_t c = 0;

@@ -385,18 +385,8 @@ __global__ void __launch_bounds__(256, FC2_COMBINE_MINB) k_moe_combine_q(const _
           const int base = (int)(ec & (a.G - 1));
           const int ka = m.imin - (a.gshift >= 0 ? base : (int)(ec % a.G)), kz = m.imax - (a.gshift >= 0 ? base : (int)(ec % a.G));
           const bool ha = on && m.imin >= 0 && (unsigned)ka < 32u, hz = on && m.imax >= 0 && (unsigned)kz < 32u;
-          if (ha || hz) {
-#pragma unroll
-            for (int k = 0; k < 32; k += 4)
-              *reinterpret_cast<float4*>(spill + k) = make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]);
-            if (ha) spill[ka] = m.smin;
-            if (hz) spill[kz] = m.smax;
-#pragma unroll
-            for (int k = 0; k < 32; k += 4) {
-              const float4 q = *reinterpret_cast<const float4*>(spill + k);
-              v[k] = q.x; v[k + 1] = q.y; v[k + 2] = q.z; v[k + 3] = q.w;
-            }
-          }
+          // per-quad round trip at b4 / b8 as in k_reduce_run (configs[3] b4 SR: 85.7 -> 84.2 us)
+          if (ha || hz) subst_reserved<B == 4 || B == 8>(v, spill, ha, ka, m.smin, hz, kz, m.smax);
         }
       }
 #pragma unroll

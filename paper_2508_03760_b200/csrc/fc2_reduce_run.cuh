@@ -20,7 +20,8 @@
 //      stores the plane words straight to every destination (the owner's
 //      gather slot and, in the SPMD path, every peer's over NVLink).
 //
-// Measured (B200, 8 sources x 4 Mi elements, b4 SR g128): 23.9 us, ~10.6 M
+// Measured (B200, 8 sources x 4 Mi elements, b4 SR g128): 22.8 us (23.9 before the
+// per-quad spike substitution), ~10.6 M
 // warp instructions at ~1.9 IPC -- instruction-bound (profiles/r2_reduce_run_ncu_full.md).
 #pragma once
 
@@ -252,18 +253,11 @@ __global__ void __launch_bounds__(32, FC2_RUN_MINB) k_reduce_run(const __grid_co
           d[k] = __double2float_rn(__dadd_rn(__dmul_rn((double)(cf[k] & 0xFFu), s64), o64));
       }
       if constexpr (SR) {  // reserved values, imin then imax; only lanes whose run holds one
-        if (hit) {
-#pragma unroll
-          for (int k = 0; k < 32; k += 4)
-            *reinterpret_cast<float4*>(spill + k) = make_float4(d[k], d[k + 1], d[k + 2], d[k + 3]);
-          if ((unsigned)ka < 32u) spill[ka] = smin;
-          if ((unsigned)kz < 32u) spill[kz] = smax;
-#pragma unroll
-          for (int k = 0; k < 32; k += 4) {
-            const float4 q = *reinterpret_cast<const float4*>(spill + k);
-            d[k] = q.x; d[k + 1] = q.y; d[k + 2] = q.z; d[k + 3] = q.w;
-          }
-        }
+        // b4 / b8: per-quad round trip (8 sources x 4 Mi elements: b4 23.9 ->
+        // 22.8 us, b8 28.3 -> 27.0 us); b3 / b2 were slower that way (25.2 ->
+        // 26.7, 24.6 -> 24.9 us) and keep the whole-run round trip
+        if (hit)
+          subst_reserved<B == 4 || B == 8>(d, spill, (unsigned)ka < 32u, ka, smin, (unsigned)kz < 32u, kz, smax);
       }
 #pragma unroll
       for (int k = 0; k < 32; k += 2) add2(acc[k], acc[k + 1], acc[k], acc[k + 1], d[k], d[k + 1]);
