@@ -55,7 +55,8 @@ def test_two_step_matches_oracle(N, n, bits, g, sr):
     assert np.array_equal(res.outputs[0], want[0])
 
 
-@pytest.mark.parametrize("N,bits,g,sr", [(8, 4, 128, True), (4, 3, 64, True), (8, 8, 128, True), (2, 2, 32, False)])
+@pytest.mark.parametrize("N,bits,g,sr", [(8, 4, 128, True), (4, 3, 64, True), (8, 8, 128, True), (2, 2, 32, False),
+                                         (4, 4, 64, True), (3, 8, 32, True)])
 def test_two_step_stress_matches_oracle(N, bits, g, sr):
     """The stage-2 reducer on the stress mix (tests/test_gpu_codec.py): sums of
     groups from different regimes across ranks, requantized."""

@@ -41,6 +41,7 @@ def tokens_bf16(T, H, seed):
     (8, [64] * 8, 7168, 8, 256, 4, 128, True),
     (2, [20, 30], 264, 2, 8, 4, 24, True),  # generic encoder (g = 24) + unfused combine (H % 32 != 0)
     (2, [40, 9], 1024, 2, 8, 6, 32, False),
+    (2, [40, 25], 1024, 2, 8, 8, 128, True),  # b8 SR: per-quad reserved-value substitution in the combine
 ])
 @pytest.mark.parametrize("resident", ["host_f32", "cuda_bf16"])
 def test_moe_dispatch_combine_match_oracle(N, Ts, H, K, E, bits, g, sr, resident):
