@@ -257,21 +257,31 @@ __device__ __forceinline__ uint32_t pair_tie_bits(uint32_t X0, uint32_t X1, int 
 // FB = 16 tie flags with the work on the FMA pipe (the ALU pipe is the
 // encoder's bottleneck).  y + kTieShift moves the tie window frac(y) in
 // [0, 16] ulp to [0x7BF0, 0x7C00], which is exactly the set of 16-bit
-// patterns an ordered f16 compare h >= 64512 accepts (0x7C00 = +inf, NaNs and
-// negatives compare false) -- so one PRMT + one HSET2 test a pair, with no
+// patterns an ordered f16 compare h >= 65024 (0x7BF0) accepts (0x7C00 = +inf, NaNs and
+// negatives compare false) -- so one PRMT + one HFMA2.SAT (tie_ge) test a pair, with no
 // masking; exact-integer codes (frac = 0x8008) land on negative f16 and are
 // not flagged.  The 1.0 / 0.0 results are summed as r * 2^k into an f16 pair
 // that starts at 1024 (HFMA2): pair k of 8 sets bit k of the low byte of each
 // half (1024 + v, v < 256, is exact).  tie_bits16 merges the two
 // accumulators of a run into the split layout of pair_tie_bits.
 constexpr float kTieShift = 31728.0f / 65536.0f;  // 0x7BF0 ulp of 2^-16
+// 1.0 where h >= 65024 (0x7BF0) as an ordered f16 compare, else 0.0, on the
+// FMA pipe: sat(h - 64992).  Every f16 at or above 65024 is at least 32 above
+// 64992 (the ulp there is 32; the difference is exact) and saturates to 1,
+// +inf gives 1, NaN flushes to +0, and everything below 65024 gives a result
+// <= 0 that saturates to 0 (checked over all 65536 patterns).  Against an
+// HSET2 on the ALU pipe: 64 MiB b4 SR encode 20.45 -> 19.92 us, b3 SR
+// 22.6 -> 22.1 us.
+__device__ __forceinline__ __half2 tie_ge(__half2 h) {
+  return __hfma2_sat(h, __half2(__ushort_as_half(0x3C00), __ushort_as_half(0x3C00)),
+                     __half2(__ushort_as_half(0xFBEF), __ushort_as_half(0xFBEF)));  // 1.0, -64992
+}
 __device__ __forceinline__ void add2(float& r0, float& r1, float a0, float a1, float b0, float b1);
 __device__ __forceinline__ void tie_acc16(__half2& acc, float y0, float y1, int k) {
   float z0, z1;  // exact: y in [128, 256) on the 2^-16 grid, y + shift < 256
   add2(z0, z1, y0, y1, kTieShift, kTieShift);
   const uint32_t h = __byte_perm(__float_as_uint(z0), __float_as_uint(z1), 0x5410);
-  const __half2 r = __hge2(*reinterpret_cast<const __half2*>(&h), __half2(__ushort_as_half(0x7BF0), __ushort_as_half(0x7BF0)));
-  acc = __hfma2(r, __float2half2_rn((float)(1 << k)), acc);
+  acc = __hfma2(tie_ge(*reinterpret_cast<const __half2*>(&h)), __float2half2_rn((float)(1 << k)), acc);
 }
 // FB = 15 (B = 8): bit 15 of the low half is the code's LSB, so the same
 // window is tested on |h| (the f16 abs ignores bit 15); y + shift carries into
@@ -281,9 +291,7 @@ __device__ __forceinline__ void tie_acc15(__half2& acc, float y0, float y1, int 
   float z0, z1;
   add2(z0, z1, y0, y1, kTieShift15, kTieShift15);
   const uint32_t h = __byte_perm(__float_as_uint(z0), __float_as_uint(z1), 0x5410);
-  const __half2 r = __hge2(__habs2(*reinterpret_cast<const __half2*>(&h)),
-                           __half2(__ushort_as_half(0x7BF0), __ushort_as_half(0x7BF0)));
-  acc = __hfma2(r, __float2half2_rn((float)(1 << k)), acc);
+  acc = __hfma2(tie_ge(__habs2(*reinterpret_cast<const __half2*>(&h))), __float2half2_rn((float)(1 << k)), acc);
 }
 __device__ __forceinline__ uint32_t tie_bits16(const __half2 (&acc)[2]) {
   return __byte_perm(*reinterpret_cast<const uint32_t*>(&acc[0]), *reinterpret_cast<const uint32_t*>(&acc[1]),

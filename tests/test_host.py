@@ -141,3 +141,18 @@ def test_topology_json_roundtrip(tmp_path):
     assert fc.Topology.load(p) == t
     with pytest.raises(fc.ConfigError):
         fc.preset("nope")
+
+
+def test_tie_ge_saturating_form_matches_compare():
+    """fc2_common.cuh tie_ge: sat(h - 64992) in f16 (HFMA2.SAT) equals the
+    ordered compare h >= 65024 (0x7BF0) for every 16-bit pattern, NaN
+    flushing to 0 as .sat does."""
+    h = np.arange(1 << 16, dtype=np.uint32).astype(np.uint16).view(np.float16)
+    c = float(np.array([0xFBEF], dtype=np.uint16).view(np.float16)[0])
+    t = float(np.array([0x7BF0], dtype=np.uint16).view(np.float16)[0])
+    assert (c, t) == (-64992.0, 65024.0)
+    with np.errstate(all="ignore"):
+        r = (h.astype(np.float64) + c).astype(np.float16).astype(np.float64)  # one rounding, as the fma
+        sat = np.where(np.isnan(r), 0.0, np.clip(r, 0.0, 1.0))
+        ge = (h.astype(np.float64) >= t).astype(np.float64)
+    assert np.array_equal(sat, ge)
