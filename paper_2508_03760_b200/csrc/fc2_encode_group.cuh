@@ -247,7 +247,7 @@ __device__ __forceinline__ void pack_run_fb16(const uint32_t (&X)[32], uint32_t 
           const int sh = W * sl - O;
           v = sh >= 0 ? ((A & (mrep << O)) << sh) : ((A >> (-sh)) & (mrep << (W * sl)));
         }
-        word |= v;
+        word += v;  // disjoint fields: the add is the or, and folds with the shift into one IMAD (FMA pipe)
       }
       w[LaneWords<B>::base(u) + t] = word;
     }
